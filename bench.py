@@ -1,0 +1,326 @@
+#!/usr/bin/env python
+"""Throughput of the B200-native LOD diffusion step (arxiv 2110.13368 hot path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c3]
+
+One "step" = one [diffuse_decay_step; cell_sources_sinks_step] pass over the
+whole grid. Metric: voxel-substrate updates per second
+(vsu/s, FP64) and the fraction of the measured HBM roofline.
+
+Default workload at N=1 is BASELINE.json configs[2] (C3: 256^3 x 4 substrates,
+100k cells), the single-GPU LOD roofline benchmark the north_star targets;
+configs[1] (C2, 16 MB) fits in L2 and is a parity case, not a bench line.
+For N>1 (torchrun, one rank per GPU) each rank advances its own C3 replica
+(ensemble sharding, no data-path collective; "scaling": "weak").
+
+`--impl reference` times the reference's own CPU implementation (the
+unmodified sources compiled into oracle/_ref by oracle/Makefile) on this
+host's cores for the same workload; under torchrun only rank 0 runs it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "voxel-substrate diffusion updates/sec (FP64) at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "vsu/s"
+BYTES_PER_VSU_STEP = 48  # 3 sweeps x (8 B read + 8 B write), SURVEY.md §8 d2
+BYTES_PER_VSU_SWEEP = 16
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel_class):
+    """DRAM bytes per launch from the committed ncu --set full summary (or None)."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    return d.get(kernel_class)
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "50",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            time.sleep(0.06)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out = ""
+
+    def summary(self):
+        rows = [r.split(",") for r in (self.out or "").strip().splitlines() if r.count(",") >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows]
+        mx = max(float(r[2]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(float(r[3]) for r in rows)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_reference_timing(w, sample_budget_s=20.0, max_steps=None):
+    """Times the reference CPU path (oracle/_ref) on this host: all cores and one core."""
+    import oracle
+    cores = oracle.nproc()
+    out = {"kind": "reference" if oracle.reference_available() else "port", "cores": cores}
+    if not oracle.reference_available():
+        return None
+    ref = oracle.Reference(w, workers=cores)
+    t1 = ref.run(1)  # warm-up step (also sizes the sample)
+    n = max(1, min(int(sample_budget_s * 0.6 / max(t1, 1e-6)), 50 if max_steps is None else max_steps))
+    t = ref.run(n)
+    out["value"] = w.vsu_per_step * n / t
+    out["sample"] = f"{n} full steps of {w.name.split(':')[0]} on {cores} threads (reference WorkerPool parallel({cores}))"
+    ref.close()
+    ser = oracle.Reference(w, workers=0)
+    t1s = ser.run(1)
+    ns = max(1, min(int(sample_budget_s * 0.4 / max(t1s, 1e-6)), 10))
+    ts = ser.run(ns)
+    out["single_core"] = {"value": w.vsu_per_step * ns / ts, "cores": 1,
+                          "sample": f"{ns} full steps, BackendKind::serial()"}
+    ser.close()
+    return out
+
+
+def run_reference_arm(args, w):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    cfg = config_for(args, w, world)
+    if not oracle.reference_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libbiodiff_ref.so not built"}))
+        return
+    cores = oracle.nproc()
+    ref = oracle.Reference(w, workers=cores)
+    t_w = ref.run(max(1, min(args.warmup, 3)))
+    per = t_w / max(1, min(args.warmup, 3))
+    budget = 120.0
+    n = max(1, min(args.steps, int(budget / max(per, 1e-9))))
+    t = ref.run(n)
+    value = w.vsu_per_step * n / t
+    sample = (f"{n} of {args.steps} requested full steps of {w.name.split(':')[0]} on {cores} threads "
+              f"(reference WorkerPool parallel({cores}), steady_clock around the step loop)")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / n, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic, seeded (paper_2110_13368_b200/workloads.py)", "config": cfg,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    ref.close()
+    print(json.dumps(line), flush=True)
+
+
+def config_for(args, w, world):
+    return {"workload": w.name, "grid": list(w.n), "substrates": w.S, "cells": w.n_agents,
+            "dt_min": w.dt, "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+            "l2": f"field {w.voxels * w.S * 8 / 1e6:.0f} MB per replica vs 126 MB L2"
+                  + (" (inputs larger than L2)" if w.voxels * w.S * 8 > 126e6 else " (fits in L2)")}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c3", choices=["c1", "c2", "c3"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: >= 3 warm-up steps
+
+    from paper_2110_13368_b200 import workloads as W
+    w = W.CONFIGS[args.workload](args.steps)
+
+    if args.impl == "reference":
+        run_reference_arm(args, w)
+        return
+
+    world, rank, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2110_13368_b200 as B
+    from paper_2110_13368_b200.workloads import session_for as make_session
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    device = local if world > 1 else 0
+    s = make_session(w, device=device)
+    field_bytes = w.voxels * w.S * 8
+
+    # Warm-up (also instantiates graphs / loads modules).
+    s.advance(args.warmup, w.dt)
+    s.synchronize()
+    barrier()
+
+    # Timed region: exactly K steps, per-kernel CUDA events on the session stream.
+    s.set_kernel_timing(True)
+    l0 = s.launch_count()
+    with ClockSampler(device) as clk:
+        s.synchronize()
+        barrier()
+        s.event_record(0)
+        s.advance(args.steps, w.dt)
+        s.event_record(1)
+        ms = s.event_elapsed(0, 1)
+        s.synchronize()
+        barrier()
+    launches = s.launch_count() - l0
+    ktimes = s.kernel_times()
+    s.set_kernel_timing(False)
+    if dist is not None:
+        import torch
+        t = torch.tensor([ms], device=f"cuda:{device}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = w.vsu_per_step * args.steps * world / (ms / 1e3)
+
+    # Roofline of the dominant kernel (largest share of the timed region).
+    peak, peak_src = peaks()
+    sweep_classes = [c for c in ("sweep_x", "sweep_y", "sweep_z") if ktimes[c][0]]
+    dom = max(sweep_classes, key=lambda c: ktimes[c][1])
+    n_l, t_l = ktimes[dom]
+    avg_ms = t_l / n_l
+    alg_bytes = BYTES_PER_VSU_SWEEP * w.voxels * w.S
+    achieved = alg_bytes / (avg_ms / 1e3) / 1e9
+    kernel_total = sum(v[1] for v in ktimes.values())
+    step_achieved = BYTES_PER_VSU_STEP * w.vsu_per_step * args.steps / (ms / 1e3) / 1e9
+
+    # End to end through the C ABI with host buffers (pinned), strict drop-in
+    # semantics: every step uploads the field, steps once, reads it back.
+    import torch
+    host_in = torch.from_numpy(w.initial_field()).pin_memory()
+    host_out = torch.empty(w.voxels * w.S, dtype=torch.float64).pin_memory()
+    hin = host_in.numpy()
+    hout = host_out.numpy()
+    E = max(1, args.e2e_steps)
+    barrier()
+    s.event_record(2)
+    for _ in range(E):
+        s.upload_field(hin)
+        s.diffuse_decay_step()
+        s.cell_sources_sinks_step(w.dt)
+        s.download_field(hout)
+    s.event_record(3)
+    e2e_ms = s.event_elapsed(2, 3)
+    # Resident run through the same API: upload once, K steps, read back once.
+    s.event_record(4)
+    s.upload_field(hin)
+    s.advance(args.steps, w.dt)
+    s.download_field(hout)
+    s.event_record(5)
+    res_ms = s.event_elapsed(4, 5)
+    if dist is not None:
+        t = torch.tensor([e2e_ms, res_ms], device=f"cuda:{device}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms, res_ms = (float(x) for x in t.tolist())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_timing(w)
+            if cpu is not None:
+                cpu["unit"] = UNIT
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"error": str(e)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic, seeded spherical-tumour layout (paper_2110_13368_b200/workloads.py, SURVEY.md §8 d3)",
+            "config": config_for(args, w, world),
+            "roofline": {
+                "bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": ncu_traffic(dom),
+                "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_ms, "peak_source": peak_src,
+                "kernel_share_of_step": t_l / kernel_total if kernel_total else None,
+                "step": {"achieved": step_achieved, "frac": step_achieved / peak,
+                         "bytes_per_vsu": BYTES_PER_VSU_STEP},
+                "per_kernel_ms": {k: {"launches": v[0], "avg_ms": (v[1] / v[0]) if v[0] else None}
+                                  for k, v in ktimes.items()},
+            },
+            "cpu_baseline": cpu,
+            "e2e": {"value": w.vsu_per_step * E * world / (e2e_ms / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": field_bytes, "d2h_bytes_per_step": field_bytes,
+                    "steps": E, "semantics": "per step: upload field (pinned host) + step + download field"},
+            "e2e_resident": {"value": w.vsu_per_step * args.steps * world / (res_ms / 1e3), "unit": UNIT,
+                             "h2d_bytes_per_step": field_bytes / args.steps,
+                             "d2h_bytes_per_step": field_bytes / args.steps,
+                             "semantics": "upload once, advance(K), download once"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "sweep_paths": {ax: str(p) for ax, p in zip("xyz", _paths(s))},
+        }
+        print(json.dumps(line), flush=True)
+    s.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def _paths(s):
+    return [os.environ.get("BIODIFF_SWEEP_PATH", "auto")] * 3
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,173 @@
+/*
+ * biodiff_b200.h — C ABI of the B200-native LOD diffusion step.
+ *
+ * This is the "extern-C API" the reference's build declares but whose
+ * sources are absent from the snapshot (libbiodiff SHARED from capi/capi.cpp
+ * and include/biodiff/biodiff.h, /root/reference/proj/src/CMakeLists.txt:17-23).
+ * Every entry point below names the reference C++ interface it stands in for.
+ *
+ * Conventions:
+ *   - Every function returns an int status; no exception crosses the ABI.
+ *       BIODIFF_OK          0
+ *       BIODIFF_ERR_CONFIG  1  config_error            (errors.hpp:9-12)
+ *       BIODIFF_ERR_STATE   2  state_error, std::invalid_argument, std::domain_error,
+ *                              std::out_of_range, CUDA failures (errors.hpp:19-22)
+ *       BIODIFF_ERR_IO      4  io_error                (errors.hpp:14-17)
+ *     biodiff_last_error() returns the message of the calling thread's last failure.
+ *   - Host arrays are caller-owned and copied (or read) during the call; the
+ *     session owns all device memory. Plain pointers and sizes only.
+ *   - Field layout is the reference's (mesh.hpp:59-61):
+ *       values[(i + j*nx + k*nx*ny)*S + s], FP64.
+ *   - One host thread drives a session at a time (backend.hpp:44-45).
+ *   - The CUDA path is the only compute path: there is no CPU fallback. A
+ *     session cannot be created without a visible sm_100 device.
+ */
+#ifndef BIODIFF_B200_H
+#define BIODIFF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BIODIFF_OK 0
+#define BIODIFF_ERR_CONFIG 1
+#define BIODIFF_ERR_STATE 2
+#define BIODIFF_ERR_IO 4
+
+#define BIODIFF_AXIS_X 0
+#define BIODIFF_AXIS_Y 1
+#define BIODIFF_AXIS_Z 2
+
+/* CartesianMesh (mesh.hpp:17-57). */
+typedef struct biodiff_mesh {
+    double x_min, x_max, y_min, y_max, z_min, z_max;
+    double dx, dy, dz;
+    int32_t nx, ny, nz;
+} biodiff_mesh;
+
+typedef struct biodiff_session biodiff_session;
+
+/* ---- library / host-side helpers (no device work) ---------------------- */
+
+/* Message of this thread's last failed call ("" if none). */
+const char* biodiff_last_error(void);
+
+/* ABI version: major*10000 + minor*100 + patch. */
+int32_t biodiff_version(void);
+
+/* CartesianMesh::from_bounds (mesh.hpp:28-31, mesh.cpp:174-206). */
+int biodiff_mesh_from_bounds(double x_min, double x_max, double y_min, double y_max, double z_min, double z_max,
+                             double dx, double dy, double dz, biodiff_mesh* out);
+
+/* CartesianMesh::nearest_voxel (mesh.hpp:42-45, mesh.cpp:234-250). */
+int biodiff_nearest_voxel(const biodiff_mesh* mesh, const double position[3], int64_t* voxel);
+
+/* precompute_thomas_coefficients (solver.hpp:35-40, solver.cpp:129-179) for
+ * one axis: off_diag[S], denom_inv[n*S], c_back[n*S] with n the axis length.
+ * D, lambda: per-substrate diffusion coefficient and decay rate. */
+int biodiff_precompute_thomas(const biodiff_mesh* mesh, int32_t substrates, const double* diffusion,
+                              const double* decay, double dt, int32_t axis, int32_t dims, double* off_diag,
+                              double* denom_inv, double* c_back);
+
+/* Number of usable sm_100 devices (0 when none). */
+int biodiff_device_count(int32_t* count);
+
+/* ---- sessions: device-resident Microenvironment + WorkerPool stand-in --- */
+
+/* Creates a session bound to `device`, with a device-resident DensityField of
+ * mesh.voxel_count()*substrates values (zero-filled). The session is the
+ * execution-strategy plugin that replaces WorkerPool& (backend.hpp:34-66,
+ * select_backend SPEC.md:303-311). */
+int biodiff_session_create(const biodiff_mesh* mesh, int32_t substrates, int32_t device, biodiff_session** out);
+int biodiff_session_destroy(biodiff_session* session);
+
+/* SolverWorkspaces::build (solver.hpp:66-67, solver.cpp:359-369): builds the
+ * x/y/z workspaces on the host exactly as the reference does and uploads
+ * their bits. D, lambda: per-substrate arrays of length S. */
+int biodiff_set_substrates(biodiff_session* session, const double* diffusion, const double* decay, double dt);
+
+/* Upload of one prebuilt SolverWorkspace (solver.hpp:24-33): off_diag[S],
+ * denom_inv[n*S], c_back[n*S]. `dims` and `dt` must agree across axes. */
+int biodiff_set_workspace(biodiff_session* session, int32_t axis, int32_t n, int32_t dims, double dt,
+                          const double* off_diag, const double* denom_inv, const double* c_back);
+
+/* Replaces the DirichletMap (mesh.hpp:124-141) with `count` entries:
+ * voxel[count], mask[count*S] (nonzero = clamped), values[count*S]. Entries
+ * may come in any order; duplicates merge as DirichletMap::add does
+ * (mesh.cpp:300-321: later adds win per masked substrate). */
+int biodiff_set_dirichlet(biodiff_session* session, int64_t count, const int64_t* voxel, const uint8_t* mask,
+                          const double* values);
+
+/* Replaces the AgentPopulation (agents.hpp:389-424): validates as the
+ * reference ctor does (agents.cpp:456-479) and builds the (voxel, id)
+ * grouping on the host (agents.cpp:492-509). positions[3n], volume[n],
+ * secretion/uptake/saturation[n*S]. */
+int biodiff_set_agents(biodiff_session* session, int64_t n, const int64_t* ids, const double* positions,
+                       const double* volume, const double* secretion, const double* uptake,
+                       const double* saturation);
+
+/* Group count of the current agent grouping and a copy of it:
+ * group_voxel[G], group_offsets[G+1], order[n] (agent indices in the
+ * caller's order) — AgentPopulation::grouping() (agents.hpp:402-406). */
+int biodiff_agent_grouping(biodiff_session* session, int64_t* groups, int64_t* group_voxel,
+                           int64_t* group_offsets, int64_t* order);
+
+/* Host <-> device copies of the DensityField values (a1 layout). */
+int biodiff_upload_field(biodiff_session* session, const double* values, int64_t count);
+int biodiff_download_field(biodiff_session* session, double* values, int64_t count);
+
+/* diffusion_sweep (solver.hpp:51-52, solver.cpp:330-347) along one axis. */
+int biodiff_diffusion_sweep(biodiff_session* session, int32_t axis);
+
+/* apply_dirichlet_conditions (solver.hpp:55, solver.cpp:349-357). */
+int biodiff_apply_dirichlet(biodiff_session* session);
+
+/* diffuse_decay_step (solver.hpp:72-73, solver.cpp:371-381): x, y, z sweeps
+ * (active axes) with the Dirichlet clamp fused into the last sweep. */
+int biodiff_diffuse_decay_step(biodiff_session* session);
+
+/* cell_sources_sinks_step (agents.hpp:431-432, agents.cpp:511-548). */
+int biodiff_cell_sources_sinks_step(biodiff_session* session, double dt);
+
+/* The engine's inner loop: steps x [diffuse_decay_step;
+ * cell_sources_sinks_step(dt)]; sources are skipped when with_sources == 0.
+ * dt must equal the workspace dt. Runs asynchronously on the session stream
+ * (captured once into a CUDA graph per (steps-chunk, with_sources)). */
+int biodiff_advance(biodiff_session* session, int64_t steps, double dt, int32_t with_sources);
+
+/* Blocks until all queued work of the session is done. */
+int biodiff_synchronize(biodiff_session* session);
+
+/* The session's CUDA stream (a cudaStream_t), for callers that want to
+ * order their own work or events against it. */
+int biodiff_session_stream(biodiff_session* session, void** stream);
+
+/* Kernel-level timing: when enabled, every kernel launch on the session is
+ * bracketed by CUDA events on the session stream; biodiff_kernel_times
+ * returns, per kernel class, the number of launches and the summed device
+ * milliseconds since the last reset. Classes: 0 sweep_x, 1 sweep_y,
+ * 2 sweep_z, 3 dirichlet, 4 sources. Returns the number of classes in *n. */
+int biodiff_set_kernel_timing(biodiff_session* session, int32_t enabled);
+int biodiff_kernel_times(biodiff_session* session, int32_t* n, int64_t* launches, double* milliseconds);
+
+/* Records CUDA event `slot` (0..15) on the session stream / returns the
+ * device milliseconds between two recorded slots (synchronizes on `end`). */
+int biodiff_event_record(biodiff_session* session, int32_t slot);
+int biodiff_event_elapsed(biodiff_session* session, int32_t begin, int32_t end, double* milliseconds);
+
+/* Number of kernel launches issued by the session since creation. */
+int biodiff_launch_count(biodiff_session* session, int64_t* launches);
+
+/* Device-side cross_check (validation.hpp:288-292, validation.cpp:112-137)
+ * of the session field against a host field: max_abs, max_rel, worst value
+ * index, pass (|a-b| <= abs_tol + rel_tol*max(|a|,|b|) everywhere). */
+int biodiff_cross_check(biodiff_session* session, const double* other, int64_t count, double abs_tol,
+                        double rel_tol, double* max_abs, double* max_rel, int64_t* worst_index, int32_t* pass);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BIODIFF_B200_H */

@@ -1,0 +1,323 @@
+// ref_shim.cpp — TEST INFRASTRUCTURE ONLY.
+//
+// An extern "C" driver over the UNMODIFIED reference sources, compiled where
+// they lie under /root/reference/proj/src/core by oracle/Makefile into
+// oracle/_ref/libbiodiff_ref.so. It builds reference objects programmatically
+// (mirroring build_microenvironment config.cpp:494-527 and build_agents
+// config.cpp:529-566, since config.cpp needs the absent Boost) and drives the
+// reference's own entry points:
+//   SolverWorkspaces::build        solver.cpp:359-369
+//   diffusion_sweep                solver.cpp:330-347
+//   apply_dirichlet_conditions     solver.cpp:349-357
+//   diffuse_decay_step             solver.cpp:371-381
+//   cell_sources_sinks_step        agents.cpp:511-548
+//   AgentPopulation (grouping)     agents.cpp:448-509
+//   run_convergence_test           validation.cpp:65-110
+//   run_dirichlet_mutant_check     validation.cpp:274-287
+// The step loop [diffuse_decay_step; cell_sources_sinks_step] is SPEC.md:297
+// (the engine itself is absent from the snapshot).
+//
+// Only tests/ and bench.py (reference arm / cpu_baseline) load this library.
+#include "core/agents.hpp"
+#include "core/backend.hpp"
+#include "core/errors.hpp"
+#include "core/mesh.hpp"
+#include "core/solver.hpp"
+#include "core/validation.hpp"
+
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+using namespace biodiff;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f)
+{
+    try {
+        f();
+        return 0;
+    } catch (const config_error& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const io_error& e) {
+        g_err = e.what();
+        return 4;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 2;
+    }
+}
+
+struct RefCtx {
+    Microenvironment env;
+    std::optional<SolverWorkspaces> ws;
+    AgentPopulation agents;
+    std::unique_ptr<WorkerPool> pool;
+};
+
+} // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// Builds a Microenvironment. When `staged` is nonzero the reference's own
+// Microenvironment::create (nested-vector staging, mesh.cpp:335-357) is used;
+// otherwise the public fields are filled directly (SURVEY.md §7 hard part 8),
+// which yields the identical field without the 3x staging memory.
+int ref_create(const double* bounds, const double* spacing, int S, const double* D, const double* lambda,
+               const double* ic, int workers, int staged, void** out)
+{
+    return guarded([&] {
+        auto ctx = std::make_unique<RefCtx>();
+        const CartesianMesh mesh = CartesianMesh::from_bounds(bounds[0], bounds[1], bounds[2], bounds[3], bounds[4],
+                                                              bounds[5], spacing[0], spacing[1], spacing[2]);
+        std::vector<SubstrateParams> params;
+        for (int s = 0; s < S; ++s) params.push_back({"s" + std::to_string(s), D[s], lambda[s], ic[s]});
+        if (staged) {
+            ctx->env = Microenvironment::create(mesh, std::move(params));
+        } else {
+            ctx->env.mesh = mesh;
+            ctx->env.substrates = std::move(params);
+            ctx->env.field.substrates = S;
+            ctx->env.field.values.resize(static_cast<std::size_t>(mesh.voxel_count()) * S);
+            for (std::size_t v = 0; v < static_cast<std::size_t>(mesh.voxel_count()); ++v)
+                for (int s = 0; s < S; ++s) ctx->env.field.values[v * S + s] = ic[s];
+        }
+        ctx->pool = std::make_unique<WorkerPool>(workers <= 0 ? BackendKind::serial()
+                                                              : BackendKind::make_parallel(workers));
+        *out = ctx.release();
+    });
+}
+
+void ref_destroy(void* h) { delete static_cast<RefCtx*>(h); }
+
+int ref_mesh_dims(void* h, int* n)
+{
+    auto* c = static_cast<RefCtx*>(h);
+    n[0] = c->env.mesh.nx;
+    n[1] = c->env.mesh.ny;
+    n[2] = c->env.mesh.nz;
+    return 0;
+}
+
+int ref_set_field(void* h, const double* v, int64_t count)
+{
+    return guarded([&] {
+        auto* c = static_cast<RefCtx*>(h);
+        if (static_cast<std::size_t>(count) != c->env.field.values.size())
+            throw std::invalid_argument("field size mismatch");
+        std::memcpy(c->env.field.values.data(), v, sizeof(double) * count);
+    });
+}
+
+int ref_get_field(void* h, double* v, int64_t count)
+{
+    return guarded([&] {
+        auto* c = static_cast<RefCtx*>(h);
+        if (static_cast<std::size_t>(count) != c->env.field.values.size())
+            throw std::invalid_argument("field size mismatch");
+        std::memcpy(v, c->env.field.values.data(), sizeof(double) * count);
+    });
+}
+
+// DirichletMap::add (mesh.cpp:300-321), one call per entry in caller order.
+int ref_add_dirichlet(void* h, int64_t count, const int64_t* voxel, const uint8_t* mask, const double* values)
+{
+    return guarded([&] {
+        auto* c = static_cast<RefCtx*>(h);
+        const int S = c->env.substrate_count();
+        for (int64_t e = 0; e < count; ++e)
+            c->env.dirichlet.add(voxel[e], std::vector<std::uint8_t>(mask + e * S, mask + (e + 1) * S),
+                                 std::vector<double>(values + e * S, values + (e + 1) * S),
+                                 c->env.mesh.voxel_count(), S);
+    });
+}
+
+// Reads back the canonical (sorted, merged) Dirichlet entries.
+int64_t ref_dirichlet_size(void* h) { return static_cast<int64_t>(static_cast<RefCtx*>(h)->env.dirichlet.size()); }
+
+int ref_get_dirichlet(void* h, int64_t* voxel, uint8_t* mask, double* values)
+{
+    auto* c = static_cast<RefCtx*>(h);
+    const int S = c->env.substrate_count();
+    int64_t e = 0;
+    for (const auto& d : c->env.dirichlet.entries()) {
+        voxel[e] = d.voxel;
+        for (int s = 0; s < S; ++s) {
+            mask[e * S + s] = d.mask[s];
+            values[e * S + s] = d.values[s];
+        }
+        ++e;
+    }
+    return 0;
+}
+
+// Boundary clamp exactly as build_microenvironment (config.cpp:506-525).
+int ref_add_boundary_dirichlet(void* h, const uint8_t* mask, const double* values)
+{
+    return guarded([&] {
+        auto* c = static_cast<RefCtx*>(h);
+        const auto& mesh = c->env.mesh;
+        const int S = c->env.substrate_count();
+        std::vector<std::uint8_t> m(mask, mask + S);
+        std::vector<double> v(values, values + S);
+        for (int k = 0; k < mesh.nz; ++k)
+            for (int j = 0; j < mesh.ny; ++j)
+                for (int i = 0; i < mesh.nx; ++i)
+                    if (mesh.is_boundary_voxel(i, j, k))
+                        c->env.dirichlet.add(mesh.voxel_index(i, j, k), m, v, mesh.voxel_count(), S);
+    });
+}
+
+// AgentPopulation ctor (agents.cpp:448-454): validate + grouping.
+int ref_set_agents(void* h, int64_t n, const int64_t* ids, const double* pos, const double* volume,
+                   const double* secretion, const double* uptake, const double* saturation)
+{
+    return guarded([&] {
+        auto* c = static_cast<RefCtx*>(h);
+        const int S = c->env.substrate_count();
+        std::vector<CellAgent> agents;
+        agents.reserve(static_cast<std::size_t>(n));
+        for (int64_t a = 0; a < n; ++a) {
+            CellAgent ag;
+            ag.id = ids[a];
+            ag.position = {pos[3 * a], pos[3 * a + 1], pos[3 * a + 2]};
+            ag.volume = volume[a];
+            ag.secretion_rates.assign(secretion + a * S, secretion + (a + 1) * S);
+            ag.uptake_rates.assign(uptake + a * S, uptake + (a + 1) * S);
+            ag.saturation_densities.assign(saturation + a * S, saturation + (a + 1) * S);
+            agents.push_back(std::move(ag));
+        }
+        c->agents = AgentPopulation(std::move(agents), c->env.mesh, S);
+    });
+}
+
+int64_t ref_group_count(void* h) { return static_cast<int64_t>(static_cast<RefCtx*>(h)->agents.grouping().size()); }
+
+int ref_get_grouping(void* h, int64_t* group_voxel, int64_t* group_offsets, int64_t* order)
+{
+    auto* c = static_cast<RefCtx*>(h);
+    int64_t g = 0, m = 0;
+    for (const auto& [voxel, idxs] : c->agents.grouping()) {
+        group_voxel[g] = voxel;
+        group_offsets[g] = m;
+        for (std::size_t i : idxs) order[m++] = static_cast<int64_t>(i);
+        ++g;
+    }
+    group_offsets[g] = m;
+    return 0;
+}
+
+int ref_build_workspaces(void* h, double dt)
+{
+    return guarded([&] {
+        auto* c = static_cast<RefCtx*>(h);
+        c->ws = SolverWorkspaces::build(c->env.mesh, c->env.substrates, dt);
+    });
+}
+
+// Copies one axis workspace; returns 3 if the axis is inactive.
+int ref_get_workspace(void* h, int axis, double* off_diag, double* denom_inv, double* c_back, int* dims)
+{
+    auto* c = static_cast<RefCtx*>(h);
+    if (!c->ws) return 2;
+    const std::optional<SolverWorkspace>& w = axis == 0 ? c->ws->x : axis == 1 ? c->ws->y : c->ws->z;
+    if (!w) return 3;
+    std::memcpy(off_diag, w->off_diag.data(), sizeof(double) * w->off_diag.size());
+    std::memcpy(denom_inv, w->denom_inv.data(), sizeof(double) * w->denom_inv.size());
+    std::memcpy(c_back, w->c_back.data(), sizeof(double) * w->c_back.size());
+    *dims = w->dims;
+    return 0;
+}
+
+int ref_sweep(void* h, int axis)
+{
+    return guarded([&] {
+        auto* c = static_cast<RefCtx*>(h);
+        if (!c->ws) throw state_error("workspaces not built");
+        const std::optional<SolverWorkspace>& w = axis == 0 ? c->ws->x : axis == 1 ? c->ws->y : c->ws->z;
+        if (!w) throw state_error("axis not active");
+        diffusion_sweep(c->env.field, c->env.mesh, *w, *c->pool);
+    });
+}
+
+int ref_apply_dirichlet(void* h)
+{
+    return guarded([&] {
+        auto* c = static_cast<RefCtx*>(h);
+        apply_dirichlet_conditions(c->env.field, c->env.dirichlet);
+    });
+}
+
+int ref_diffuse_decay_step(void* h)
+{
+    return guarded([&] {
+        auto* c = static_cast<RefCtx*>(h);
+        if (!c->ws) throw state_error("workspaces not built");
+        diffuse_decay_step(c->env, *c->ws, *c->pool);
+    });
+}
+
+int ref_sources_step(void* h, double dt)
+{
+    return guarded([&] {
+        auto* c = static_cast<RefCtx*>(h);
+        cell_sources_sinks_step(c->env.field, c->agents, c->env.mesh, dt, *c->pool);
+    });
+}
+
+// The SPEC.md:297 inner loop: steps x [diffuse_decay_step; cell_sources_sinks_step].
+// *seconds receives the steady_clock time of the loop alone.
+int ref_run(void* h, int64_t steps, double dt, int with_sources, double* seconds)
+{
+    return guarded([&] {
+        auto* c = static_cast<RefCtx*>(h);
+        if (!c->ws) c->ws = SolverWorkspaces::build(c->env.mesh, c->env.substrates, dt);
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int64_t s = 0; s < steps; ++s) {
+            diffuse_decay_step(c->env, *c->ws, *c->pool);
+            if (with_sources) cell_sources_sinks_step(c->env.field, c->agents, c->env.mesh, dt, *c->pool);
+        }
+        const auto t1 = std::chrono::steady_clock::now();
+        if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+    });
+}
+
+// Method 1 (validation.cpp:65-110). kind 0 temporal, 1 spatial.
+int ref_convergence(int kind, int levels, double* order, double* steps, double* errors, int* pass)
+{
+    return guarded([&] {
+        const ConvergenceReport r =
+            run_convergence_test(kind == 0 ? RefineKind::temporal : RefineKind::spatial, levels);
+        *order = r.fitted_order;
+        for (std::size_t i = 0; i < r.points.size(); ++i) {
+            steps[i] = r.points[i].step;
+            errors[i] = r.points[i].linf_error;
+        }
+        *pass = r.pass ? 1 : 0;
+    });
+}
+
+// Method 3 mutant (validation.cpp:274-287): flags = {clean, crosscheck, table}.
+int ref_mutant_check(int* flags)
+{
+    return guarded([&] {
+        const MutantCheckReport r = run_dirichlet_mutant_check();
+        flags[0] = r.clean_reproducible;
+        flags[1] = r.crosscheck_detected;
+        flags[2] = r.table_detected;
+    });
+}
+
+} // extern "C"

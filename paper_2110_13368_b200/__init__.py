@@ -1,0 +1,356 @@
+"""B200-native LOD diffusion step (arxiv 2110.13368 hot path).
+
+Python binding of the C ABI in ``include/biodiff_b200.h`` (ctypes over the
+in-tree ``_lib/libbiodiff_b200.so``). The compute path is the CUDA library
+only: importing works without a GPU (for the host helpers), but creating a
+:class:`Session` needs an sm_100 device and fails loudly otherwise — there
+is no CPU fallback.
+
+The names mirror the reference's C++ API (/root/reference/proj/src/core):
+``diffuse_decay_step`` (solver.hpp:72), ``cell_sources_sinks_step``
+(agents.hpp:431), ``diffusion_sweep`` (solver.hpp:51),
+``apply_dirichlet_conditions`` (solver.hpp:55),
+``precompute_thomas_coefficients`` (solver.hpp:38), ``cross_check``
+(validation.hpp:291), with errors raised as the reference's exception
+categories (errors.hpp:9-24).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+__all__ = [
+    "LIB_PATH", "lib", "BiodiffError", "ConfigError", "StateError", "IOError_",
+    "Mesh", "Session", "mesh_from_bounds", "nearest_voxel", "precompute_thomas_coefficients",
+    "device_count", "AXIS_X", "AXIS_Y", "AXIS_Z", "KERNEL_CLASSES",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libbiodiff_b200.so")
+
+AXIS_X, AXIS_Y, AXIS_Z = 0, 1, 2
+KERNEL_CLASSES = ("sweep_x", "sweep_y", "sweep_z", "dirichlet", "sources")
+
+
+class BiodiffError(RuntimeError):
+    code = 2
+
+
+class ConfigError(BiodiffError):
+    """config_error (errors.hpp:9-12), status 1."""
+    code = 1
+
+
+class StateError(BiodiffError):
+    """state_error / argument / domain / CUDA errors (errors.hpp:19-22), status 2."""
+    code = 2
+
+
+class IOError_(BiodiffError):
+    """io_error (errors.hpp:14-17), status 4."""
+    code = 4
+
+
+class Mesh(ctypes.Structure):
+    """CartesianMesh (mesh.hpp:17-57) as the C ABI's biodiff_mesh."""
+
+    _fields_ = [
+        ("x_min", ctypes.c_double), ("x_max", ctypes.c_double),
+        ("y_min", ctypes.c_double), ("y_max", ctypes.c_double),
+        ("z_min", ctypes.c_double), ("z_max", ctypes.c_double),
+        ("dx", ctypes.c_double), ("dy", ctypes.c_double), ("dz", ctypes.c_double),
+        ("nx", ctypes.c_int32), ("ny", ctypes.c_int32), ("nz", ctypes.c_int32),
+    ]
+
+    @property
+    def shape(self):
+        return (self.nx, self.ny, self.nz)
+
+    @property
+    def voxel_count(self) -> int:
+        return int(self.nx) * int(self.ny) * int(self.nz)
+
+    @property
+    def voxel_volume(self) -> float:
+        return self.dx * self.dy * self.dz
+
+    def bounds(self):
+        return (self.x_min, self.x_max, self.y_min, self.y_max, self.z_min, self.z_max)
+
+    def __repr__(self):
+        return f"Mesh({self.nx}x{self.ny}x{self.nz}, h=({self.dx},{self.dy},{self.dz}))"
+
+
+_P = ctypes.POINTER
+_d = ctypes.c_double
+_i32 = ctypes.c_int32
+_i64 = ctypes.c_int64
+_vp = ctypes.c_void_p
+
+_SIGNATURES = {
+    "biodiff_last_error": (ctypes.c_char_p, []),
+    "biodiff_version": (_i32, []),
+    "biodiff_mesh_from_bounds": (ctypes.c_int, [_d] * 9 + [_P(Mesh)]),
+    "biodiff_nearest_voxel": (ctypes.c_int, [_P(Mesh), _P(_d), _P(_i64)]),
+    "biodiff_precompute_thomas": (ctypes.c_int, [_P(Mesh), _i32, _P(_d), _P(_d), _d, _i32, _i32, _P(_d), _P(_d), _P(_d)]),
+    "biodiff_device_count": (ctypes.c_int, [_P(_i32)]),
+    "biodiff_session_create": (ctypes.c_int, [_P(Mesh), _i32, _i32, _P(_vp)]),
+    "biodiff_session_destroy": (ctypes.c_int, [_vp]),
+    "biodiff_set_substrates": (ctypes.c_int, [_vp, _P(_d), _P(_d), _d]),
+    "biodiff_set_workspace": (ctypes.c_int, [_vp, _i32, _i32, _i32, _d, _P(_d), _P(_d), _P(_d)]),
+    "biodiff_set_dirichlet": (ctypes.c_int, [_vp, _i64, _P(_i64), _P(ctypes.c_uint8), _P(_d)]),
+    "biodiff_set_agents": (ctypes.c_int, [_vp, _i64, _P(_i64), _P(_d), _P(_d), _P(_d), _P(_d), _P(_d)]),
+    "biodiff_agent_grouping": (ctypes.c_int, [_vp, _P(_i64), _P(_i64), _P(_i64), _P(_i64)]),
+    "biodiff_upload_field": (ctypes.c_int, [_vp, _P(_d), _i64]),
+    "biodiff_download_field": (ctypes.c_int, [_vp, _P(_d), _i64]),
+    "biodiff_diffusion_sweep": (ctypes.c_int, [_vp, _i32]),
+    "biodiff_apply_dirichlet": (ctypes.c_int, [_vp]),
+    "biodiff_diffuse_decay_step": (ctypes.c_int, [_vp]),
+    "biodiff_cell_sources_sinks_step": (ctypes.c_int, [_vp, _d]),
+    "biodiff_advance": (ctypes.c_int, [_vp, _i64, _d, _i32]),
+    "biodiff_synchronize": (ctypes.c_int, [_vp]),
+    "biodiff_session_stream": (ctypes.c_int, [_vp, _P(_vp)]),
+    "biodiff_set_kernel_timing": (ctypes.c_int, [_vp, _i32]),
+    "biodiff_kernel_times": (ctypes.c_int, [_vp, _P(_i32), _P(_i64), _P(_d)]),
+    "biodiff_event_record": (ctypes.c_int, [_vp, _i32]),
+    "biodiff_event_elapsed": (ctypes.c_int, [_vp, _i32, _i32, _P(_d)]),
+    "biodiff_launch_count": (ctypes.c_int, [_vp, _P(_i64)]),
+    "biodiff_cross_check": (ctypes.c_int, [_vp, _P(_d), _i64, _d, _d, _P(_d), _P(_d), _P(_i64), _P(_i32)]),
+}
+
+EXPORTED_SYMBOLS = tuple(_SIGNATURES)
+
+_lib: Optional[ctypes.CDLL] = None
+
+
+def lib() -> ctypes.CDLL:
+    """Loads the in-tree CUDA library (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `make -C paper_2110_13368_b200` "
+                "(or __graft_entry__.build()); there is no CPU fallback")
+        handle = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def _check(status: int):
+    if status == 0:
+        return
+    msg = lib().biodiff_last_error().decode(errors="replace")
+    cls = {1: ConfigError, 2: StateError, 4: IOError_}.get(status, BiodiffError)
+    raise cls(msg)
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(_P(_d))
+
+
+def _f64(a, n=None) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if n is not None and a.size != n:
+        raise ValueError(f"expected {n} values, got {a.size}")
+    return a
+
+
+def mesh_from_bounds(x_min, x_max, y_min, y_max, z_min, z_max, dx, dy, dz) -> Mesh:
+    """CartesianMesh::from_bounds (mesh.cpp:174-206)."""
+    m = Mesh()
+    _check(lib().biodiff_mesh_from_bounds(x_min, x_max, y_min, y_max, z_min, z_max, dx, dy, dz, ctypes.byref(m)))
+    return m
+
+
+def nearest_voxel(mesh: Mesh, position) -> int:
+    """CartesianMesh::nearest_voxel (mesh.cpp:234-250)."""
+    p = _f64(position, 3)
+    out = _i64()
+    _check(lib().biodiff_nearest_voxel(ctypes.byref(mesh), _dptr(p), ctypes.byref(out)))
+    return int(out.value)
+
+
+def precompute_thomas_coefficients(mesh: Mesh, diffusion, decay, dt: float, axis: int, dims: int):
+    """precompute_thomas_coefficients (solver.cpp:129-179) -> (off_diag[S], denom_inv[n,S], c_back[n,S])."""
+    D = _f64(diffusion)
+    L = _f64(decay, D.size)
+    S = D.size
+    n = (mesh.nx, mesh.ny, mesh.nz)[axis]
+    q = np.zeros(S)
+    dinv = np.zeros(n * S)
+    cb = np.zeros(n * S)
+    _check(lib().biodiff_precompute_thomas(ctypes.byref(mesh), S, _dptr(D), _dptr(L), dt, axis, dims,
+                                           _dptr(q), _dptr(dinv), _dptr(cb)))
+    return q, dinv.reshape(n, S), cb.reshape(n, S)
+
+
+def device_count() -> int:
+    n = _i32()
+    _check(lib().biodiff_device_count(ctypes.byref(n)))
+    return int(n.value)
+
+
+@dataclass
+class CrossCheckReport:
+    """validation.hpp:279-286."""
+    max_abs: float
+    max_rel: float
+    worst_value_index: int
+    worst_voxel: int
+    worst_substrate: int
+    passed: bool
+
+
+class Session:
+    """A device-resident Microenvironment plus the execution strategy that
+    replaces WorkerPool& (backend.hpp:34). Mirrors the reference entry
+    points; the field stays on the device until :meth:`download_field`."""
+
+    def __init__(self, mesh: Mesh, substrates: int, device: int = 0):
+        self.mesh = mesh
+        self.S = int(substrates)
+        h = _vp()
+        _check(lib().biodiff_session_create(ctypes.byref(mesh), self.S, device, ctypes.byref(h)))
+        self._h = h
+
+    # -- lifetime -------------------------------------------------------
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().biodiff_session_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def value_count(self) -> int:
+        return self.mesh.voxel_count * self.S
+
+    # -- set-up ---------------------------------------------------------
+    def set_substrates(self, diffusion, decay, dt: float):
+        """SolverWorkspaces::build (solver.cpp:359-369) + upload."""
+        _check(lib().biodiff_set_substrates(self._h, _dptr(_f64(diffusion, self.S)), _dptr(_f64(decay, self.S)), dt))
+
+    def set_workspace(self, axis: int, dims: int, dt: float, off_diag, denom_inv, c_back):
+        n = (self.mesh.nx, self.mesh.ny, self.mesh.nz)[axis]
+        _check(lib().biodiff_set_workspace(self._h, axis, n, dims, dt, _dptr(_f64(off_diag, self.S)),
+                                           _dptr(_f64(denom_inv, n * self.S)), _dptr(_f64(c_back, n * self.S))))
+
+    def set_dirichlet(self, voxels, mask, values):
+        """DirichletMap entries (mesh.hpp:113-141); add-merge semantics."""
+        v = np.ascontiguousarray(np.asarray(voxels, dtype=np.int64).ravel())
+        m = np.ascontiguousarray(np.asarray(mask, dtype=np.uint8).reshape(v.size * self.S))
+        x = _f64(values, v.size * self.S)
+        _check(lib().biodiff_set_dirichlet(self._h, v.size, v.ctypes.data_as(_P(_i64)),
+                                           m.ctypes.data_as(_P(ctypes.c_uint8)), _dptr(x)))
+
+    def set_agents(self, ids, positions, volume, secretion, uptake, saturation):
+        """AgentPopulation (agents.cpp:448-509): validate + (voxel, id) grouping."""
+        ids = np.ascontiguousarray(np.asarray(ids, dtype=np.int64).ravel())
+        n = ids.size
+        self._n_agents = n
+        _check(lib().biodiff_set_agents(
+            self._h, n, ids.ctypes.data_as(_P(_i64)), _dptr(_f64(positions, 3 * n)), _dptr(_f64(volume, n)),
+            _dptr(_f64(secretion, n * self.S)), _dptr(_f64(uptake, n * self.S)), _dptr(_f64(saturation, n * self.S))))
+
+    def agent_grouping(self):
+        g = _i64()
+        _check(lib().biodiff_agent_grouping(self._h, ctypes.byref(g), None, None, None))
+        G = int(g.value)
+        gv = np.zeros(G, np.int64)
+        go = np.zeros(G + 1, np.int64)
+        # order length = total agents = go[-1]; query with a generous buffer first
+        order = np.zeros(max(1, self._agent_capacity(G)), np.int64)
+        _check(lib().biodiff_agent_grouping(self._h, ctypes.byref(g), gv.ctypes.data_as(_P(_i64)),
+                                            go.ctypes.data_as(_P(_i64)), order.ctypes.data_as(_P(_i64))))
+        return gv, go, order[: go[-1]]
+
+    def _agent_capacity(self, G):
+        return getattr(self, "_n_agents", 0)
+
+    # -- field ----------------------------------------------------------
+    def upload_field(self, values):
+        a = _f64(values, self.value_count)
+        _check(lib().biodiff_upload_field(self._h, _dptr(a), a.size))
+
+    def download_field(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        if out is None:
+            out = np.empty(self.value_count, np.float64)
+        _check(lib().biodiff_download_field(self._h, _dptr(out), out.size))
+        return out
+
+    # -- the hot path ---------------------------------------------------
+    def diffusion_sweep(self, axis: int):
+        _check(lib().biodiff_diffusion_sweep(self._h, axis))
+
+    def apply_dirichlet_conditions(self):
+        _check(lib().biodiff_apply_dirichlet(self._h))
+
+    def diffuse_decay_step(self):
+        _check(lib().biodiff_diffuse_decay_step(self._h))
+
+    def cell_sources_sinks_step(self, dt: float):
+        _check(lib().biodiff_cell_sources_sinks_step(self._h, dt))
+
+    def advance(self, steps: int, dt: float, with_sources: bool = True):
+        _check(lib().biodiff_advance(self._h, int(steps), dt, 1 if with_sources else 0))
+
+    def synchronize(self):
+        _check(lib().biodiff_synchronize(self._h))
+
+    def stream(self) -> int:
+        s = _vp()
+        _check(lib().biodiff_session_stream(self._h, ctypes.byref(s)))
+        return int(s.value or 0)
+
+    # -- instrumentation ------------------------------------------------
+    def set_kernel_timing(self, enabled: bool):
+        _check(lib().biodiff_set_kernel_timing(self._h, 1 if enabled else 0))
+
+    def kernel_times(self):
+        n = _i32()
+        _check(lib().biodiff_kernel_times(self._h, ctypes.byref(n), None, None))
+        launches = np.zeros(n.value, np.int64)
+        ms = np.zeros(n.value, np.float64)
+        _check(lib().biodiff_kernel_times(self._h, ctypes.byref(n), launches.ctypes.data_as(_P(_i64)), _dptr(ms)))
+        return {KERNEL_CLASSES[c]: (int(launches[c]), float(ms[c])) for c in range(n.value)}
+
+    def event_record(self, slot: int):
+        _check(lib().biodiff_event_record(self._h, slot))
+
+    def event_elapsed(self, begin: int, end: int) -> float:
+        ms = _d()
+        _check(lib().biodiff_event_elapsed(self._h, begin, end, ctypes.byref(ms)))
+        return ms.value
+
+    def launch_count(self) -> int:
+        n = _i64()
+        _check(lib().biodiff_launch_count(self._h, ctypes.byref(n)))
+        return int(n.value)
+
+    def cross_check(self, other, abs_tol: float, rel_tol: float) -> CrossCheckReport:
+        """Device-side cross_check of the session field against `other` (validation.cpp:112-137)."""
+        b = _f64(other, self.value_count)
+        ma, mr, wi, ok = _d(), _d(), _i64(), _i32()
+        _check(lib().biodiff_cross_check(self._h, _dptr(b), b.size, abs_tol, rel_tol, ctypes.byref(ma),
+                                         ctypes.byref(mr), ctypes.byref(wi), ctypes.byref(ok)))
+        w = int(wi.value)
+        return CrossCheckReport(ma.value, mr.value, w, w // self.S if w >= 0 else -1,
+                                w % self.S if w >= 0 else -1, bool(ok.value))

@@ -1,0 +1,386 @@
+// extern "C" boundary (include/biodiff_b200.h) over the host mirror and the
+// device session. Exceptions are mapped to status codes exactly as the
+// reference maps its exception types to exit codes (errors.hpp:9-24,
+// SPEC.md:499): config_error -> 1, io_error -> 4, everything else -> 2.
+#include "../../include/biodiff_b200.h"
+
+#include "device.hpp"
+#include "host.hpp"
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+
+using namespace biodiff_b200;
+
+struct biodiff_session {
+    std::unique_ptr<DeviceSession> dev;
+    CartesianMesh mesh;
+    int S = 0;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f)
+{
+    try {
+        f();
+        return BIODIFF_OK;
+    } catch (const config_error& e) {
+        g_last_error = e.what();
+        return BIODIFF_ERR_CONFIG;
+    } catch (const io_error& e) {
+        g_last_error = e.what();
+        return BIODIFF_ERR_IO;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "out of host memory";
+        return BIODIFF_ERR_STATE;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return BIODIFF_ERR_STATE;
+    } catch (...) {
+        g_last_error = "unknown error";
+        return BIODIFF_ERR_STATE;
+    }
+}
+
+CartesianMesh to_mesh(const biodiff_mesh* m)
+{
+    if (!m) throw std::invalid_argument("null mesh");
+    CartesianMesh c;
+    c.x_min = m->x_min;
+    c.x_max = m->x_max;
+    c.y_min = m->y_min;
+    c.y_max = m->y_max;
+    c.z_min = m->z_min;
+    c.z_max = m->z_max;
+    c.dx = m->dx;
+    c.dy = m->dy;
+    c.dz = m->dz;
+    c.nx = m->nx;
+    c.ny = m->ny;
+    c.nz = m->nz;
+    if (c.nx < 1 || c.ny < 1 || c.nz < 1) throw config_error("mesh voxel counts must be positive");
+    if (!(c.dx > 0.0) || !(c.dy > 0.0) || !(c.dz > 0.0)) throw config_error("mesh spacing must be positive");
+    return c;
+}
+
+void from_mesh(const CartesianMesh& c, biodiff_mesh* m)
+{
+    m->x_min = c.x_min;
+    m->x_max = c.x_max;
+    m->y_min = c.y_min;
+    m->y_max = c.y_max;
+    m->z_min = c.z_min;
+    m->z_max = c.z_max;
+    m->dx = c.dx;
+    m->dy = c.dy;
+    m->dz = c.dz;
+    m->nx = c.nx;
+    m->ny = c.ny;
+    m->nz = c.nz;
+}
+
+DeviceSession& dev(biodiff_session* s)
+{
+    if (!s || !s->dev) throw std::invalid_argument("null session");
+    return *s->dev;
+}
+
+Axis to_axis(int32_t a)
+{
+    if (a < 0 || a > 2) throw std::invalid_argument("axis must be 0 (x), 1 (y) or 2 (z)");
+    return static_cast<Axis>(a);
+}
+
+void need(const void* p, const char* what)
+{
+    if (!p) throw std::invalid_argument(std::string("null pointer: ") + what);
+}
+
+} // namespace
+
+extern "C" {
+
+const char* biodiff_last_error(void) { return g_last_error.c_str(); }
+
+int32_t biodiff_version(void) { return 10000; }
+
+int biodiff_mesh_from_bounds(double x_min, double x_max, double y_min, double y_max, double z_min, double z_max,
+                             double dx, double dy, double dz, biodiff_mesh* out)
+{
+    return guarded([&] {
+        need(out, "out");
+        from_mesh(CartesianMesh::from_bounds(x_min, x_max, y_min, y_max, z_min, z_max, dx, dy, dz), out);
+    });
+}
+
+int biodiff_nearest_voxel(const biodiff_mesh* mesh, const double position[3], int64_t* voxel)
+{
+    return guarded([&] {
+        need(position, "position");
+        need(voxel, "voxel");
+        *voxel = to_mesh(mesh).nearest_voxel({position[0], position[1], position[2]});
+    });
+}
+
+int biodiff_precompute_thomas(const biodiff_mesh* mesh, int32_t substrates, const double* diffusion,
+                              const double* decay, double dt, int32_t axis, int32_t dims, double* off_diag,
+                              double* denom_inv, double* c_back)
+{
+    return guarded([&] {
+        need(diffusion, "diffusion");
+        need(decay, "decay");
+        need(off_diag, "off_diag");
+        need(denom_inv, "denom_inv");
+        need(c_back, "c_back");
+        if (substrates < 1) throw std::invalid_argument("no substrates to precompute coefficients for");
+        const SolverWorkspace w = precompute_thomas_coefficients(
+            to_mesh(mesh), std::vector<double>(diffusion, diffusion + substrates),
+            std::vector<double>(decay, decay + substrates), dt, to_axis(axis), dims);
+        std::memcpy(off_diag, w.off_diag.data(), sizeof(double) * w.off_diag.size());
+        std::memcpy(denom_inv, w.denom_inv.data(), sizeof(double) * w.denom_inv.size());
+        std::memcpy(c_back, w.c_back.data(), sizeof(double) * w.c_back.size());
+    });
+}
+
+int biodiff_device_count(int32_t* count)
+{
+    return guarded([&] {
+        need(count, "count");
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess) n = 0;
+        int usable = 0;
+        for (int d = 0; d < n; ++d) {
+            cudaDeviceProp p;
+            if (cudaGetDeviceProperties(&p, d) == cudaSuccess && p.major == 10) ++usable;
+        }
+        *count = usable;
+    });
+}
+
+int biodiff_session_create(const biodiff_mesh* mesh, int32_t substrates, int32_t device, biodiff_session** out)
+{
+    return guarded([&] {
+        need(out, "out");
+        *out = nullptr;
+        auto s = std::make_unique<biodiff_session>();
+        s->mesh = to_mesh(mesh);
+        s->S = substrates;
+        s->dev = std::make_unique<DeviceSession>(s->mesh, substrates, device);
+        *out = s.release();
+    });
+}
+
+int biodiff_session_destroy(biodiff_session* session)
+{
+    return guarded([&] { delete session; });
+}
+
+int biodiff_set_substrates(biodiff_session* session, const double* diffusion, const double* decay, double dt)
+{
+    return guarded([&] {
+        need(diffusion, "diffusion");
+        need(decay, "decay");
+        std::vector<SubstrateParams> params;
+        for (int s = 0; s < dev(session).substrates(); ++s) {
+            if (diffusion[s] < 0.0) throw config_error("substrate has negative diffusion coefficient");
+            if (decay[s] < 0.0) throw config_error("substrate has negative decay rate");
+            params.push_back({"s" + std::to_string(s), diffusion[s], decay[s], 0.0});
+        }
+        dev(session).set_workspaces(SolverWorkspaces::build(session->mesh, params, dt));
+    });
+}
+
+int biodiff_set_workspace(biodiff_session* session, int32_t axis, int32_t n, int32_t dims, double dt,
+                          const double* off_diag, const double* denom_inv, const double* c_back)
+{
+    return guarded([&] {
+        need(off_diag, "off_diag");
+        need(denom_inv, "denom_inv");
+        need(c_back, "c_back");
+        dev(session).set_workspace(to_axis(axis), n, dims, dt, off_diag, denom_inv, c_back);
+    });
+}
+
+int biodiff_set_dirichlet(biodiff_session* session, int64_t count, const int64_t* voxel, const uint8_t* mask,
+                          const double* values)
+{
+    return guarded([&] {
+        if (count < 0) throw std::invalid_argument("negative Dirichlet entry count");
+        if (count > 0) {
+            need(voxel, "voxel");
+            need(mask, "mask");
+            need(values, "values");
+        }
+        DeviceSession& d = dev(session);
+        const int S = d.substrates();
+        DirichletMap map;
+        for (int64_t e = 0; e < count; ++e)
+            map.add(voxel[e], std::vector<std::uint8_t>(mask + e * S, mask + (e + 1) * S),
+                    std::vector<double>(values + e * S, values + (e + 1) * S), session->mesh.voxel_count(), S);
+        d.set_dirichlet(map);
+    });
+}
+
+int biodiff_set_agents(biodiff_session* session, int64_t n, const int64_t* ids, const double* positions,
+                       const double* volume, const double* secretion, const double* uptake,
+                       const double* saturation)
+{
+    return guarded([&] {
+        if (n < 0) throw std::invalid_argument("negative agent count");
+        if (n > 0) {
+            need(ids, "ids");
+            need(positions, "positions");
+            need(volume, "volume");
+            need(secretion, "secretion");
+            need(uptake, "uptake");
+            need(saturation, "saturation");
+        }
+        DeviceSession& d = dev(session);
+        const int S = d.substrates();
+        std::vector<CellAgent> agents(static_cast<std::size_t>(n));
+        for (int64_t a = 0; a < n; ++a) {
+            CellAgent& c = agents[a];
+            c.id = ids[a];
+            c.position = {positions[3 * a], positions[3 * a + 1], positions[3 * a + 2]};
+            c.volume = volume[a];
+            c.secretion_rates.assign(secretion + a * S, secretion + (a + 1) * S);
+            c.uptake_rates.assign(uptake + a * S, uptake + (a + 1) * S);
+            c.saturation_densities.assign(saturation + a * S, saturation + (a + 1) * S);
+        }
+        d.set_agents(AgentPopulation(std::move(agents), session->mesh, S));
+    });
+}
+
+int biodiff_agent_grouping(biodiff_session* session, int64_t* groups, int64_t* group_voxel, int64_t* group_offsets,
+                           int64_t* order)
+{
+    return guarded([&] {
+        need(groups, "groups");
+        const auto& g = dev(session).agents().grouping();
+        *groups = static_cast<int64_t>(g.size());
+        if (!group_voxel || !group_offsets || !order) return;
+        int64_t m = 0;
+        for (std::size_t k = 0; k < g.size(); ++k) {
+            group_voxel[k] = g[k].first;
+            group_offsets[k] = m;
+            for (std::size_t idx : g[k].second) order[m++] = static_cast<int64_t>(idx);
+        }
+        group_offsets[g.size()] = m;
+    });
+}
+
+int biodiff_upload_field(biodiff_session* session, const double* values, int64_t count)
+{
+    return guarded([&] {
+        need(values, "values");
+        dev(session).upload(values, count);
+    });
+}
+
+int biodiff_download_field(biodiff_session* session, double* values, int64_t count)
+{
+    return guarded([&] {
+        need(values, "values");
+        dev(session).download(values, count);
+    });
+}
+
+int biodiff_diffusion_sweep(biodiff_session* session, int32_t axis)
+{
+    return guarded([&] { dev(session).sweep(to_axis(axis)); });
+}
+
+int biodiff_apply_dirichlet(biodiff_session* session)
+{
+    return guarded([&] { dev(session).apply_dirichlet(); });
+}
+
+int biodiff_diffuse_decay_step(biodiff_session* session)
+{
+    return guarded([&] { dev(session).diffuse_decay_step(); });
+}
+
+int biodiff_cell_sources_sinks_step(biodiff_session* session, double dt)
+{
+    return guarded([&] { dev(session).sources(dt); });
+}
+
+int biodiff_advance(biodiff_session* session, int64_t steps, double dt, int32_t with_sources)
+{
+    return guarded([&] { dev(session).advance(steps, dt, with_sources != 0); });
+}
+
+int biodiff_synchronize(biodiff_session* session)
+{
+    return guarded([&] { dev(session).synchronize(); });
+}
+
+int biodiff_session_stream(biodiff_session* session, void** stream)
+{
+    return guarded([&] {
+        need(stream, "stream");
+        *stream = dev(session).stream();
+    });
+}
+
+int biodiff_set_kernel_timing(biodiff_session* session, int32_t enabled)
+{
+    return guarded([&] { dev(session).set_kernel_timing(enabled != 0); });
+}
+
+int biodiff_kernel_times(biodiff_session* session, int32_t* n, int64_t* launches, double* milliseconds)
+{
+    return guarded([&] {
+        need(n, "n");
+        *n = kNumKernelClasses;
+        if (launches && milliseconds) dev(session).kernel_times(launches, milliseconds);
+    });
+}
+
+int biodiff_event_record(biodiff_session* session, int32_t slot)
+{
+    return guarded([&] { dev(session).event_record(slot); });
+}
+
+int biodiff_event_elapsed(biodiff_session* session, int32_t begin, int32_t end, double* milliseconds)
+{
+    return guarded([&] {
+        need(milliseconds, "milliseconds");
+        *milliseconds = dev(session).event_elapsed(begin, end);
+    });
+}
+
+int biodiff_launch_count(biodiff_session* session, int64_t* launches)
+{
+    return guarded([&] {
+        need(launches, "launches");
+        *launches = dev(session).launch_count();
+    });
+}
+
+int biodiff_cross_check(biodiff_session* session, const double* other, int64_t count, double abs_tol,
+                        double rel_tol, double* max_abs, double* max_rel, int64_t* worst_index, int32_t* pass)
+{
+    return guarded([&] {
+        need(other, "other");
+        need(max_abs, "max_abs");
+        need(max_rel, "max_rel");
+        need(worst_index, "worst_index");
+        need(pass, "pass");
+        bool p = false;
+        std::int64_t w = -1;
+        dev(session).cross_check(other, count, abs_tol, rel_tol, max_abs, max_rel, &w, &p);
+        *worst_index = w;
+        *pass = p ? 1 : 0;
+    });
+}
+
+} // extern "C"

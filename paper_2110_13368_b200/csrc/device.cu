@@ -1,0 +1,724 @@
+// DeviceSession: device memory, kernel selection and launch, CUDA-graph
+// capture of the step loop, and the DeviceBackend glue of host.hpp.
+#include "device.hpp"
+#include "kernels.cuh"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
+
+namespace biodiff_b200 {
+
+namespace {
+
+void ck(cudaError_t e, const char* what)
+{
+    if (e != cudaSuccess) throw state_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+void dfree(T*& p)
+{
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+template <class T>
+T* dalloc_copy(const T* host, std::size_t count, cudaStream_t st)
+{
+    T* d = nullptr;
+    if (count == 0) return nullptr;
+    ck(cudaMalloc(&d, sizeof(T) * count), "cudaMalloc");
+    ck(cudaMemcpyAsync(d, host, sizeof(T) * count, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync H2D");
+    return d;
+}
+
+const char* env_or(const char* name, const char* dflt)
+{
+    const char* v = std::getenv(name);
+    return v ? v : dflt;
+}
+
+int smem_limit_bytes()
+{
+    // Per-CTA budget of the shared-memory tile paths: keep >= 2 CTAs per SM.
+    return std::atoi(env_or("BIODIFF_SMEM_MAX_KB", "100")) * 1024;
+}
+
+} // namespace
+
+DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int device)
+    : mesh_(mesh), S_(substrates), device_(device)
+{
+    if (substrates < 1) throw config_error("a session needs at least one substrate");
+    if (mesh.nx < 1 || mesh.ny < 1 || mesh.nz < 1) throw config_error("mesh has an empty axis");
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        throw state_error("no CUDA device visible: the B200 path has no CPU fallback");
+    if (device < 0 || device >= count) throw config_error("device index out of range");
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop;
+    ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10)
+        throw state_error(std::string("device ") + prop.name + " is not sm_100 (Blackwell B200); this build targets sm_100a only");
+    cudaStream_t st;
+    ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+    stream_ = st;
+    ck(cudaMalloc(&rho_, sizeof(double) * value_count()), "cudaMalloc field");
+    ck(cudaMemsetAsync(rho_, 0, sizeof(double) * value_count(), st), "cudaMemset field");
+    ck(cudaMalloc(&shell_values_, sizeof(double) * S_), "cudaMalloc shell");
+    ck(cudaMemsetAsync(shell_values_, 0, sizeof(double) * S_, st), "cudaMemset shell");
+    choose_paths();
+}
+
+DeviceSession::~DeviceSession()
+{
+    cudaSetDevice(device_);
+    if (stream_) cudaStreamSynchronize(static_cast<cudaStream_t>(stream_));
+    invalidate_graphs();
+    for (auto& w : ws_) {
+        dfree(w.q);
+        dfree(w.dinv);
+        dfree(w.cb);
+    }
+    dfree(rho_);
+    dfree(dir_all_voxel_);
+    dfree(dir_all_mask_);
+    dfree(dir_all_values_);
+    dfree(dir_res_voxel_);
+    dfree(dir_res_mask_);
+    dfree(dir_res_values_);
+    dfree(shell_values_);
+    dfree(group_voxel_);
+    dfree(group_offsets_);
+    dfree(agent_volume_);
+    dfree(agent_secretion_);
+    dfree(agent_uptake_);
+    dfree(agent_saturation_);
+    for (auto& pe : pending_events_) {
+        cudaEventDestroy(static_cast<cudaEvent_t>(pe.second.first));
+        cudaEventDestroy(static_cast<cudaEvent_t>(pe.second.second));
+    }
+    for (void* e : event_pool_) cudaEventDestroy(static_cast<cudaEvent_t>(e));
+    for (void* e : slots_)
+        if (e) cudaEventDestroy(static_cast<cudaEvent_t>(e));
+    if (stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
+}
+
+void DeviceSession::choose_paths()
+{
+    const std::string force = env_or("BIODIFF_SWEEP_PATH", "auto");
+    const int limit = smem_limit_bytes();
+    const int rowlen = mesh_.nx * S_;
+    const bool aligned = (rowlen % 2) == 0;
+    for (int ax = 0; ax < 3; ++ax) {
+        const int n = ax == 0 ? mesh_.nx : ax == 1 ? mesh_.ny : mesh_.nz;
+        const int nch = (n + kernels::kChunk - 1) / kernels::kChunk;
+        long long bytes;
+        if (ax == 0) {
+            const int L = std::max(1, kernels::kLanes / S_);
+            const int pitch = ((rowlen + 15) / 16) * 16 + ((S_ + 1) / 2) * 2;
+            bytes = kernels::bar_bytes(nch) + static_cast<long long>(L) * pitch * 8;
+            if (S_ > kernels::kLanes) bytes = std::numeric_limits<long long>::max();
+        } else {
+            bytes = kernels::bar_bytes(nch) + static_cast<long long>(kernels::kLanes) * n * 8;
+        }
+        SweepPath p = bytes <= limit ? (aligned ? SweepPath::smem_bulk : SweepPath::smem_plain) : SweepPath::global;
+        if (force == "global") p = SweepPath::global;
+        if (force == "smem" && bytes <= 227 * 1024) p = aligned ? SweepPath::smem_bulk : SweepPath::smem_plain;
+        if (force == "smem_plain" && bytes <= 227 * 1024) p = SweepPath::smem_plain;
+        path_[ax] = p;
+    }
+}
+
+void DeviceSession::invalidate_graphs()
+{
+    for (auto& g : graphs_) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(g.second.first));
+    graphs_.clear();
+}
+
+void DeviceSession::set_workspace(Axis axis, int n, int dims, double dt, const double* q, const double* dinv,
+                                  const double* cb)
+{
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    const int ax = static_cast<int>(axis);
+    const int expect = ax == 0 ? mesh_.nx : ax == 1 ? mesh_.ny : mesh_.nz;
+    if (n != expect) throw state_error("workspace line length " + std::to_string(n) + " does not match the mesh axis");
+    if (dims < 1 || dims > 3) throw std::invalid_argument("decay split count must be 1, 2, or 3");
+    if (!(dt > 0.0)) throw std::invalid_argument("solver step size must be positive");
+    auto st = static_cast<cudaStream_t>(stream_);
+    ck(cudaStreamSynchronize(st), "sync");
+    DeviceWorkspace& w = ws_[ax];
+    dfree(w.q);
+    dfree(w.dinv);
+    dfree(w.cb);
+    w.q = dalloc_copy(q, S_, st);
+    w.dinv = dalloc_copy(dinv, static_cast<std::size_t>(n) * S_, st);
+    w.cb = dalloc_copy(cb, static_cast<std::size_t>(n) * S_, st);
+    w.n = n;
+    w.dims = dims;
+    w.dt = dt;
+    w.active = true;
+    dims_ = dims;
+    dt_ = dt;
+    invalidate_graphs();
+}
+
+void DeviceSession::set_workspaces(const SolverWorkspaces& ws)
+{
+    if (!ws.x) throw state_error("solver workspaces not built");
+    for (int ax = 0; ax < 3; ++ax) ws_[ax].active = false;
+    auto put = [&](const std::optional<SolverWorkspace>& w) {
+        if (!w) return;
+        if (w->substrates != S_) throw state_error("workspace substrate count does not match the field");
+        set_workspace(w->axis, w->n, w->dims, w->dt, w->off_diag.data(), w->denom_inv.data(), w->c_back.data());
+    };
+    put(ws.x);
+    put(ws.y);
+    put(ws.z);
+}
+
+// Splits the map into the per-substrate boundary-shell rule (evaluated in
+// the last sweep's epilogue) and residual entries. Writes of distinct
+// (voxel, substrate) pairs commute, so the split is bitwise equivalent to
+// applying every entry after the sweeps (solver.cpp:380).
+void DeviceSession::set_dirichlet(const DirichletMap& map)
+{
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    auto st = static_cast<cudaStream_t>(stream_);
+    ck(cudaStreamSynchronize(st), "sync");
+    const int S = S_;
+    const auto& entries = map.entries();
+    const std::int64_t count = static_cast<std::int64_t>(entries.size());
+    std::vector<std::int64_t> vox(count);
+    std::vector<std::uint8_t> mask(count * S);
+    std::vector<double> vals(count * S);
+    for (std::int64_t e = 0; e < count; ++e) {
+        const auto& d = entries[e];
+        if (d.voxel < 0 || d.voxel >= mesh_.voxel_count()) throw std::out_of_range("Dirichlet voxel outside mesh");
+        vox[e] = d.voxel;
+        for (int s = 0; s < S; ++s) {
+            mask[e * S + s] = d.mask[s] ? 1 : 0;
+            vals[e * S + s] = d.values[s];
+        }
+    }
+    // Shell analysis.
+    const std::int64_t nboundary = mesh_.boundary_voxel_count();
+    std::uint64_t shell = 0;
+    std::vector<double> shell_vals(S, 0.0);
+    if (S <= 64 && nboundary > 0) {
+        for (int s = 0; s < S; ++s) {
+            std::int64_t hits = 0;
+            bool first = true, same = true;
+            double v0 = 0.0;
+            for (std::int64_t e = 0; e < count && same; ++e) {
+                if (!mask[e * S + s]) continue;
+                const auto ijk = mesh_.voxel_ijk(vox[e]);
+                if (!mesh_.is_boundary_voxel(ijk[0], ijk[1], ijk[2])) continue;
+                const double v = vals[e * S + s];
+                if (first) {
+                    v0 = v;
+                    first = false;
+                } else if (std::memcmp(&v, &v0, sizeof(double)) != 0) {
+                    same = false;
+                }
+                ++hits;
+            }
+            if (same && hits == nboundary) {
+                shell |= (1ull << s);
+                shell_vals[s] = v0;
+            }
+        }
+    }
+    std::vector<std::int64_t> rvox;
+    std::vector<std::uint8_t> rmask;
+    std::vector<double> rvals;
+    for (std::int64_t e = 0; e < count; ++e) {
+        const auto ijk = mesh_.voxel_ijk(vox[e]);
+        const bool boundary = mesh_.is_boundary_voxel(ijk[0], ijk[1], ijk[2]);
+        bool any = false;
+        for (int s = 0; s < S; ++s) {
+            const bool covered = boundary && ((shell >> s) & 1ull);
+            if (mask[e * S + s] && !covered) any = true;
+        }
+        if (!any) continue;
+        rvox.push_back(vox[e]);
+        for (int s = 0; s < S; ++s) {
+            const bool covered = boundary && ((shell >> s) & 1ull);
+            rmask.push_back(mask[e * S + s] && !covered ? 1 : 0);
+            rvals.push_back(vals[e * S + s]);
+        }
+    }
+    dfree(dir_all_voxel_);
+    dfree(dir_all_mask_);
+    dfree(dir_all_values_);
+    dfree(dir_res_voxel_);
+    dfree(dir_res_mask_);
+    dfree(dir_res_values_);
+    dir_all_count_ = count;
+    dir_all_voxel_ = dalloc_copy(vox.data(), vox.size(), st);
+    dir_all_mask_ = dalloc_copy(mask.data(), mask.size(), st);
+    dir_all_values_ = dalloc_copy(vals.data(), vals.size(), st);
+    dir_res_count_ = static_cast<std::int64_t>(rvox.size());
+    dir_res_voxel_ = dalloc_copy(rvox.data(), rvox.size(), st);
+    dir_res_mask_ = dalloc_copy(rmask.data(), rmask.size(), st);
+    dir_res_values_ = dalloc_copy(rvals.data(), rvals.size(), st);
+    shell_mask_ = shell;
+    ck(cudaMemcpyAsync(shell_values_, shell_vals.data(), sizeof(double) * S, cudaMemcpyHostToDevice, st), "shell");
+    ck(cudaStreamSynchronize(st), "sync");
+    invalidate_graphs();
+}
+
+void DeviceSession::set_agents(const AgentPopulation& agents)
+{
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    auto st = static_cast<cudaStream_t>(stream_);
+    ck(cudaStreamSynchronize(st), "sync");
+    const int S = S_;
+    const auto& groups = agents.grouping();
+    const auto& all = agents.agents();
+    std::vector<std::int64_t> gv, go;
+    std::vector<double> vol, sec, upt, sat;
+    gv.reserve(groups.size());
+    go.reserve(groups.size() + 1);
+    std::int64_t m = 0;
+    for (const auto& [voxel, idxs] : groups) {
+        if (voxel < 0 || voxel >= mesh_.voxel_count())
+            throw state_error("agent voxel " + std::to_string(voxel) + " outside the mesh; rebuild the voxel grouping");
+        gv.push_back(voxel);
+        go.push_back(m);
+        for (std::size_t idx : idxs) {
+            const CellAgent& a = all[idx];
+            if (a.secretion_rates.size() != static_cast<std::size_t>(S))
+                throw state_error("agent rate vectors do not match the substrate count");
+            vol.push_back(a.volume);
+            for (int s = 0; s < S; ++s) {
+                sec.push_back(a.secretion_rates[s]);
+                upt.push_back(a.uptake_rates[s]);
+                sat.push_back(a.saturation_densities[s]);
+            }
+            ++m;
+        }
+    }
+    go.push_back(m);
+    dfree(group_voxel_);
+    dfree(group_offsets_);
+    dfree(agent_volume_);
+    dfree(agent_secretion_);
+    dfree(agent_uptake_);
+    dfree(agent_saturation_);
+    groups_ = static_cast<std::int64_t>(gv.size());
+    n_agents_ = m;
+    group_voxel_ = dalloc_copy(gv.data(), gv.size(), st);
+    group_offsets_ = dalloc_copy(go.data(), go.size(), st);
+    agent_volume_ = dalloc_copy(vol.data(), vol.size(), st);
+    agent_secretion_ = dalloc_copy(sec.data(), sec.size(), st);
+    agent_uptake_ = dalloc_copy(upt.data(), upt.size(), st);
+    agent_saturation_ = dalloc_copy(sat.data(), sat.size(), st);
+    ck(cudaStreamSynchronize(st), "sync");
+    agents_ = agents;
+    invalidate_graphs();
+}
+
+void DeviceSession::upload(const double* values, std::int64_t count)
+{
+    if (count != value_count()) throw state_error("density field size does not match the mesh");
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    ck(cudaMemcpyAsync(rho_, values, sizeof(double) * count, cudaMemcpyHostToDevice,
+                       static_cast<cudaStream_t>(stream_)),
+       "upload");
+}
+
+void DeviceSession::download(double* values, std::int64_t count)
+{
+    if (count != value_count()) throw state_error("density field size does not match the mesh");
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    auto st = static_cast<cudaStream_t>(stream_);
+    ck(cudaMemcpyAsync(values, rho_, sizeof(double) * count, cudaMemcpyDeviceToHost, st), "download");
+    ck(cudaStreamSynchronize(st), "sync");
+}
+
+void DeviceSession::synchronize()
+{
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    ck(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_)), "cudaStreamSynchronize");
+}
+
+void DeviceSession::event_record(int slot)
+{
+    if (slot < 0 || slot >= 16) throw std::invalid_argument("event slot must be 0..15");
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    if (!slots_[slot]) {
+        cudaEvent_t e;
+        ck(cudaEventCreate(&e), "cudaEventCreate");
+        slots_[slot] = e;
+    }
+    ck(cudaEventRecord(static_cast<cudaEvent_t>(slots_[slot]), static_cast<cudaStream_t>(stream_)), "cudaEventRecord");
+}
+
+double DeviceSession::event_elapsed(int begin, int end)
+{
+    if (begin < 0 || begin >= 16 || end < 0 || end >= 16 || !slots_[begin] || !slots_[end])
+        throw std::invalid_argument("event slot not recorded");
+    ck(cudaEventSynchronize(static_cast<cudaEvent_t>(slots_[end])), "cudaEventSynchronize");
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, static_cast<cudaEvent_t>(slots_[begin]), static_cast<cudaEvent_t>(slots_[end])),
+       "cudaEventElapsedTime");
+    return ms;
+}
+
+void DeviceSession::check_ready(Axis axis) const
+{
+    if (!ws_[static_cast<int>(axis)].active) throw state_error("solver workspace for this axis not set");
+}
+
+void DeviceSession::begin_kernel(int cls)
+{
+    ++launches_;
+    if (!timing_) return;
+    cudaEvent_t a, b;
+    if (event_pool_.size() >= 2) {
+        a = static_cast<cudaEvent_t>(event_pool_.back());
+        event_pool_.pop_back();
+        b = static_cast<cudaEvent_t>(event_pool_.back());
+        event_pool_.pop_back();
+    } else {
+        ck(cudaEventCreate(&a), "cudaEventCreate");
+        ck(cudaEventCreate(&b), "cudaEventCreate");
+    }
+    ck(cudaEventRecord(a, static_cast<cudaStream_t>(stream_)), "cudaEventRecord");
+    pending_events_.push_back({cls, {a, b}});
+}
+
+void DeviceSession::end_kernel(int cls)
+{
+    (void)cls;
+    ck(cudaGetLastError(), "kernel launch");
+    if (!timing_) return;
+    ck(cudaEventRecord(static_cast<cudaEvent_t>(pending_events_.back().second.second),
+                       static_cast<cudaStream_t>(stream_)),
+       "cudaEventRecord");
+}
+
+void DeviceSession::set_kernel_timing(bool on)
+{
+    synchronize();
+    timing_ = on;
+    for (int c = 0; c < kNumKernelClasses; ++c) {
+        class_launches_[c] = 0;
+        class_ms_[c] = 0.0;
+    }
+    for (auto& pe : pending_events_) {
+        event_pool_.push_back(pe.second.first);
+        event_pool_.push_back(pe.second.second);
+    }
+    pending_events_.clear();
+}
+
+void DeviceSession::kernel_times(std::int64_t* launches, double* ms)
+{
+    synchronize();
+    for (auto& pe : pending_events_) {
+        float t = 0.f;
+        ck(cudaEventElapsedTime(&t, static_cast<cudaEvent_t>(pe.second.first),
+                                static_cast<cudaEvent_t>(pe.second.second)),
+           "cudaEventElapsedTime");
+        class_launches_[pe.first] += 1;
+        class_ms_[pe.first] += t;
+        event_pool_.push_back(pe.second.first);
+        event_pool_.push_back(pe.second.second);
+    }
+    pending_events_.clear();
+    for (int c = 0; c < kNumKernelClasses; ++c) {
+        launches[c] = class_launches_[c];
+        ms[c] = class_ms_[c];
+    }
+}
+
+void DeviceSession::launch_sweep(Axis axis, bool clamp)
+{
+    const int ax = static_cast<int>(axis);
+    const DeviceWorkspace& w = ws_[ax];
+    auto st = static_cast<cudaStream_t>(stream_);
+    const int S = S_;
+    const int rowlen = mesh_.nx * S;
+    kernels::Clamp cl{shell_values_, clamp ? shell_mask_ : 0ull};
+    const bool do_clamp = clamp && shell_mask_ != 0;
+    const SweepPath p = path_[ax];
+    const int cls = ax;
+    begin_kernel(cls);
+    if (p == SweepPath::global) {
+        kernels::GlobalSweep g{rho_, w.q, w.dinv, w.cb, ax, mesh_.nx, mesh_.ny, mesh_.nz, S, w.n, 0, cl};
+        g.chains = mesh_.voxel_count() * S / w.n;
+        const int block = 128;
+        const long long grid = (g.chains + block - 1) / block;
+        if (do_clamp)
+            kernels::sweep_global<true><<<static_cast<unsigned>(grid), block, 0, st>>>(g);
+        else
+            kernels::sweep_global<false><<<static_cast<unsigned>(grid), block, 0, st>>>(g);
+    } else if (ax == 0) {
+        kernels::XSweep x{};
+        x.rho = rho_;
+        x.q = w.q;
+        x.dinv = w.dinv;
+        x.cb = w.cb;
+        x.lines = static_cast<long long>(mesh_.ny) * mesh_.nz;
+        x.nx = mesh_.nx;
+        x.ny = mesh_.ny;
+        x.nz = mesh_.nz;
+        x.S = S;
+        x.rowlen = rowlen;
+        x.pitch = ((rowlen + 15) / 16) * 16 + ((S + 1) / 2) * 2;
+        x.L = std::max(1, kernels::kLanes / S);
+        x.clamp = cl;
+        const int nch = (mesh_.nx + kernels::kChunk - 1) / kernels::kChunk;
+        const int smem = kernels::bar_bytes(nch) + x.L * x.pitch * 8;
+        const long long grid = (x.lines + x.L - 1) / x.L;
+        auto launch = [&](auto kern) {
+            ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
+            kern<<<static_cast<unsigned>(grid), kernels::kLanes, smem, st>>>(x);
+        };
+        const bool bulk = p == SweepPath::smem_bulk;
+        if (do_clamp)
+            bulk ? launch(kernels::sweep_x_smem<true, true>) : launch(kernels::sweep_x_smem<true, false>);
+        else
+            bulk ? launch(kernels::sweep_x_smem<false, true>) : launch(kernels::sweep_x_smem<false, false>);
+    } else {
+        kernels::StridedSweep y{};
+        y.rho = rho_;
+        y.q = w.q;
+        y.dinv = w.dinv;
+        y.cb = w.cb;
+        const long long row = rowlen;
+        const long long plane = row * mesh_.ny;
+        if (ax == 1) {
+            y.stride = row;
+            y.outer_stride = plane;
+            y.n_outer = mesh_.nz;
+        } else {
+            y.stride = plane;
+            y.outer_stride = row;
+            y.n_outer = mesh_.ny;
+        }
+        y.n = w.n;
+        y.rowlen = rowlen;
+        y.tiles_per_row = (rowlen + kernels::kLanes - 1) / kernels::kLanes;
+        y.S = S;
+        y.nx = mesh_.nx;
+        y.clamp = cl;
+        const int nch = (w.n + kernels::kChunk - 1) / kernels::kChunk;
+        const int smem = kernels::bar_bytes(nch) + kernels::kLanes * w.n * 8;
+        const long long grid = static_cast<long long>(y.tiles_per_row) * y.n_outer;
+        auto launch = [&](auto kern) {
+            ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
+            kern<<<static_cast<unsigned>(grid), kernels::kLanes, smem, st>>>(y);
+        };
+        const bool bulk = p == SweepPath::smem_bulk;
+        if (do_clamp)
+            bulk ? launch(kernels::sweep_strided_smem<true, true>) : launch(kernels::sweep_strided_smem<true, false>);
+        else
+            bulk ? launch(kernels::sweep_strided_smem<false, true>) : launch(kernels::sweep_strided_smem<false, false>);
+    }
+    end_kernel(cls);
+}
+
+void DeviceSession::launch_residual_dirichlet(bool all_entries)
+{
+    const std::int64_t count = all_entries ? dir_all_count_ : dir_res_count_;
+    if (count == 0) return;
+    const long long total = count * S_;
+    const int block = 256;
+    begin_kernel(kDirichlet);
+    kernels::dirichlet_entries<<<static_cast<unsigned>((total + block - 1) / block), block, 0,
+                                 static_cast<cudaStream_t>(stream_)>>>(
+        rho_, S_, count, all_entries ? dir_all_voxel_ : dir_res_voxel_,
+        all_entries ? dir_all_mask_ : dir_res_mask_, all_entries ? dir_all_values_ : dir_res_values_);
+    end_kernel(kDirichlet);
+}
+
+void DeviceSession::launch_sources(double dt)
+{
+    if (groups_ == 0) return;
+    const double inv_voxel_volume = 1.0 / mesh_.voxel_volume(); // agents.cpp:518
+    const long long total = groups_ * S_;
+    const int block = 128;
+    begin_kernel(kSources);
+    kernels::sources_groups<<<static_cast<unsigned>((total + block - 1) / block), block, 0,
+                              static_cast<cudaStream_t>(stream_)>>>(
+        rho_, S_, groups_, group_voxel_, group_offsets_, agent_volume_, agent_secretion_, agent_uptake_,
+        agent_saturation_, dt, inv_voxel_volume);
+    end_kernel(kSources);
+}
+
+void DeviceSession::sweep(Axis axis)
+{
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    check_ready(axis);
+    launch_sweep(axis, false);
+}
+
+void DeviceSession::apply_dirichlet()
+{
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    launch_residual_dirichlet(true);
+}
+
+// solver.cpp:371-381 with the clamp fused into the last active sweep.
+void DeviceSession::step_body(bool with_sources, double dt)
+{
+    const Axis last = ws_[2].active ? Axis::z : ws_[1].active ? Axis::y : Axis::x;
+    launch_sweep(Axis::x, last == Axis::x);
+    if (ws_[1].active) launch_sweep(Axis::y, last == Axis::y);
+    if (ws_[2].active) launch_sweep(Axis::z, last == Axis::z);
+    launch_residual_dirichlet(false);
+    if (with_sources) launch_sources(dt);
+}
+
+void DeviceSession::diffuse_decay_step()
+{
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    check_ready(Axis::x);
+    step_body(false, 0.0);
+}
+
+void DeviceSession::sources(double dt)
+{
+    if (!(dt > 0.0)) throw std::invalid_argument("reaction step size must be positive");
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    launch_sources(dt);
+}
+
+void DeviceSession::advance(std::int64_t steps, double dt, bool with_sources)
+{
+    if (steps < 0) throw std::invalid_argument("step count must be non-negative");
+    if (steps == 0) return;
+    if (!(dt > 0.0)) throw std::invalid_argument("reaction step size must be positive");
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    check_ready(Axis::x);
+    if (std::memcmp(&dt, &dt_, sizeof(double)) != 0)
+        throw state_error("advance dt does not match the solver workspace dt");
+    auto st = static_cast<cudaStream_t>(stream_);
+    if (timing_ || std::getenv("BIODIFF_NO_GRAPH")) {
+        for (std::int64_t s = 0; s < steps; ++s) step_body(with_sources, dt);
+        return;
+    }
+    // Launch-bound small grids: replay a captured graph of up to kGraphSteps steps.
+    constexpr std::int64_t kGraphSteps = 50;
+    auto run_chunk = [&](std::int64_t n) {
+        std::uint64_t bits;
+        std::memcpy(&bits, &dt, sizeof(bits));
+        GraphKey key{n, with_sources, bits};
+        auto it = graphs_.find(key);
+        if (it == graphs_.end()) {
+            const std::int64_t before = launches_;
+            cudaGraph_t graph;
+            ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+            for (std::int64_t s = 0; s < n; ++s) step_body(with_sources, dt);
+            ck(cudaStreamEndCapture(st, &graph), "end capture");
+            cudaGraphExec_t exec;
+            ck(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
+            cudaGraphDestroy(graph);
+            const int kernels_in_graph = static_cast<int>(launches_ - before);
+            launches_ = before;
+            it = graphs_.emplace(key, std::make_pair(static_cast<void*>(exec), kernels_in_graph)).first;
+        }
+        ck(cudaGraphLaunch(static_cast<cudaGraphExec_t>(it->second.first), st), "graph launch");
+        launches_ += it->second.second;
+    };
+    const std::int64_t full = steps / kGraphSteps;
+    for (std::int64_t c = 0; c < full; ++c) run_chunk(kGraphSteps);
+    if (steps % kGraphSteps) run_chunk(steps % kGraphSteps);
+}
+
+void DeviceSession::cross_check(const double* other, std::int64_t count, double abs_tol, double rel_tol,
+                                double* max_abs, double* max_rel, std::int64_t* worst, bool* pass)
+{
+    if (count != value_count()) throw std::invalid_argument("cross_check fields have different shapes");
+    if (abs_tol < 0.0 || rel_tol < 0.0) throw std::invalid_argument("cross_check tolerances must be non-negative");
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    auto st = static_cast<cudaStream_t>(stream_);
+    double* b = nullptr;
+    unsigned long long* scratch = nullptr;
+    ck(cudaMalloc(&b, sizeof(double) * count), "cudaMalloc");
+    ck(cudaMalloc(&scratch, 4 * sizeof(unsigned long long)), "cudaMalloc");
+    const unsigned long long init[4] = {0ull, 0ull, ~0ull, 0ull};
+    ck(cudaMemcpyAsync(scratch, init, sizeof(init), cudaMemcpyHostToDevice, st), "H2D");
+    ck(cudaMemcpyAsync(b, other, sizeof(double) * count, cudaMemcpyHostToDevice, st), "H2D");
+    begin_kernel(kDirichlet + 0); // accounted with the auxiliary kernels
+    kernels::cross_check_max<<<148 * 4, 256, 0, st>>>(rho_, b, count, scratch, scratch + 1, abs_tol, rel_tol,
+                                                      reinterpret_cast<int*>(scratch + 3));
+    end_kernel(kDirichlet);
+    begin_kernel(kDirichlet);
+    kernels::cross_check_argmax<<<148 * 4, 256, 0, st>>>(rho_, b, count, scratch, scratch + 2);
+    end_kernel(kDirichlet);
+    unsigned long long out[4];
+    ck(cudaMemcpyAsync(out, scratch, sizeof(out), cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+    cudaFree(b);
+    cudaFree(scratch);
+    std::memcpy(max_abs, &out[0], sizeof(double));
+    std::memcpy(max_rel, &out[1], sizeof(double));
+    *worst = out[2] == ~0ull ? -1 : static_cast<std::int64_t>(out[2]);
+    *pass = (out[3] & 1ull) == 0;
+}
+
+// ---- DeviceBackend (host.hpp) --------------------------------------------
+
+DeviceBackend::DeviceBackend(int device) : device_(device) {}
+DeviceBackend::~DeviceBackend() = default;
+
+void DeviceBackend::attach(const Microenvironment& env, const SolverWorkspaces& ws, const AgentPopulation* agents)
+{
+    session_ = std::make_unique<DeviceSession>(env.mesh, env.substrate_count(), device_);
+    session_->set_workspaces(ws);
+    session_->set_dirichlet(env.dirichlet);
+    if (agents) attach_agents(*agents);
+    session_->upload(env.field.values.data(), static_cast<std::int64_t>(env.field.values.size()));
+}
+
+void DeviceBackend::attach_agents(const AgentPopulation& agents)
+{
+    if (!session_) throw state_error("device backend not attached");
+    session_->set_agents(agents);
+    agents_from_ = &agents;
+}
+
+void DeviceBackend::upload(const DensityField& field)
+{
+    if (!session_) throw state_error("device backend not attached");
+    session_->upload(field.values.data(), static_cast<std::int64_t>(field.values.size()));
+}
+
+void DeviceBackend::download(DensityField& field)
+{
+    if (!session_) throw state_error("device backend not attached");
+    field.values.resize(static_cast<std::size_t>(session_->value_count()));
+    field.substrates = session_->substrates();
+    session_->download(field.values.data(), static_cast<std::int64_t>(field.values.size()));
+}
+
+void diffuse_decay_step(Microenvironment& env, const SolverWorkspaces& workspaces, DeviceBackend& backend)
+{
+    if (!workspaces.x) throw state_error("solver workspaces not built");
+    (void)env;
+    backend.session().diffuse_decay_step();
+}
+
+void cell_sources_sinks_step(DensityField& field, const AgentPopulation& agents, const CartesianMesh& mesh, double dt,
+                             DeviceBackend& backend)
+{
+    (void)field;
+    (void)mesh;
+    if (!(dt > 0.0)) throw std::invalid_argument("reaction step size must be positive");
+    if (agents.empty()) return;
+    // Re-upload when the caller hands a different population than the one
+    // attached (agents are static between grouping rebuilds).
+    if (backend.attached_agents() != &agents || backend.session().agents().size() != agents.size())
+        backend.attach_agents(agents);
+    backend.session().sources(dt);
+}
+
+} // namespace biodiff_b200

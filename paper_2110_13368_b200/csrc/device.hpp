@@ -1,0 +1,141 @@
+// DeviceSession: the device-resident state of one Microenvironment and the
+// launch logic of the sm_100a kernels (kernels.cu). Plain C++ interface so
+// host.cpp / capi.cpp need no CUDA headers.
+#pragma once
+
+#include "host.hpp"
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
+
+namespace biodiff_b200 {
+
+enum KernelClass { kSweepX = 0, kSweepY = 1, kSweepZ = 2, kDirichlet = 3, kSources = 4, kNumKernelClasses = 5 };
+
+// Device-side copy of one SolverWorkspace (solver.hpp:24-33).
+struct DeviceWorkspace {
+    bool active = false;
+    int n = 0;
+    int dims = 0;
+    double dt = 0.0;
+    double* q = nullptr;    // [S]
+    double* dinv = nullptr; // [n*S]
+    double* cb = nullptr;   // [n*S]
+};
+
+// Which kernel implementation a sweep uses (chosen per axis at set-up; the
+// env var BIODIFF_SWEEP_PATH=smem|global forces one for A/B measurements).
+enum class SweepPath { smem_bulk, smem_plain, global };
+
+class DeviceSession {
+public:
+    DeviceSession(const CartesianMesh& mesh, int substrates, int device);
+    ~DeviceSession();
+    DeviceSession(const DeviceSession&) = delete;
+    DeviceSession& operator=(const DeviceSession&) = delete;
+
+    const CartesianMesh& mesh() const { return mesh_; }
+    int substrates() const { return S_; }
+    std::int64_t value_count() const { return mesh_.voxel_count() * S_; }
+
+    void set_workspace(Axis axis, int n, int dims, double dt, const double* q, const double* dinv, const double* cb);
+    void set_workspaces(const SolverWorkspaces& ws);
+    void set_dirichlet(const DirichletMap& map);
+    void set_agents(const AgentPopulation& agents);
+    const AgentPopulation& agents() const { return agents_; }
+
+    void upload(const double* values, std::int64_t count);
+    void download(double* values, std::int64_t count);
+
+    void sweep(Axis axis);                 // diffusion_sweep, no clamp
+    void apply_dirichlet();                // apply_dirichlet_conditions
+    void diffuse_decay_step();             // x, y, z (+ fused clamp) + residual clamp
+    void sources(double dt);               // cell_sources_sinks_step
+    void advance(std::int64_t steps, double dt, bool with_sources);
+    void synchronize();
+    void* stream() const { return stream_; }
+    void event_record(int slot);
+    double event_elapsed(int begin, int end);
+
+    void set_kernel_timing(bool on);
+    void kernel_times(std::int64_t* launches, double* ms);
+    std::int64_t launch_count() const { return launches_; }
+    SweepPath path(Axis axis) const { return path_[static_cast<int>(axis)]; }
+
+    void cross_check(const double* other, std::int64_t count, double abs_tol, double rel_tol, double* max_abs,
+                     double* max_rel, std::int64_t* worst, bool* pass);
+
+private:
+    void check_ready(Axis axis) const;
+    void launch_sweep(Axis axis, bool clamp);
+    void launch_residual_dirichlet(bool all_entries);
+    void launch_sources(double dt);
+    void step_body(bool with_sources, double dt);
+    void begin_kernel(int cls);
+    void end_kernel(int cls);
+    void invalidate_graphs();
+    void choose_paths();
+
+    CartesianMesh mesh_;
+    int S_ = 0;
+    int device_ = 0;
+    void* stream_ = nullptr; // cudaStream_t
+    double* rho_ = nullptr;
+    DeviceWorkspace ws_[3];
+    int dims_ = 0;
+    double dt_ = 0.0;
+    SweepPath path_[3] = {SweepPath::global, SweepPath::global, SweepPath::global};
+
+    // Dirichlet: every entry (for apply_dirichlet), plus the split used by
+    // the fused step: a per-substrate "whole boundary shell" rule evaluated in
+    // the last sweep's epilogue and the residual entries it does not cover.
+    std::int64_t dir_all_count_ = 0;
+    std::int64_t* dir_all_voxel_ = nullptr;
+    std::uint8_t* dir_all_mask_ = nullptr;
+    double* dir_all_values_ = nullptr;
+    std::int64_t dir_res_count_ = 0;
+    std::int64_t* dir_res_voxel_ = nullptr;
+    std::uint8_t* dir_res_mask_ = nullptr;
+    double* dir_res_values_ = nullptr;
+    std::uint64_t shell_mask_ = 0;
+    double* shell_values_ = nullptr; // [S]
+
+    // Agents in group order (CSR): group voxel, offsets, per-agent params.
+    AgentPopulation agents_;
+    std::int64_t groups_ = 0;
+    std::int64_t n_agents_ = 0;
+    std::int64_t* group_voxel_ = nullptr;
+    std::int64_t* group_offsets_ = nullptr;
+    double* agent_volume_ = nullptr;
+    double* agent_secretion_ = nullptr;
+    double* agent_uptake_ = nullptr;
+    double* agent_saturation_ = nullptr;
+
+    // Launch accounting / timing.
+    std::int64_t launches_ = 0;
+    bool timing_ = false;
+    std::vector<std::pair<int, std::pair<void*, void*>>> pending_events_;
+    std::vector<void*> event_pool_;
+    std::int64_t class_launches_[kNumKernelClasses] = {};
+    double class_ms_[kNumKernelClasses] = {};
+    int kernels_per_step_ = 0;
+
+    // Graph cache for advance(): key (steps in graph, with_sources, dt bits).
+    struct GraphKey {
+        std::int64_t steps;
+        bool sources;
+        std::uint64_t dt_bits;
+        bool operator<(const GraphKey& o) const
+        {
+            if (steps != o.steps) return steps < o.steps;
+            if (sources != o.sources) return sources < o.sources;
+            return dt_bits < o.dt_bits;
+        }
+    };
+    std::map<GraphKey, std::pair<void*, int>> graphs_; // cudaGraphExec_t, kernels per replay
+    void* slots_[16] = {};                              // cudaEvent_t for event_record()
+};
+
+} // namespace biodiff_b200

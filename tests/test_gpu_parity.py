@@ -1,0 +1,258 @@
+"""GPU parity: the CUDA library, called through its C ABI, against the
+oracle and the reference-generated golden fixtures. The bar is bit
+equality (integer/index work exact; FP64 kernels use explicitly rounded
+operations in the reference's order — SURVEY.md Appendix A). Where a test
+compares at a tolerance it says so: north_star's relative 1e-10 per voxel."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2110_13368_b200 as B
+from oracle import Oracle
+from paper_2110_13368_b200 import workloads as W
+from tests.helpers import bits_equal, first_diff, golden_names, load_golden, make_session
+
+pytestmark = pytest.mark.gpu
+
+NORTH_STAR_REL_TOL = 1e-10  # BASELINE.json north_star: relative L-inf per voxel
+
+
+@pytest.fixture(autouse=True)
+def _need_gpu():
+    if B.device_count() == 0:
+        pytest.fail("no sm_100 device visible: GPU tests must run on a B200 (no CPU fallback)")
+
+
+def _paths(monkeypatch, path):
+    if path == "auto":
+        monkeypatch.delenv("BIODIFF_SWEEP_PATH", raising=False)
+    else:
+        monkeypatch.setenv("BIODIFF_SWEEP_PATH", path)
+
+
+SWEEP_SHAPES = [
+    ((16, 16, 16), 1), ((20, 18, 16), 2), ((24, 20, 18), 4), ((17, 9, 11), 1), ((33, 7, 5), 3),
+    ((64, 64, 64), 4), ((100, 30, 20), 2), ((300, 6, 5), 2), ((8, 8, 500), 1), ((50, 50, 50), 1),
+    ((1, 12, 9), 2), ((7, 1, 40), 1), ((5, 3, 2), 8), ((40, 3, 3), 40),
+]
+
+
+@pytest.mark.parametrize("path", ["auto", "global", "smem", "smem_plain"])
+@pytest.mark.parametrize("shape,S", SWEEP_SHAPES)
+def test_single_sweep_bitwise(shape, S, path, monkeypatch):
+    """diffusion_sweep (solver.cpp:330-347) along every active axis, every kernel path."""
+    _paths(monkeypatch, path)
+    w = W.make("t", shape, S, 0, 1, seed=2)
+    rng = np.random.default_rng(hash((shape, S)) & 0xffff)
+    f0 = rng.random(w.voxels * S) * 50.0
+    s = make_session(w)
+    ws = Oracle.workspaces(shape, (w.dx,) * 3, w.diffusion, w.decay, w.dt)
+    for ax in ws:
+        s.upload_field(f0)
+        s.diffusion_sweep(ax)
+        got = s.download_field()
+        want = f0.copy()
+        Oracle.sweep(want, shape, S, ax, ws[ax])
+        assert bits_equal(got, want), f"axis {ax}: {first_diff(got, want)}"
+    s.close()
+
+
+@pytest.mark.parametrize("name", golden_names())
+@pytest.mark.parametrize("path", ["auto", "global"])
+def test_golden_fixture_bitwise(name, path, monkeypatch):
+    """Full runs vs the reference's own outputs (tests/golden, made by oracle/_ref)."""
+    _paths(monkeypatch, path)
+    w, z = load_golden(name)
+    m = B.mesh_from_bounds(*w.bounds(), w.dx, w.dx, w.dx)
+    s = B.Session(m, w.S)
+    s.set_substrates(w.diffusion, w.decay, w.dt)
+    s.set_dirichlet(z["dir_voxels"], z["dir_mask"], z["dir_values"])  # the reference's canonical map
+    if w.n_agents:
+        s.set_agents(w.agent_ids, w.agent_pos, w.agent_vol, w.agent_sec, w.agent_upt, w.agent_sat)
+        gv, go, order = s.agent_grouping()
+        assert np.array_equal(gv, z["group_voxel"]) and np.array_equal(go, z["group_offsets"])
+        assert np.array_equal(order, z["group_order"])
+    s.upload_field(w.initial_field())
+    if bool(z["initial_clamp"]):
+        s.apply_dirichlet_conditions()
+    with_sources = bool(z["with_sources"])
+    for _ in range(w.steps):
+        s.diffuse_decay_step()
+        if with_sources and w.n_agents:
+            s.cell_sources_sinks_step(w.dt)
+    got = s.download_field()
+    assert bits_equal(got, z["field"]), first_diff(got, z["field"])
+    s.close()
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_golden_fixture_advance_graph(name):
+    """Same runs through advance() (CUDA-graph replay of the SPEC.md:297 loop)."""
+    w, z = load_golden(name)
+    if bool(z["initial_clamp"]) or not bool(z["with_sources"]):
+        pytest.skip("advance() runs the plain engine loop")
+    s = make_session(w)
+    s.advance(w.steps, w.dt, with_sources=True)
+    got = s.download_field()
+    assert bits_equal(got, z["field"]), first_diff(got, z["field"])
+    s.close()
+
+
+@pytest.mark.parametrize("cfg,steps", [("c1", 300), ("c2", 40)])
+def test_config_runs_bitwise_vs_oracle(cfg, steps):
+    """C1 (50^3 x 1, 1k cells) and C2 (100^3 x 2, 10k cells) at full grid size."""
+    w = W.CONFIGS[cfg](steps)
+    s = make_session(w)
+    s.advance(steps, w.dt, with_sources=True)
+    got = s.download_field()
+    want = Oracle.run(w, steps)
+    assert bits_equal(got, want), first_diff(got, want)
+    rep = s.cross_check(want, 0.0, 0.0)
+    assert rep.passed and rep.max_abs == 0.0 and rep.worst_value_index == -1
+    s.close()
+
+
+def test_c3_full_size_bitwise_two_steps():
+    """C3 (256^3 x 4, 100k cells): two full steps bit-identical to the oracle."""
+    w = W.c3(2)
+    s = make_session(w)
+    s.advance(2, w.dt, with_sources=True)
+    got = s.download_field()
+    want = Oracle.run(w, 2)
+    assert bits_equal(got, want), first_diff(got, want)
+    s.close()
+
+
+def test_interior_dirichlet_and_partial_masks():
+    w = W.make("t", (40, 36, 30), 3, 500, 1, seed=31, interior_clamps=200, immune_fraction=0.3)
+    s = make_session(w)
+    s.advance(20, w.dt)
+    got = s.download_field()
+    want = Oracle.run(w, 20)
+    assert bits_equal(got, want), first_diff(got, want)
+    # Clamp semantic: every clamped (voxel, s) holds its value exactly after a diffusion step.
+    s.diffuse_decay_step()
+    got = s.download_field()
+    v, m, x = w.dirichlet_entries()
+    S = w.S
+    for e in range(0, v.size, 37):
+        for k in range(S):
+            if m[e, k]:
+                assert got[v[e] * S + k] == x[e, k]
+    s.close()
+
+
+def test_standalone_dirichlet_and_sources_match_oracle():
+    w = W.make("t", (30, 20, 10), 2, 2000, 1, seed=41, interior_clamps=30)
+    rng = np.random.default_rng(3)
+    f0 = rng.random(w.voxels * w.S) * 40
+    s = make_session(w)
+    s.upload_field(f0)
+    s.apply_dirichlet_conditions()
+    want = f0.copy()
+    v, m, x = w.dirichlet_entries()
+    Oracle.dirichlet(want, w.S, v, m, x)
+    got = s.download_field()
+    assert bits_equal(got, want)
+    s.apply_dirichlet_conditions()  # idempotent
+    assert bits_equal(s.download_field(), want)
+    s.cell_sources_sinks_step(w.dt)
+    g = Oracle.group(w.agent_ids, w.agent_pos, w.bounds(), (w.dx,) * 3, w.n)
+    Oracle.sources(want, w.S, g, w.agent_vol, w.agent_sec, w.agent_upt, w.agent_sat, w.dt, 1.0 / w.dx ** 3)
+    got = s.download_field()
+    assert bits_equal(got, want), first_diff(got, want)
+    s.close()
+
+
+def test_no_agents_no_dirichlet_and_empty_inputs():
+    w = W.make("t", (12, 12, 12), 1, 0, 1)
+    w.substrates = [("a", 1000.0, 0.0, 0.0, None)]
+    rng = np.random.default_rng(8)
+    f0 = rng.random(w.voxels)
+    s = make_session(w)
+    s.set_dirichlet(np.zeros(0, np.int64), np.zeros((0, 1), np.uint8), np.zeros((0, 1)))
+    s.set_agents(np.zeros(0, np.int64), np.zeros((0, 3)), np.zeros(0), np.zeros((0, 1)), np.zeros((0, 1)),
+                 np.zeros((0, 1)))
+    s.upload_field(f0)
+    s.advance(100, w.dt, with_sources=True)
+    got = s.download_field()
+    assert abs(got.sum() - f0.sum()) <= 1e-12 * f0.sum()  # mass conservation
+    want = Oracle.run(w, 100, field=f0)
+    assert bits_equal(got, want)
+    s.close()
+
+
+def test_advance_equals_stepwise_and_counts_launches():
+    w = W.make("t", (32, 24, 20), 2, 300, 1, seed=5)
+    a = make_session(w)
+    b = make_session(w)
+    a.advance(57, w.dt)
+    for _ in range(57):
+        b.diffuse_decay_step()
+        b.cell_sources_sinks_step(w.dt)
+    assert bits_equal(a.download_field(), b.download_field())
+    assert a.launch_count() == b.launch_count() > 0
+    a.close()
+    b.close()
+
+
+def test_kernel_timing_reports_every_class():
+    w = W.make("t", (64, 64, 64), 2, 1000, 1, seed=6, interior_clamps=10)
+    s = make_session(w)
+    s.set_kernel_timing(True)
+    s.advance(3, w.dt)
+    t = s.kernel_times()
+    assert t["sweep_x"][0] == t["sweep_y"][0] == t["sweep_z"][0] == 3
+    assert t["sources"][0] == 3 and t["dirichlet"][0] == 3
+    assert all(ms > 0 for n, ms in t.values() if n)
+    s.close()
+
+
+def test_errors_map_to_reference_categories():
+    w = W.make("t", (10, 10, 10), 1, 0, 1)
+    s = make_session(w)
+    with pytest.raises(B.StateError):
+        s.advance(3, w.dt * 2)  # dt must match the workspace (solver.hpp:57-68)
+    with pytest.raises(B.StateError):
+        s.set_workspace(0, 3, 0.01, [1.0], np.ones(11), np.ones(11))  # wrong n for the mesh
+    with pytest.raises(B.StateError):
+        s.cell_sources_sinks_step(0.0)  # agents.cpp:514
+    with pytest.raises(B.StateError):
+        s.set_agents([1, 1], np.zeros((2, 3)), [1, 1], np.zeros(2), np.zeros(2), np.zeros(2))  # duplicate id
+    with pytest.raises(B.StateError):
+        s.set_agents([1], [[1e9, 0, 0]], [1], [0.0], [0.0], [0.0])  # outside the domain
+    with pytest.raises(B.StateError):
+        s.set_dirichlet([5000], [[1]], [[1.0]])  # voxel outside mesh
+    with pytest.raises(B.ConfigError):
+        B.Session(s.mesh, 0)
+    s.close()
+
+
+def test_cross_check_semantics():
+    w = W.make("t", (10, 10, 10), 2, 0, 1)
+    s = make_session(w)
+    f = w.initial_field() + 1.0
+    s.upload_field(f)
+    g = f.copy()
+    g[123] += 1e-3
+    rep = s.cross_check(g, 1e-9, 1e-9)
+    assert not rep.passed and rep.worst_value_index == 123 and rep.worst_voxel == 61 and rep.worst_substrate == 1
+    assert s.cross_check(f, 0.0, 0.0).passed
+    s.close()
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2"])
+def test_long_run_within_north_star_tolerance(cfg):
+    """3000 steps (30 sim-min) at the C1/C2 grids: bitwise in practice; the
+    north_star bar (relative 1e-10 per voxel) is asserted explicitly."""
+    steps = 3000 if cfg == "c1" else 600
+    w = W.CONFIGS[cfg](steps)
+    s = make_session(w)
+    s.advance(steps, w.dt)
+    got = s.download_field()
+    want = Oracle.run(w, steps)
+    rep = s.cross_check(want, 0.0, NORTH_STAR_REL_TOL)
+    assert rep.passed, rep
+    assert bits_equal(got, want), first_diff(got, want)
+    s.close()
