@@ -50,6 +50,56 @@ int smem_limit_bytes()
 
 } // namespace
 
+int settle_row(int n, int S, const double* dinv, const double* cb, std::vector<double>& dconst,
+               std::vector<double>& cconst)
+{
+    dconst.assign(S, 0.0);
+    cconst.assign(S, 0.0);
+    if (n < 3) return n;
+    int settle = 0;
+    for (int s = 0; s < S; ++s) {
+        const double dv = dinv[static_cast<std::size_t>(n - 2) * S + s];
+        const double cv = cb[static_cast<std::size_t>(n - 2) * S + s];
+        dconst[s] = dv;
+        cconst[s] = cv;
+        int m = n - 2;
+        while (m > 0 && std::memcmp(&dinv[static_cast<std::size_t>(m - 1) * S + s], &dv, 8) == 0 &&
+               std::memcmp(&cb[static_cast<std::size_t>(m - 1) * S + s], &cv, 8) == 0)
+            --m;
+        settle = std::max(settle, m);
+    }
+    // Row 0 is special (fwd_first) and never uses the shortcut.
+    return std::max(settle, 1);
+}
+
+void DeviceSession::build_tensor_maps()
+{
+    for (auto& ok : tmap_ok_) ok = false;
+    const long long rowlen = static_cast<long long>(mesh_.nx) * S_;
+    if (rowlen % 2 != 0) return; // strides must be multiples of 16 bytes
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return;
+    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    auto encode = reinterpret_cast<Encode>(fn);
+    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(rowlen), static_cast<cuuint64_t>(mesh_.ny),
+                                static_cast<cuuint64_t>(mesh_.nz)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(rowlen) * 8,
+                                   static_cast<cuuint64_t>(rowlen) * mesh_.ny * 8};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    for (int ax = 1; ax <= 2; ++ax) {
+        const cuuint32_t box[3] = {static_cast<cuuint32_t>(kernels::kLanes),
+                                   static_cast<cuuint32_t>(ax == 1 ? kernels::kChunk : 1),
+                                   static_cast<cuuint32_t>(ax == 2 ? kernels::kChunk : 1)};
+        CUresult r = encode(reinterpret_cast<CUtensorMap*>(tmap_[ax]), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, rho_,
+                            dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        tmap_ok_[ax] = (r == CUDA_SUCCESS);
+    }
+}
+
 DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int device)
     : mesh_(mesh), S_(substrates), device_(device)
 {
@@ -71,6 +121,7 @@ DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int devi
     ck(cudaMemsetAsync(rho_, 0, sizeof(double) * value_count(), st), "cudaMemset field");
     ck(cudaMalloc(&shell_values_, sizeof(double) * S_), "cudaMalloc shell");
     ck(cudaMemsetAsync(shell_values_, 0, sizeof(double) * S_, st), "cudaMemset shell");
+    build_tensor_maps();
     choose_paths();
 }
 
@@ -83,6 +134,8 @@ DeviceSession::~DeviceSession()
         dfree(w.q);
         dfree(w.dinv);
         dfree(w.cb);
+        dfree(w.dconst);
+        dfree(w.cconst);
     }
     dfree(rho_);
     dfree(dir_all_voxel_);
@@ -126,9 +179,11 @@ void DeviceSession::choose_paths()
         } else {
             bytes = kernels::bar_bytes(nch) + static_cast<long long>(kernels::kLanes) * n * 8;
         }
-        SweepPath p = bytes <= limit ? (aligned ? SweepPath::smem_bulk : SweepPath::smem_plain) : SweepPath::global;
+        // y/z async path needs the TMA tensor map; x uses plain bulk copies.
+        const bool async_ok = aligned && (ax == 0 || tmap_ok_[ax]);
+        SweepPath p = bytes <= limit ? (async_ok ? SweepPath::smem_bulk : SweepPath::smem_plain) : SweepPath::global;
         if (force == "global") p = SweepPath::global;
-        if (force == "smem" && bytes <= 227 * 1024) p = aligned ? SweepPath::smem_bulk : SweepPath::smem_plain;
+        if (force == "smem" && bytes <= 227 * 1024) p = async_ok ? SweepPath::smem_bulk : SweepPath::smem_plain;
         if (force == "smem_plain" && bytes <= 227 * 1024) p = SweepPath::smem_plain;
         path_[ax] = p;
     }
@@ -155,9 +210,16 @@ void DeviceSession::set_workspace(Axis axis, int n, int dims, double dt, const d
     dfree(w.q);
     dfree(w.dinv);
     dfree(w.cb);
+    dfree(w.dconst);
+    dfree(w.cconst);
     w.q = dalloc_copy(q, S_, st);
     w.dinv = dalloc_copy(dinv, static_cast<std::size_t>(n) * S_, st);
     w.cb = dalloc_copy(cb, static_cast<std::size_t>(n) * S_, st);
+    std::vector<double> dc, cc;
+    w.settle = std::getenv("BIODIFF_NO_SETTLE") ? n : settle_row(n, S_, dinv, cb, dc, cc);
+    w.dconst = dalloc_copy(dc.data(), dc.size(), st);
+    w.cconst = dalloc_copy(cc.data(), cc.size(), st);
+    ck(cudaStreamSynchronize(st), "sync"); // host staging vectors go out of scope
     w.n = n;
     w.dims = dims;
     w.dt = dt;
@@ -447,9 +509,9 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
     const int rowlen = mesh_.nx * S;
     kernels::Clamp cl{shell_values_, clamp ? shell_mask_ : 0ull};
     const bool do_clamp = clamp && shell_mask_ != 0;
+    const kernels::Coef coef{w.q, w.dinv, w.cb, w.dconst, w.cconst, w.settle};
     const SweepPath p = path_[ax];
-    const int cls = ax;
-    begin_kernel(cls);
+    begin_kernel(ax);
     if (p == SweepPath::global) {
         kernels::GlobalSweep g{rho_, w.q, w.dinv, w.cb, ax, mesh_.nx, mesh_.ny, mesh_.nz, S, w.n, 0, cl};
         g.chains = mesh_.voxel_count() * S / w.n;
@@ -462,9 +524,7 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
     } else if (ax == 0) {
         kernels::XSweep x{};
         x.rho = rho_;
-        x.q = w.q;
-        x.dinv = w.dinv;
-        x.cb = w.cb;
+        x.coef = coef;
         x.lines = static_cast<long long>(mesh_.ny) * mesh_.nz;
         x.nx = mesh_.nx;
         x.ny = mesh_.ny;
@@ -489,11 +549,10 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
     } else {
         kernels::StridedSweep y{};
         y.rho = rho_;
-        y.q = w.q;
-        y.dinv = w.dinv;
-        y.cb = w.cb;
+        y.coef = coef;
         const long long row = rowlen;
         const long long plane = row * mesh_.ny;
+        y.axis = ax;
         if (ax == 1) {
             y.stride = row;
             y.outer_stride = plane;
@@ -510,19 +569,23 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
         y.nx = mesh_.nx;
         y.clamp = cl;
         const int nch = (w.n + kernels::kChunk - 1) / kernels::kChunk;
-        const int smem = kernels::bar_bytes(nch) + kernels::kLanes * w.n * 8;
         const long long grid = static_cast<long long>(y.tiles_per_row) * y.n_outer;
-        auto launch = [&](auto kern) {
-            ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
-            kern<<<static_cast<unsigned>(grid), kernels::kLanes, smem, st>>>(y);
-        };
-        const bool bulk = p == SweepPath::smem_bulk;
-        if (do_clamp)
-            bulk ? launch(kernels::sweep_strided_smem<true, true>) : launch(kernels::sweep_strided_smem<true, false>);
-        else
-            bulk ? launch(kernels::sweep_strided_smem<false, true>) : launch(kernels::sweep_strided_smem<false, false>);
+        if (p == SweepPath::smem_bulk) {
+            const int smem = kernels::bar_bytes(nch) + kernels::kLanes * nch * kernels::kChunk * 8;
+            const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(tmap_[ax]);
+            auto launch = [&](auto kern) {
+                ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
+                kern<<<static_cast<unsigned>(grid), kernels::kLanes, smem, st>>>(tm, y);
+            };
+            do_clamp ? launch(kernels::sweep_yz_tma<true>) : launch(kernels::sweep_yz_tma<false>);
+        } else {
+            const int smem = kernels::kLanes * w.n * 8;
+            ck(cudaFuncSetAttribute(kernels::sweep_yz_plain, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+               "smem attr");
+            kernels::sweep_yz_plain<<<static_cast<unsigned>(grid), kernels::kLanes, smem, st>>>(y, do_clamp);
+        }
     }
-    end_kernel(cls);
+    end_kernel(ax);
 }
 
 void DeviceSession::launch_residual_dirichlet(bool all_entries)

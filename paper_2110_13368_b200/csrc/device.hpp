@@ -20,14 +20,23 @@ struct DeviceWorkspace {
     int n = 0;
     int dims = 0;
     double dt = 0.0;
-    double* q = nullptr;    // [S]
-    double* dinv = nullptr; // [n*S]
-    double* cb = nullptr;   // [n*S]
+    double* q = nullptr;      // [S]
+    double* dinv = nullptr;   // [n*S]
+    double* cb = nullptr;     // [n*S]
+    double* dconst = nullptr; // [S] settled denom_inv (rows settle..n-2)
+    double* cconst = nullptr; // [S] settled c_back
+    int settle = 0;           // first row of the bit-constant region (n = none)
 };
 
 // Which kernel implementation a sweep uses (chosen per axis at set-up; the
 // env var BIODIFF_SWEEP_PATH=smem|global forces one for A/B measurements).
 enum class SweepPath { smem_bulk, smem_plain, global };
+
+// Host-side analysis of a workspace's coefficient columns: the first row
+// from which denom_inv and c_back are bit-constant up to row n-2 (max over
+// substrates), and those constants.
+int settle_row(int n, int S, const double* dinv, const double* cb, std::vector<double>& dconst,
+               std::vector<double>& cconst);
 
 class DeviceSession {
 public:
@@ -136,6 +145,9 @@ private:
     };
     std::map<GraphKey, std::pair<void*, int>> graphs_; // cudaGraphExec_t, kernels per replay
     void* slots_[16] = {};                              // cudaEvent_t for event_record()
+    alignas(64) unsigned char tmap_[3][128] = {};       // CUtensorMap per axis (y, z used)
+    bool tmap_ok_[3] = {false, false, false};
+    void build_tensor_maps();
 };
 
 } // namespace biodiff_b200

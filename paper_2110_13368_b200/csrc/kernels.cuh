@@ -11,6 +11,7 @@
 
 #include "ptx.cuh"
 
+#include <cuda.h>
 #include <cstdint>
 
 namespace biodiff_b200 {
@@ -22,8 +23,22 @@ constexpr int kChunk = 32;   // positions per mbarrier chunk along the sweep axi
 __host__ __device__ constexpr int bar_bytes(int nch) { return ((nch * 8 + 127) / 128) * 128; }
 
 struct Clamp {
-    const double* values;   // [S] shell clamp values
+    const double* values;    // [S] shell clamp values
     unsigned long long mask; // bit s: substrate s clamped on every boundary voxel
+};
+
+// Thomas coefficients of one axis. The precomputed pivots settle to
+// bit-constant values a few dozen rows into the line (SURVEY.md §7 hard part
+// 3): rows in [settle, n-2] use dconst[s] / cconst[s] from registers instead
+// of a load. `settle` is the max over substrates (warp-uniform) and is
+// verified on the host bit for bit; settle = n disables the shortcut.
+struct Coef {
+    const double* q;      // [S]
+    const double* dinv;   // [n*S]
+    const double* cb;     // [n*S]
+    const double* dconst; // [S]
+    const double* cconst; // [S]
+    int settle;
 };
 
 __device__ __forceinline__ double fwd_first(double v, double d) { return __dmul_rn(v, d); }
@@ -33,22 +48,132 @@ __device__ __forceinline__ double fwd(double v, double prev, double q, double d)
 }
 __device__ __forceinline__ double bwd(double v, double next, double cb) { return __dadd_rn(v, __dmul_rn(cb, next)); }
 
+// Per-lane view of one chain (line x substrate) resident in shared memory:
+// element m lives at col[m*step].
+struct Chain {
+    double* col;
+    int step;
+    int S;
+    const double* dinv; // coefficient column of this lane's substrate (stride S)
+    const double* cb;
+    double q, dc, cc;
+    int settle, n;
+    bool clamp_s, face;
+    double clamp_v;
+};
+
+// Forward elimination over positions [m0, m1) (m0 >= 1).
+template <bool CONSTC>
+__device__ __forceinline__ double fwd_range(const Chain& c, int m0, int m1, double prev)
+{
+    int m = m0;
+    for (; m + 8 <= m1; m += 8) {
+        double v[8], d[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            v[u] = c.col[(m + u) * c.step];
+            d[u] = CONSTC ? c.dc : __ldg(c.dinv + (m + u) * c.S);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            prev = fwd(v[u], prev, c.q, d[u]);
+            c.col[(m + u) * c.step] = prev;
+        }
+    }
+    for (; m < m1; ++m) {
+        prev = fwd(c.col[m * c.step], prev, c.q, CONSTC ? c.dc : __ldg(c.dinv + m * c.S));
+        c.col[m * c.step] = prev;
+    }
+    return prev;
+}
+
+// Back substitution over positions mtop down to m0 (inclusive), storing the
+// (optionally clamped) result while the recurrence carries the unclamped one.
+template <bool CONSTC, bool CLAMP>
+__device__ __forceinline__ double bwd_range(const Chain& c, int mtop, int m0, double next)
+{
+    int m = mtop;
+    for (; m - 7 >= m0; m -= 8) {
+        double v[8], b[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            v[u] = c.col[(m - u) * c.step];
+            b[u] = CONSTC ? c.cc : __ldg(c.cb + (m - u) * c.S);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            next = bwd(v[u], next, b[u]);
+            double out = next;
+            if (CLAMP && c.clamp_s && (c.face || (m - u) == 0)) out = c.clamp_v;
+            c.col[(m - u) * c.step] = out;
+        }
+    }
+    for (; m >= m0; --m) {
+        next = bwd(c.col[m * c.step], next, CONSTC ? c.cc : __ldg(c.cb + m * c.S));
+        double out = next;
+        if (CLAMP && c.clamp_s && (c.face || m == 0)) out = c.clamp_v;
+        c.col[m * c.step] = out;
+    }
+    return next;
+}
+
+// The full Thomas solve of one chain, chunk by chunk. wait(ch) blocks until
+// chunk ch has landed in shared memory; flush(ch) is called (by every lane,
+// after the chunk's final values are in shared memory) to write it back.
+template <bool CLAMP, class Wait, class Flush>
+__device__ __forceinline__ void solve_chain(const Chain& c, bool active, int nch, Wait wait, Flush flush)
+{
+    const int n = c.n;
+    double prev = 0.0;
+    for (int ch = 0; ch < nch; ++ch) {
+        wait(ch);
+        const int m0 = ch * kChunk;
+        const int m1 = min(n, m0 + kChunk);
+        if (active) {
+            int m = m0;
+            if (m == 0) {
+                prev = fwd_first(c.col[0], __ldg(c.dinv));
+                c.col[0] = prev;
+                m = 1;
+            }
+            if (m >= c.settle && m1 <= n - 1)
+                prev = fwd_range<true>(c, m, m1, prev);
+            else
+                prev = fwd_range<false>(c, m, m1, prev);
+        }
+    }
+    double next = prev;
+    if (CLAMP && active && c.clamp_s) c.col[(n - 1) * c.step] = c.clamp_v; // position n-1 is always a face
+    for (int ch = nch - 1; ch >= 0; --ch) {
+        const int m0 = ch * kChunk;
+        int mtop = min(n, m0 + kChunk) - 1;
+        if (ch == nch - 1) --mtop; // n-1 holds the final value already
+        if (active && mtop >= m0) {
+            if (m0 >= c.settle)
+                next = bwd_range<true, CLAMP>(c, mtop, m0, next);
+            else
+                next = bwd_range<false, CLAMP>(c, mtop, m0, next);
+        }
+        flush(ch);
+    }
+}
+
 // ---------------------------------------------------------------------------
-// y / z sweep, shared-memory resident tile.
-// A CTA (one warp) owns 32 contiguous doubles of one row (32 (i,s) chains)
-// and the whole line along the sweep axis: tile[m*32 + lane]. Rows arrive
-// by cp.async.bulk in chunks of kChunk rows (one mbarrier each) so the
-// forward recurrence starts on the first chunk; the backward recurrence
-// writes each finished chunk straight back with bulk stores. HBM traffic is
-// one read + one write per value (the line never leaves the SM in between).
+// y / z sweep with TMA. A CTA (one warp) owns 32 contiguous doubles of one
+// row — 32 (i,s) chains — and the whole line along the sweep axis:
+// tile[m*32 + lane]. One elected lane issues 3-D tiled TMA loads of
+// 32 x 32-position boxes (one mbarrier each) so the forward recurrence starts
+// on the first box, and TMA stores each finished box during the backward
+// recurrence. HBM traffic: one read + one write per value; the line stays in
+// shared memory in between. Partial tiles at the row end / line end are
+// handled by TMA bounds (zero fill on load, clipped stores).
 // ---------------------------------------------------------------------------
 struct StridedSweep {
     double* rho;
-    const double* q;
-    const double* dinv;
-    const double* cb;
+    Coef coef;
     long long stride;       // doubles between consecutive positions along the axis
     long long outer_stride; // doubles between consecutive outer indices
+    int axis;               // 1 = y (outer k), 2 = z (outer j)
     int n;                  // line length
     int n_outer;            // number of outer indices (ny for z, nz for y)
     int rowlen;             // nx*S
@@ -58,8 +183,31 @@ struct StridedSweep {
     Clamp clamp;
 };
 
-template <bool CLAMP, bool BULK>
-__global__ void __launch_bounds__(kLanes) sweep_strided_smem(StridedSweep a)
+__device__ __forceinline__ Chain make_chain_yz(const StridedSweep& a, double* tile, int lane, int e0,
+                                               long long outer, bool active)
+{
+    const int e = e0 + (active ? lane : 0);
+    const int s = e % a.S;
+    const int i = e / a.S;
+    Chain c;
+    c.col = tile + lane;
+    c.step = kLanes;
+    c.S = a.S;
+    c.dinv = a.coef.dinv + s;
+    c.cb = a.coef.cb + s;
+    c.q = a.coef.q[s];
+    c.dc = a.coef.dconst[s];
+    c.cc = a.coef.cconst[s];
+    c.settle = a.coef.settle;
+    c.n = a.n;
+    c.clamp_s = (a.clamp.mask >> s) & 1ull;
+    c.clamp_v = c.clamp_s ? a.clamp.values[s] : 0.0;
+    c.face = (i == 0 || i == a.nx - 1 || outer == 0 || outer == a.n_outer - 1);
+    return c;
+}
+
+template <bool CLAMP>
+__global__ void __launch_bounds__(kLanes) sweep_yz_tma(const __grid_constant__ CUtensorMap tmap, StridedSweep a)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     const int nch = (a.n + kChunk - 1) / kChunk;
@@ -67,142 +215,86 @@ __global__ void __launch_bounds__(kLanes) sweep_strided_smem(StridedSweep a)
     double* tile = reinterpret_cast<double*>(smem + bar_bytes(nch));
     const int lane = threadIdx.x;
     const int et = static_cast<int>(blockIdx.x % a.tiles_per_row);
-    const long long outer = blockIdx.x / a.tiles_per_row;
+    const int outer = static_cast<int>(blockIdx.x / a.tiles_per_row);
+    const int e0 = et * kLanes;
+    const int width = min(kLanes, a.rowlen - e0);
+    // Tensor coordinates (dim0 = row element, dim1 = j, dim2 = k) of box ch.
+    auto coords = [&](int ch, int& c1, int& c2) {
+        if (a.axis == 2) {
+            c1 = outer;
+            c2 = ch * kChunk;
+        } else {
+            c1 = ch * kChunk;
+            c2 = outer;
+        }
+    };
+    if (lane == 0) {
+        ptx::tma_prefetch_desc(&tmap);
+        for (int ch = 0; ch < nch; ++ch) ptx::mbar_init(&bars[ch], 1);
+        ptx::fence_mbar_init();
+        for (int ch = 0; ch < nch; ++ch) {
+            int c1, c2;
+            coords(ch, c1, c2);
+            ptx::mbar_arrive_expect_tx(&bars[ch], kLanes * kChunk * 8);
+            ptx::tma_load_3d(tile + ch * kChunk * kLanes, &tmap, e0, c1, c2, &bars[ch]);
+        }
+    }
+    __syncwarp();
+    const bool active = lane < width;
+    const Chain c = make_chain_yz(a, tile, lane, e0, outer, active);
+    solve_chain<CLAMP>(
+        c, active, nch, [&](int ch) { ptx::mbar_wait(&bars[ch], 0); },
+        [&](int ch) {
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                int c1, c2;
+                coords(ch, c1, c2);
+                ptx::tma_store_3d(&tmap, e0, c1, c2, tile + ch * kChunk * kLanes);
+                ptx::bulk_commit();
+            }
+        });
+    if (lane == 0) ptx::bulk_wait_read_all();
+}
+
+// Same tile without TMA (rows with an odd number of doubles cannot be
+// described by a tensor map: strides must be 16-byte multiples).
+__global__ void __launch_bounds__(kLanes) sweep_yz_plain(StridedSweep a, bool clamp)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    double* tile = reinterpret_cast<double*>(smem);
+    const int lane = threadIdx.x;
+    const int et = static_cast<int>(blockIdx.x % a.tiles_per_row);
+    const int outer = static_cast<int>(blockIdx.x / a.tiles_per_row);
     const int e0 = et * kLanes;
     const int width = min(kLanes, a.rowlen - e0);
     double* base = a.rho + outer * a.outer_stride + e0;
-
-    if (BULK) {
-        if (lane == 0) {
-            for (int c = 0; c < nch; ++c) ptx::mbar_init(&bars[c], 1);
-            ptx::fence_mbar_init();
-            for (int c = 0; c < nch; ++c) {
-                const int rows = min(kChunk, a.n - c * kChunk);
-                ptx::mbar_arrive_expect_tx(&bars[c], static_cast<uint32_t>(rows * width * 8));
-            }
-        }
-        __syncwarp();
-        for (int m = lane; m < a.n; m += kLanes)
-            ptx::bulk_g2s(tile + m * kLanes, base + m * a.stride, static_cast<uint32_t>(width * 8),
-                          &bars[m / kChunk]);
-    } else {
-        for (int m = 0; m < a.n; ++m)
-            if (lane < width) tile[m * kLanes + lane] = base[m * a.stride + lane];
-        __syncwarp();
-    }
-
     const bool active = lane < width;
-    const int e = e0 + (active ? lane : 0);
-    const int s = e % a.S;
-    const int i = e / a.S;
-    const double qs = a.q[s];
-    const double* dinv = a.dinv + s;
-    const double* cb = a.cb + s;
-    const int S = a.S;
-    bool clamp_s = false, lane_face = false;
-    double clamp_v = 0.0;
-    if (CLAMP) {
-        clamp_s = (a.clamp.mask >> s) & 1ull;
-        clamp_v = a.clamp.values[s];
-        lane_face = (i == 0 || i == a.nx - 1 || outer == 0 || outer == a.n_outer - 1);
-    }
-    double* col = tile + lane;
-
-    // Forward elimination.
-    double prev = 0.0;
-    for (int c = 0; c < nch; ++c) {
-        if (BULK) ptx::mbar_wait(&bars[c], 0);
-        const int m0 = c * kChunk;
-        const int m1 = min(a.n, m0 + kChunk);
-        if (active) {
-            int m = m0;
-            if (m == 0) {
-                prev = fwd_first(col[0], __ldg(dinv));
-                col[0] = prev;
-                m = 1;
-            }
-            for (; m + 8 <= m1; m += 8) {
-                double v[8], d[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    v[u] = col[(m + u) * kLanes];
-                    d[u] = __ldg(dinv + (m + u) * S);
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    prev = fwd(v[u], prev, qs, d[u]);
-                    col[(m + u) * kLanes] = prev;
-                }
-            }
-            for (; m < m1; ++m) {
-                prev = fwd(col[m * kLanes], prev, qs, __ldg(dinv + m * S));
-                col[m * kLanes] = prev;
-            }
-        }
-    }
-
-    // Back substitution, chunk by chunk from the top; each finished chunk is
-    // written back while the next one is computed.
-    double next = prev;
-    const int last = a.n - 1;
-    if (CLAMP && active && clamp_s) col[last * kLanes] = clamp_v; // m = n-1 is always a face
-    for (int c = nch - 1; c >= 0; --c) {
-        const int m0 = c * kChunk;
-        const int mtop = min(a.n, m0 + kChunk) - 1;
-        if (active) {
-            int m = (c == nch - 1) ? mtop - 1 : mtop;
-            for (; m - 7 >= m0; m -= 8) {
-                double v[8], b[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    v[u] = col[(m - u) * kLanes];
-                    b[u] = __ldg(cb + (m - u) * S);
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    next = bwd(v[u], next, b[u]);
-                    double out = next;
-                    if (CLAMP && clamp_s && (lane_face || (m - u) == 0)) out = clamp_v;
-                    col[(m - u) * kLanes] = out;
-                }
-            }
-            for (; m >= m0; --m) {
-                next = bwd(col[m * kLanes], next, __ldg(cb + m * S));
-                double out = next;
-                if (CLAMP && clamp_s && (lane_face || m == 0)) out = clamp_v;
-                col[m * kLanes] = out;
-            }
-        }
-        if (BULK) {
-            ptx::fence_proxy_async_smem();
-            __syncwarp();
-            const int m = m0 + lane;
-            if (m <= mtop) {
-                ptx::bulk_s2g(base + m * a.stride, tile + m * kLanes, static_cast<uint32_t>(width * 8));
-                ptx::bulk_commit();
-            }
-        }
-    }
-    if (BULK) {
-        ptx::bulk_wait_read_all();
-    } else {
-        __syncwarp();
-        for (int m = 0; m < a.n; ++m)
-            if (lane < width) base[m * a.stride + lane] = tile[m * kLanes + lane];
-    }
+    for (int m = 0; m < a.n; ++m)
+        if (active) tile[m * kLanes + lane] = base[m * a.stride + lane];
+    __syncwarp();
+    const Chain c = make_chain_yz(a, tile, lane, e0, outer, active);
+    const int nch = (a.n + kChunk - 1) / kChunk;
+    auto none = [](int) {};
+    if (clamp)
+        solve_chain<true>(c, active, nch, none, none);
+    else
+        solve_chain<false>(c, active, nch, none, none);
+    __syncwarp();
+    for (int m = 0; m < a.n; ++m)
+        if (active) base[m * a.stride + lane] = tile[m * kLanes + lane];
 }
 
 // ---------------------------------------------------------------------------
 // x sweep, shared-memory resident tile of L whole x-lines (contiguous in
-// HBM: one bulk copy per line and chunk). Lane -> (line l, substrate s);
-// line l lives at tile[l*pitch + i*S + s], pitch padded so that the lanes of
-// a half-warp hit distinct banks.
+// HBM). Lane -> (line l, substrate s); line l lives at
+// tile[l*pitch + i*S + s], pitch padded so the lanes of a half-warp hit
+// distinct banks. Lane 0 issues one bulk copy per (line, chunk) — 1 KB at
+// S=4 — and the stores of each finished chunk.
 // ---------------------------------------------------------------------------
 struct XSweep {
     double* rho;
-    const double* q;
-    const double* dinv;
-    const double* cb;
+    Coef coef;
     long long lines; // ny*nz
     int nx, ny, nz, S;
     int rowlen;      // nx*S
@@ -210,6 +302,29 @@ struct XSweep {
     int L;           // lines per tile (L*S <= 32)
     Clamp clamp;
 };
+
+__device__ __forceinline__ Chain make_chain_x(const XSweep& a, double* tile, int lane, long long line0, bool active)
+{
+    const int l = active ? lane / a.S : 0;
+    const int s = active ? lane % a.S : 0;
+    const long long line = line0 + l;
+    const int j = static_cast<int>(line % a.ny), k = static_cast<int>(line / a.ny);
+    Chain c;
+    c.col = tile + l * a.pitch + s;
+    c.step = a.S;
+    c.S = a.S;
+    c.dinv = a.coef.dinv + s;
+    c.cb = a.coef.cb + s;
+    c.q = a.coef.q[s];
+    c.dc = a.coef.dconst[s];
+    c.cc = a.coef.cconst[s];
+    c.settle = a.coef.settle;
+    c.n = a.nx;
+    c.clamp_s = (a.clamp.mask >> s) & 1ull;
+    c.clamp_v = c.clamp_s ? a.clamp.values[s] : 0.0;
+    c.face = (j == 0 || j == a.ny - 1 || k == 0 || k == a.nz - 1);
+    return c;
+}
 
 template <bool CLAMP, bool BULK>
 __global__ void __launch_bounds__(kLanes) sweep_x_smem(XSweep a)
@@ -226,21 +341,18 @@ __global__ void __launch_bounds__(kLanes) sweep_x_smem(XSweep a)
 
     if (BULK) {
         if (lane == 0) {
-            for (int c = 0; c < nch; ++c) ptx::mbar_init(&bars[c], 1);
+            for (int ch = 0; ch < nch; ++ch) ptx::mbar_init(&bars[ch], 1);
             ptx::fence_mbar_init();
-            for (int c = 0; c < nch; ++c) {
-                const int cnt = min(kChunk, a.nx - c * kChunk);
-                ptx::mbar_arrive_expect_tx(&bars[c], static_cast<uint32_t>(nl * cnt * S * 8));
+            for (int ch = 0; ch < nch; ++ch) {
+                const int cnt = min(kChunk, a.nx - ch * kChunk);
+                const int off = ch * kChunk * S;
+                ptx::mbar_arrive_expect_tx(&bars[ch], static_cast<uint32_t>(nl * cnt * S * 8));
+                for (int l = 0; l < nl; ++l)
+                    ptx::bulk_g2s(tile + l * a.pitch + off, base + static_cast<long long>(l) * a.rowlen + off,
+                                  static_cast<uint32_t>(cnt * S * 8), &bars[ch]);
             }
         }
         __syncwarp();
-        for (int idx = lane; idx < nl * nch; idx += kLanes) {
-            const int c = idx / nl, l = idx % nl;
-            const int cnt = min(kChunk, a.nx - c * kChunk);
-            const int off = c * kChunk * S;
-            ptx::bulk_g2s(tile + l * a.pitch + off, base + static_cast<long long>(l) * a.rowlen + off,
-                          static_cast<uint32_t>(cnt * S * 8), &bars[c]);
-        }
     } else {
         for (int idx = lane; idx < nl * a.rowlen; idx += kLanes) {
             const int l = idx / a.rowlen, o = idx % a.rowlen;
@@ -250,98 +362,27 @@ __global__ void __launch_bounds__(kLanes) sweep_x_smem(XSweep a)
     }
 
     const bool active = lane < nl * S;
-    const int l = active ? lane / S : 0;
-    const int s = active ? lane % S : 0;
-    const double qs = a.q[s];
-    const double* dinv = a.dinv + s;
-    const double* cb = a.cb + s;
-    double* v = tile + l * a.pitch + s;
-    bool clamp_s = false, lane_face = false;
-    double clamp_v = 0.0;
-    if (CLAMP) {
-        const long long line = line0 + l;
-        const int j = static_cast<int>(line % a.ny), k = static_cast<int>(line / a.ny);
-        clamp_s = (a.clamp.mask >> s) & 1ull;
-        clamp_v = a.clamp.values[s];
-        lane_face = (j == 0 || j == a.ny - 1 || k == 0 || k == a.nz - 1);
-    }
-
-    double prev = 0.0;
-    for (int c = 0; c < nch; ++c) {
-        if (BULK) ptx::mbar_wait(&bars[c], 0);
-        const int i0 = c * kChunk;
-        const int i1 = min(a.nx, i0 + kChunk);
-        if (active) {
-            int i = i0;
-            if (i == 0) {
-                prev = fwd_first(v[0], __ldg(dinv));
-                v[0] = prev;
-                i = 1;
-            }
-            for (; i + 8 <= i1; i += 8) {
-                double x[8], d[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    x[u] = v[(i + u) * S];
-                    d[u] = __ldg(dinv + (i + u) * S);
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    prev = fwd(x[u], prev, qs, d[u]);
-                    v[(i + u) * S] = prev;
-                }
-            }
-            for (; i < i1; ++i) {
-                prev = fwd(v[i * S], prev, qs, __ldg(dinv + i * S));
-                v[i * S] = prev;
-            }
-        }
-    }
-
-    double next = prev;
-    const int last = a.nx - 1;
-    if (CLAMP && active && clamp_s) v[last * S] = clamp_v; // i = nx-1 is a face
-    for (int c = nch - 1; c >= 0; --c) {
-        const int i0 = c * kChunk;
-        const int itop = min(a.nx, i0 + kChunk) - 1;
-        if (active) {
-            int i = (c == nch - 1) ? itop - 1 : itop;
-            for (; i - 7 >= i0; i -= 8) {
-                double x[8], b[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    x[u] = v[(i - u) * S];
-                    b[u] = __ldg(cb + (i - u) * S);
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    next = bwd(x[u], next, b[u]);
-                    double out = next;
-                    if (CLAMP && clamp_s && (lane_face || (i - u) == 0)) out = clamp_v;
-                    v[(i - u) * S] = out;
-                }
-            }
-            for (; i >= i0; --i) {
-                next = bwd(v[i * S], next, __ldg(cb + i * S));
-                double out = next;
-                if (CLAMP && clamp_s && (lane_face || i == 0)) out = clamp_v;
-                v[i * S] = out;
-            }
-        }
-        if (BULK) {
-            ptx::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane < nl) {
-                const int cnt = itop - i0 + 1;
-                const int off = i0 * S;
-                ptx::bulk_s2g(base + static_cast<long long>(lane) * a.rowlen + off, tile + lane * a.pitch + off,
+    const Chain c = make_chain_x(a, tile, lane, line0, active);
+    auto wait = [&](int ch) {
+        if (BULK) ptx::mbar_wait(&bars[ch], 0);
+    };
+    auto flush = [&](int ch) {
+        if (!BULK) return;
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            const int i0 = ch * kChunk;
+            const int cnt = min(kChunk, a.nx - i0);
+            const int off = i0 * S;
+            for (int l = 0; l < nl; ++l)
+                ptx::bulk_s2g(base + static_cast<long long>(l) * a.rowlen + off, tile + l * a.pitch + off,
                               static_cast<uint32_t>(cnt * S * 8));
-                ptx::bulk_commit();
-            }
+            ptx::bulk_commit();
         }
-    }
+    };
+    solve_chain<CLAMP>(c, active, nch, wait, flush);
     if (BULK) {
-        ptx::bulk_wait_read_all();
+        if (lane == 0) ptx::bulk_wait_read_all();
     } else {
         __syncwarp();
         for (int idx = lane; idx < nl * a.rowlen; idx += kLanes) {

@@ -214,8 +214,10 @@ def test_errors_map_to_reference_categories():
     s = make_session(w)
     with pytest.raises(B.StateError):
         s.advance(3, w.dt * 2)  # dt must match the workspace (solver.hpp:57-68)
-    with pytest.raises(B.StateError):
-        s.set_workspace(0, 3, 0.01, [1.0], np.ones(11), np.ones(11))  # wrong n for the mesh
+    one = np.ones(11)
+    p = one.ctypes.data_as(B._P(B._d))
+    with pytest.raises(B.StateError):  # workspace line length != mesh axis (solver.cpp:333-335)
+        B._check(B.lib().biodiff_set_workspace(s._h, 0, 11, 3, 0.01, p, p, p))
     with pytest.raises(B.StateError):
         s.cell_sources_sinks_step(0.0)  # agents.cpp:514
     with pytest.raises(B.StateError):
