@@ -163,30 +163,75 @@ DeviceSession::~DeviceSession()
 
 void DeviceSession::choose_paths()
 {
+    // Per axis: the async tile kernel (TMA / bulk copies) with the register
+    // tail size that maximises resident chains per SM (occupancy API), else
+    // the plain shared-memory tile, else the global two-pass kernel.
+    // BIODIFF_SWEEP_PATH=global|smem|smem_plain and BIODIFF_RMAX force choices.
     const std::string force = env_or("BIODIFF_SWEEP_PATH", "auto");
-    const int limit = smem_limit_bytes();
+    const int force_rmax = std::atoi(env_or("BIODIFF_RMAX", "-1"));
     const int rowlen = mesh_.nx * S_;
     const bool aligned = (rowlen % 2) == 0;
+    constexpr int kMaxSmem = 227 * 1024;
     for (int ax = 0; ax < 3; ++ax) {
         const int n = ax == 0 ? mesh_.nx : ax == 1 ? mesh_.ny : mesh_.nz;
-        const int nch = (n + kernels::kChunk - 1) / kernels::kChunk;
-        long long bytes;
-        if (ax == 0) {
-            const int L = std::max(1, kernels::kLanes / S_);
-            const int pitch = ((rowlen + 15) / 16) * 16 + ((S_ + 1) / 2) * 2;
-            bytes = kernels::bar_bytes(nch) + static_cast<long long>(L) * pitch * 8;
-            if (S_ > kernels::kLanes) bytes = std::numeric_limits<long long>::max();
-        } else {
-            bytes = kernels::bar_bytes(nch) + static_cast<long long>(kernels::kLanes) * n * 8;
+        const bool fits_lanes = !(ax == 0 && S_ > kernels::kLanes);
+        const bool async_ok = fits_lanes && aligned && (ax == 0 || tmap_ok_[ax]);
+        int ns_plain = n;
+        const int plain_bytes = fits_lanes ? sweep_smem_bytes(ax, 0, &ns_plain) : kMaxSmem + 1;
+        int best_r = -1, best_chains = 0, best_ns = n;
+        if (async_ok && force != "smem_plain" && force != "global") {
+            for (int r : {0, 32, 64, 96}) {
+                if (force_rmax >= 0 && r != force_rmax) continue;
+                int ns = n;
+                const int bytes = sweep_smem_bytes(ax, r, &ns);
+                if (bytes > kMaxSmem) continue;
+                if (r > 0 && ns == n) continue; // no register tail: same as r = 0
+                int blocks = 0;
+                launch_tiled(ax, r, false, true, bytes, &blocks);
+                const int lanes = ax == 0 ? std::max(1, kernels::kLanes / S_) * S_ : kernels::kLanes;
+                const int chains = blocks * lanes;
+                if (chains > best_chains) {
+                    best_chains = chains;
+                    best_r = r;
+                    best_ns = ns;
+                }
+            }
         }
-        // y/z async path needs the TMA tensor map; x uses plain bulk copies.
-        const bool async_ok = aligned && (ax == 0 || tmap_ok_[ax]);
-        SweepPath p = bytes <= limit ? (async_ok ? SweepPath::smem_bulk : SweepPath::smem_plain) : SweepPath::global;
-        if (force == "global") p = SweepPath::global;
-        if (force == "smem" && bytes <= 227 * 1024) p = async_ok ? SweepPath::smem_bulk : SweepPath::smem_plain;
-        if (force == "smem_plain" && bytes <= 227 * 1024) p = SweepPath::smem_plain;
+        SweepPath p;
+        if (best_r >= 0 && (force == "auto" || force == "smem")) {
+            p = SweepPath::smem_bulk;
+            rmax_[ax] = best_r;
+            ns_[ax] = best_ns;
+        } else if (plain_bytes <= kMaxSmem && force != "global") {
+            p = SweepPath::smem_plain;
+            rmax_[ax] = 0;
+            ns_[ax] = n;
+        } else {
+            p = SweepPath::global;
+        }
         path_[ax] = p;
     }
+}
+
+// Shared memory of the tile kernels for a register tail of up to `rmax`
+// positions; *ns receives the positions kept in shared memory.
+int DeviceSession::sweep_smem_bytes(int axis, int rmax, int* ns) const
+{
+    const int n = axis == 0 ? mesh_.nx : axis == 1 ? mesh_.ny : mesh_.nz;
+    int keep = n;
+    if (rmax > 0) {
+        const int rest = n - rmax;
+        keep = rest <= 0 ? 0 : ((rest + kernels::kChunk - 1) / kernels::kChunk) * kernels::kChunk;
+        keep = std::min(keep, n);
+    }
+    *ns = keep;
+    const int nchs = (keep + kernels::kChunk - 1) / kernels::kChunk;
+    if (axis == 0) {
+        const int L = std::max(1, kernels::kLanes / S_);
+        const int pitch = ((keep * S_ + 15) / 16) * 16 + ((S_ + 1) / 2) * 2;
+        return kernels::bar_bytes(nchs) + L * pitch * 8;
+    }
+    return kernels::bar_bytes(nchs) + kernels::kLanes * nchs * kernels::kChunk * 8;
 }
 
 void DeviceSession::invalidate_graphs()
@@ -512,6 +557,13 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
     const kernels::Coef coef{w.q, w.dinv, w.cb, w.dconst, w.cconst, w.settle};
     const SweepPath p = path_[ax];
     begin_kernel(ax);
+    if (p == SweepPath::smem_bulk) {
+        int ns = 0;
+        const int smem = sweep_smem_bytes(ax, rmax_[ax], &ns);
+        launch_tiled(ax, rmax_[ax], do_clamp, false, smem, nullptr);
+        end_kernel(ax);
+        return;
+    }
     if (p == SweepPath::global) {
         kernels::GlobalSweep g{rho_, w.q, w.dinv, w.cb, ax, mesh_.nx, mesh_.ny, mesh_.nz, S, w.n, 0, cl};
         g.chains = mesh_.voxel_count() * S / w.n;
@@ -541,11 +593,10 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
             ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
             kern<<<static_cast<unsigned>(grid), kernels::kLanes, smem, st>>>(x);
         };
-        const bool bulk = p == SweepPath::smem_bulk;
         if (do_clamp)
-            bulk ? launch(kernels::sweep_x_smem<true, true>) : launch(kernels::sweep_x_smem<true, false>);
+            launch(kernels::sweep_x_smem<true, false, 0>);
         else
-            bulk ? launch(kernels::sweep_x_smem<false, true>) : launch(kernels::sweep_x_smem<false, false>);
+            launch(kernels::sweep_x_smem<false, false, 0>);
     } else {
         kernels::StridedSweep y{};
         y.rho = rho_;
@@ -568,24 +619,97 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
         y.S = S;
         y.nx = mesh_.nx;
         y.clamp = cl;
-        const int nch = (w.n + kernels::kChunk - 1) / kernels::kChunk;
+        y.ns = w.n;
         const long long grid = static_cast<long long>(y.tiles_per_row) * y.n_outer;
-        if (p == SweepPath::smem_bulk) {
-            const int smem = kernels::bar_bytes(nch) + kernels::kLanes * nch * kernels::kChunk * 8;
-            const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(tmap_[ax]);
-            auto launch = [&](auto kern) {
-                ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
-                kern<<<static_cast<unsigned>(grid), kernels::kLanes, smem, st>>>(tm, y);
-            };
-            do_clamp ? launch(kernels::sweep_yz_tma<true>) : launch(kernels::sweep_yz_tma<false>);
-        } else {
-            const int smem = kernels::kLanes * w.n * 8;
-            ck(cudaFuncSetAttribute(kernels::sweep_yz_plain, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-               "smem attr");
-            kernels::sweep_yz_plain<<<static_cast<unsigned>(grid), kernels::kLanes, smem, st>>>(y, do_clamp);
-        }
+        const int smem = kernels::kLanes * w.n * 8;
+        ck(cudaFuncSetAttribute(kernels::sweep_yz_plain, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+           "smem attr");
+        kernels::sweep_yz_plain<<<static_cast<unsigned>(grid), kernels::kLanes, smem, st>>>(y, do_clamp);
     }
     end_kernel(ax);
+}
+
+// The async tile kernels (x: bulk copies, y/z: TMA) with a register tail of
+// up to `rmax` positions. probe_only: report resident CTAs per SM instead.
+void DeviceSession::launch_tiled(int ax, int rmax, bool clamp, bool probe_only, int smem, int* blocks_per_sm)
+{
+    const DeviceWorkspace& w = ws_[ax];
+    auto st = static_cast<cudaStream_t>(stream_);
+    const int S = S_;
+    const int rowlen = mesh_.nx * S;
+    int ns = 0;
+    sweep_smem_bytes(ax, rmax, &ns);
+    kernels::Clamp cl{shell_values_, clamp ? shell_mask_ : 0ull};
+    const kernels::Coef coef{w.q, w.dinv, w.cb, w.dconst, w.cconst, w.settle};
+    auto go = [&](const void* fn, auto launch) {
+        ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
+        if (probe_only) {
+            ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, kernels::kLanes, smem), "occupancy");
+            return;
+        }
+        launch();
+    };
+    if (ax == 0) {
+        kernels::XSweep x{};
+        x.rho = rho_;
+        x.coef = coef;
+        x.lines = static_cast<long long>(mesh_.ny) * mesh_.nz;
+        x.nx = mesh_.nx;
+        x.ny = mesh_.ny;
+        x.nz = mesh_.nz;
+        x.S = S;
+        x.ns = ns;
+        x.rowlen = rowlen;
+        x.pitch = ((ns * S + 15) / 16) * 16 + ((S + 1) / 2) * 2;
+        x.L = std::max(1, kernels::kLanes / S);
+        x.clamp = cl;
+        const unsigned grid = static_cast<unsigned>((x.lines + x.L - 1) / x.L);
+        auto pick = [&](auto k) {
+            go(reinterpret_cast<const void*>(k), [&] { k<<<grid, kernels::kLanes, smem, st>>>(x); });
+        };
+        switch (rmax) {
+        case 0: clamp ? pick(kernels::sweep_x_smem<true, true, 0>) : pick(kernels::sweep_x_smem<false, true, 0>); break;
+        case 32: clamp ? pick(kernels::sweep_x_smem<true, true, 32>) : pick(kernels::sweep_x_smem<false, true, 32>); break;
+        case 64: clamp ? pick(kernels::sweep_x_smem<true, true, 64>) : pick(kernels::sweep_x_smem<false, true, 64>); break;
+        case 96: clamp ? pick(kernels::sweep_x_smem<true, true, 96>) : pick(kernels::sweep_x_smem<false, true, 96>); break;
+        default: throw state_error("unsupported register tail");
+        }
+        return;
+    }
+    kernels::StridedSweep y{};
+    y.rho = rho_;
+    y.coef = coef;
+    const long long row = rowlen;
+    const long long plane = row * mesh_.ny;
+    y.axis = ax;
+    if (ax == 1) {
+        y.stride = row;
+        y.outer_stride = plane;
+        y.n_outer = mesh_.nz;
+    } else {
+        y.stride = plane;
+        y.outer_stride = row;
+        y.n_outer = mesh_.ny;
+    }
+    y.n = w.n;
+    y.ns = ns;
+    y.rowlen = rowlen;
+    y.tiles_per_row = (rowlen + kernels::kLanes - 1) / kernels::kLanes;
+    y.S = S;
+    y.nx = mesh_.nx;
+    y.clamp = cl;
+    const unsigned grid = static_cast<unsigned>(static_cast<long long>(y.tiles_per_row) * y.n_outer);
+    const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(tmap_[ax]);
+    auto pick = [&](auto k) {
+        go(reinterpret_cast<const void*>(k), [&] { k<<<grid, kernels::kLanes, smem, st>>>(tm, y); });
+    };
+    switch (rmax) {
+    case 0: clamp ? pick(kernels::sweep_yz_tma<true, 0>) : pick(kernels::sweep_yz_tma<false, 0>); break;
+    case 32: clamp ? pick(kernels::sweep_yz_tma<true, 32>) : pick(kernels::sweep_yz_tma<false, 32>); break;
+    case 64: clamp ? pick(kernels::sweep_yz_tma<true, 64>) : pick(kernels::sweep_yz_tma<false, 64>); break;
+    case 96: clamp ? pick(kernels::sweep_yz_tma<true, 96>) : pick(kernels::sweep_yz_tma<false, 96>); break;
+    default: throw state_error("unsupported register tail");
+    }
 }
 
 void DeviceSession::launch_residual_dirichlet(bool all_entries)

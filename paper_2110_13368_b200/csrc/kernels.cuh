@@ -50,19 +50,27 @@ __device__ __forceinline__ double bwd(double v, double next, double cb) { return
 
 // Per-lane view of one chain (line x substrate) resident in shared memory:
 // element m lives at col[m*step].
+// Per-lane view of one chain (line x substrate). Positions [0, ns) live in
+// shared memory at col[m*step]; positions [ns, n) (at most RMAX of them)
+// live in registers, loaded from / stored to HBM at gcol[m*gstep].
+// Keeping the tail of every line in registers shrinks the shared-memory tile
+// so more chains are resident per SM (the recurrences are latency-bound:
+// 3 dependent FP64 ops per forward element, 2 per backward element).
 struct Chain {
     double* col;
     int step;
+    const double* gcol;
+    long long gstep;
     int S;
     const double* dinv; // coefficient column of this lane's substrate (stride S)
     const double* cb;
     double q, dc, cc;
-    int settle, n;
+    int settle, n, ns;
     bool clamp_s, face;
     double clamp_v;
 };
 
-// Forward elimination over positions [m0, m1) (m0 >= 1).
+// Forward elimination over shared-memory positions [m0, m1) (m0 >= 1).
 template <bool CONSTC>
 __device__ __forceinline__ double fwd_range(const Chain& c, int m0, int m1, double prev)
 {
@@ -87,8 +95,9 @@ __device__ __forceinline__ double fwd_range(const Chain& c, int m0, int m1, doub
     return prev;
 }
 
-// Back substitution over positions mtop down to m0 (inclusive), storing the
-// (optionally clamped) result while the recurrence carries the unclamped one.
+// Back substitution over shared-memory positions mtop down to m0, storing
+// the (optionally clamped) result while the recurrence carries the
+// unclamped one (the clamp happens after all sweeps, solver.cpp:380).
 template <bool CONSTC, bool CLAMP>
 __device__ __forceinline__ double bwd_range(const Chain& c, int mtop, int m0, double next)
 {
@@ -117,18 +126,33 @@ __device__ __forceinline__ double bwd_range(const Chain& c, int mtop, int m0, do
     return next;
 }
 
-// The full Thomas solve of one chain, chunk by chunk. wait(ch) blocks until
-// chunk ch has landed in shared memory; flush(ch) is called (by every lane,
-// after the chunk's final values are in shared memory) to write it back.
-template <bool CLAMP, class Wait, class Flush>
-__device__ __forceinline__ void solve_chain(const Chain& c, bool active, int nch, Wait wait, Flush flush)
+__device__ __forceinline__ double coef_at(const Chain& c, const double* arr, double cst, int m)
 {
-    const int n = c.n;
+    return (m >= c.settle && m < c.n - 1) ? cst : __ldg(arr + m * c.S);
+}
+
+// The full Thomas solve of one chain. wait(ch) blocks until shared-memory
+// chunk ch has landed; flush(ch) is called by every lane once the chunk's
+// final values are in shared memory, to write it back.
+template <bool CLAMP, int RMAX, class Wait, class Flush>
+__device__ __forceinline__ void solve_chain(const Chain& c, bool active, Wait wait, Flush flush)
+{
+    const int n = c.n, ns = c.ns;
+    const int R = n - ns; // register-resident positions (<= RMAX)
+    const int nchs = (ns + kChunk - 1) / kChunk;
+    double rv[RMAX > 0 ? RMAX : 1];
+    if (RMAX > 0 && active) {
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r)
+            if (r < R) rv[r] = __ldcs(c.gcol + static_cast<long long>(ns + r) * c.gstep);
+    }
+
+    // Forward elimination: shared-memory chunks, then the register tail.
     double prev = 0.0;
-    for (int ch = 0; ch < nch; ++ch) {
+    for (int ch = 0; ch < nchs; ++ch) {
         wait(ch);
         const int m0 = ch * kChunk;
-        const int m1 = min(n, m0 + kChunk);
+        const int m1 = min(ns, m0 + kChunk);
         if (active) {
             int m = m0;
             if (m == 0) {
@@ -142,12 +166,44 @@ __device__ __forceinline__ void solve_chain(const Chain& c, bool active, int nch
                 prev = fwd_range<false>(c, m, m1, prev);
         }
     }
-    double next = prev;
-    if (CLAMP && active && c.clamp_s) c.col[(n - 1) * c.step] = c.clamp_v; // position n-1 is always a face
-    for (int ch = nch - 1; ch >= 0; --ch) {
+    if (RMAX > 0 && active) {
+#pragma unroll
+        for (int r = 0; r < RMAX; ++r) {
+            if (r < R) {
+                const int m = ns + r;
+                const double d = coef_at(c, c.dinv, c.dc, m);
+                prev = (m == 0) ? fwd_first(rv[r], d) : fwd(rv[r], prev, c.q, d);
+                rv[r] = prev;
+            }
+        }
+    }
+
+    // Back substitution: register tail (stored straight to HBM), then the
+    // shared-memory chunks from the top.
+    double next = prev; // final value of position n-1
+    if (active) {
+        const double top = (CLAMP && c.clamp_s) ? c.clamp_v : next; // position n-1 is always a face
+        if (R > 0)
+            __stcs(const_cast<double*>(c.gcol) + static_cast<long long>(n - 1) * c.gstep, top);
+        else
+            c.col[(n - 1) * c.step] = top;
+    }
+    if (RMAX > 0 && active) {
+#pragma unroll
+        for (int r = RMAX - 1; r >= 0; --r) {
+            if (r < R - 1) {
+                const int m = ns + r;
+                next = bwd(rv[r], next, coef_at(c, c.cb, c.cc, m));
+                double out = next;
+                if (CLAMP && c.clamp_s && (c.face || m == 0)) out = c.clamp_v;
+                __stcs(const_cast<double*>(c.gcol) + static_cast<long long>(m) * c.gstep, out);
+            }
+        }
+    }
+    for (int ch = nchs - 1; ch >= 0; --ch) {
         const int m0 = ch * kChunk;
-        int mtop = min(n, m0 + kChunk) - 1;
-        if (ch == nch - 1) --mtop; // n-1 holds the final value already
+        int mtop = min(ns, m0 + kChunk) - 1;
+        if (R == 0 && ch == nchs - 1) --mtop; // n-1 already final
         if (active && mtop >= m0) {
             if (m0 >= c.settle)
                 next = bwd_range<true, CLAMP>(c, mtop, m0, next);
@@ -160,13 +216,14 @@ __device__ __forceinline__ void solve_chain(const Chain& c, bool active, int nch
 
 // ---------------------------------------------------------------------------
 // y / z sweep with TMA. A CTA (one warp) owns 32 contiguous doubles of one
-// row — 32 (i,s) chains — and the whole line along the sweep axis:
-// tile[m*32 + lane]. One elected lane issues 3-D tiled TMA loads of
-// 32 x 32-position boxes (one mbarrier each) so the forward recurrence starts
-// on the first box, and TMA stores each finished box during the backward
-// recurrence. HBM traffic: one read + one write per value; the line stays in
-// shared memory in between. Partial tiles at the row end / line end are
-// handled by TMA bounds (zero fill on load, clipped stores).
+// row — 32 (i,s) chains — and the whole line along the sweep axis. Line
+// positions [0, ns) sit in shared memory, tile[m*32 + lane]: one elected
+// lane issues 3-D tiled TMA loads of 32 x 32-position boxes (one mbarrier
+// each) so the forward recurrence starts on the first box, and TMA-stores
+// each finished box during the backward recurrence. Positions [ns, n) sit in
+// registers (coalesced 256-byte rows). HBM traffic: one read + one write per
+// value. Partial tiles at the row end / line end are handled by TMA bounds
+// (zero fill on load, clipped stores).
 // ---------------------------------------------------------------------------
 struct StridedSweep {
     double* rho;
@@ -175,6 +232,7 @@ struct StridedSweep {
     long long outer_stride; // doubles between consecutive outer indices
     int axis;               // 1 = y (outer k), 2 = z (outer j)
     int n;                  // line length
+    int ns;                 // positions kept in shared memory (multiple of kChunk, or n)
     int n_outer;            // number of outer indices (ny for z, nz for y)
     int rowlen;             // nx*S
     int tiles_per_row;
@@ -192,6 +250,8 @@ __device__ __forceinline__ Chain make_chain_yz(const StridedSweep& a, double* ti
     Chain c;
     c.col = tile + lane;
     c.step = kLanes;
+    c.gcol = a.rho + outer * a.outer_stride + e;
+    c.gstep = a.stride;
     c.S = a.S;
     c.dinv = a.coef.dinv + s;
     c.cb = a.coef.cb + s;
@@ -200,19 +260,20 @@ __device__ __forceinline__ Chain make_chain_yz(const StridedSweep& a, double* ti
     c.cc = a.coef.cconst[s];
     c.settle = a.coef.settle;
     c.n = a.n;
+    c.ns = a.ns;
     c.clamp_s = (a.clamp.mask >> s) & 1ull;
     c.clamp_v = c.clamp_s ? a.clamp.values[s] : 0.0;
     c.face = (i == 0 || i == a.nx - 1 || outer == 0 || outer == a.n_outer - 1);
     return c;
 }
 
-template <bool CLAMP>
+template <bool CLAMP, int RMAX>
 __global__ void __launch_bounds__(kLanes) sweep_yz_tma(const __grid_constant__ CUtensorMap tmap, StridedSweep a)
 {
     extern __shared__ __align__(128) unsigned char smem[];
-    const int nch = (a.n + kChunk - 1) / kChunk;
+    const int nchs = (a.ns + kChunk - 1) / kChunk;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
-    double* tile = reinterpret_cast<double*>(smem + bar_bytes(nch));
+    double* tile = reinterpret_cast<double*>(smem + bar_bytes(nchs));
     const int lane = threadIdx.x;
     const int et = static_cast<int>(blockIdx.x % a.tiles_per_row);
     const int outer = static_cast<int>(blockIdx.x / a.tiles_per_row);
@@ -228,11 +289,11 @@ __global__ void __launch_bounds__(kLanes) sweep_yz_tma(const __grid_constant__ C
             c2 = outer;
         }
     };
-    if (lane == 0) {
+    if (lane == 0 && nchs > 0) {
         ptx::tma_prefetch_desc(&tmap);
-        for (int ch = 0; ch < nch; ++ch) ptx::mbar_init(&bars[ch], 1);
+        for (int ch = 0; ch < nchs; ++ch) ptx::mbar_init(&bars[ch], 1);
         ptx::fence_mbar_init();
-        for (int ch = 0; ch < nch; ++ch) {
+        for (int ch = 0; ch < nchs; ++ch) {
             int c1, c2;
             coords(ch, c1, c2);
             ptx::mbar_arrive_expect_tx(&bars[ch], kLanes * kChunk * 8);
@@ -242,8 +303,8 @@ __global__ void __launch_bounds__(kLanes) sweep_yz_tma(const __grid_constant__ C
     __syncwarp();
     const bool active = lane < width;
     const Chain c = make_chain_yz(a, tile, lane, e0, outer, active);
-    solve_chain<CLAMP>(
-        c, active, nch, [&](int ch) { ptx::mbar_wait(&bars[ch], 0); },
+    solve_chain<CLAMP, RMAX>(
+        c, active, [&](int ch) { ptx::mbar_wait(&bars[ch], 0); },
         [&](int ch) {
             ptx::fence_proxy_async_smem();
             __syncwarp();
@@ -273,30 +334,33 @@ __global__ void __launch_bounds__(kLanes) sweep_yz_plain(StridedSweep a, bool cl
     for (int m = 0; m < a.n; ++m)
         if (active) tile[m * kLanes + lane] = base[m * a.stride + lane];
     __syncwarp();
-    const Chain c = make_chain_yz(a, tile, lane, e0, outer, active);
-    const int nch = (a.n + kChunk - 1) / kChunk;
+    StridedSweep b = a;
+    b.ns = a.n;
+    const Chain c = make_chain_yz(b, tile, lane, e0, outer, active);
     auto none = [](int) {};
     if (clamp)
-        solve_chain<true>(c, active, nch, none, none);
+        solve_chain<true, 0>(c, active, none, none);
     else
-        solve_chain<false>(c, active, nch, none, none);
+        solve_chain<false, 0>(c, active, none, none);
     __syncwarp();
     for (int m = 0; m < a.n; ++m)
         if (active) base[m * a.stride + lane] = tile[m * kLanes + lane];
 }
 
 // ---------------------------------------------------------------------------
-// x sweep, shared-memory resident tile of L whole x-lines (contiguous in
-// HBM). Lane -> (line l, substrate s); line l lives at
+// x sweep, tile of L whole x-lines (contiguous in HBM). Lane -> (line l,
+// substrate s). Positions [0, ns) sit in shared memory at
 // tile[l*pitch + i*S + s], pitch padded so the lanes of a half-warp hit
-// distinct banks. Lane 0 issues one bulk copy per (line, chunk) — 1 KB at
-// S=4 — and the stores of each finished chunk.
+// distinct banks; lane 0 issues one bulk copy per (line, chunk) — 1 KB at
+// S=4 — and the stores of each finished chunk. Positions [ns, nx) sit in
+// registers.
 // ---------------------------------------------------------------------------
 struct XSweep {
     double* rho;
     Coef coef;
     long long lines; // ny*nz
     int nx, ny, nz, S;
+    int ns;          // positions kept in shared memory (multiple of kChunk, or nx)
     int rowlen;      // nx*S
     int pitch;       // smem doubles per line
     int L;           // lines per tile (L*S <= 32)
@@ -312,6 +376,8 @@ __device__ __forceinline__ Chain make_chain_x(const XSweep& a, double* tile, int
     Chain c;
     c.col = tile + l * a.pitch + s;
     c.step = a.S;
+    c.gcol = a.rho + line * a.rowlen + s;
+    c.gstep = a.S;
     c.S = a.S;
     c.dinv = a.coef.dinv + s;
     c.cb = a.coef.cb + s;
@@ -320,19 +386,21 @@ __device__ __forceinline__ Chain make_chain_x(const XSweep& a, double* tile, int
     c.cc = a.coef.cconst[s];
     c.settle = a.coef.settle;
     c.n = a.nx;
+    c.ns = a.ns;
     c.clamp_s = (a.clamp.mask >> s) & 1ull;
     c.clamp_v = c.clamp_s ? a.clamp.values[s] : 0.0;
     c.face = (j == 0 || j == a.ny - 1 || k == 0 || k == a.nz - 1);
     return c;
 }
 
-template <bool CLAMP, bool BULK>
+template <bool CLAMP, bool BULK, int RMAX>
 __global__ void __launch_bounds__(kLanes) sweep_x_smem(XSweep a)
 {
     extern __shared__ __align__(128) unsigned char smem[];
-    const int nch = (a.nx + kChunk - 1) / kChunk;
+    const int ns = BULK ? a.ns : a.nx;
+    const int nchs = (ns + kChunk - 1) / kChunk;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
-    double* tile = reinterpret_cast<double*>(smem + bar_bytes(nch));
+    double* tile = reinterpret_cast<double*>(smem + bar_bytes(nchs));
     const int lane = threadIdx.x;
     const long long line0 = static_cast<long long>(blockIdx.x) * a.L;
     const int nl = static_cast<int>(min(static_cast<long long>(a.L), a.lines - line0));
@@ -340,11 +408,11 @@ __global__ void __launch_bounds__(kLanes) sweep_x_smem(XSweep a)
     double* base = a.rho + line0 * a.rowlen;
 
     if (BULK) {
-        if (lane == 0) {
-            for (int ch = 0; ch < nch; ++ch) ptx::mbar_init(&bars[ch], 1);
+        if (lane == 0 && nchs > 0) {
+            for (int ch = 0; ch < nchs; ++ch) ptx::mbar_init(&bars[ch], 1);
             ptx::fence_mbar_init();
-            for (int ch = 0; ch < nch; ++ch) {
-                const int cnt = min(kChunk, a.nx - ch * kChunk);
+            for (int ch = 0; ch < nchs; ++ch) {
+                const int cnt = min(kChunk, ns - ch * kChunk);
                 const int off = ch * kChunk * S;
                 ptx::mbar_arrive_expect_tx(&bars[ch], static_cast<uint32_t>(nl * cnt * S * 8));
                 for (int l = 0; l < nl; ++l)
@@ -362,7 +430,9 @@ __global__ void __launch_bounds__(kLanes) sweep_x_smem(XSweep a)
     }
 
     const bool active = lane < nl * S;
-    const Chain c = make_chain_x(a, tile, lane, line0, active);
+    XSweep b = a;
+    b.ns = ns;
+    const Chain c = make_chain_x(b, tile, lane, line0, active);
     auto wait = [&](int ch) {
         if (BULK) ptx::mbar_wait(&bars[ch], 0);
     };
@@ -372,7 +442,7 @@ __global__ void __launch_bounds__(kLanes) sweep_x_smem(XSweep a)
         __syncwarp();
         if (lane == 0) {
             const int i0 = ch * kChunk;
-            const int cnt = min(kChunk, a.nx - i0);
+            const int cnt = min(kChunk, ns - i0);
             const int off = i0 * S;
             for (int l = 0; l < nl; ++l)
                 ptx::bulk_s2g(base + static_cast<long long>(l) * a.rowlen + off, tile + l * a.pitch + off,
@@ -380,7 +450,7 @@ __global__ void __launch_bounds__(kLanes) sweep_x_smem(XSweep a)
             ptx::bulk_commit();
         }
     };
-    solve_chain<CLAMP>(c, active, nch, wait, flush);
+    solve_chain<CLAMP, BULK ? RMAX : 0>(c, active, wait, flush);
     if (BULK) {
         if (lane == 0) ptx::bulk_wait_read_all();
     } else {
