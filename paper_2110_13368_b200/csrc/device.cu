@@ -42,12 +42,6 @@ const char* env_or(const char* name, const char* dflt)
     return v ? v : dflt;
 }
 
-int smem_limit_bytes()
-{
-    // Per-CTA budget of the shared-memory tile paths: keep >= 2 CTAs per SM.
-    return std::atoi(env_or("BIODIFF_SMEM_MAX_KB", "100")) * 1024;
-}
-
 } // namespace
 
 int settle_row(int n, int S, const double* dinv, const double* cb, std::vector<double>& dconst,
@@ -114,6 +108,7 @@ DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int devi
     ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
     if (prop.major != 10)
         throw state_error(std::string("device ") + prop.name + " is not sm_100 (Blackwell B200); this build targets sm_100a only");
+    sm_count_ = prop.multiProcessorCount;
     cudaStream_t st;
     ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
     stream_ = st;
@@ -163,75 +158,42 @@ DeviceSession::~DeviceSession()
 
 void DeviceSession::choose_paths()
 {
-    // Per axis: the async tile kernel (TMA / bulk copies) with the register
-    // tail size that maximises resident chains per SM (occupancy API), else
-    // the plain shared-memory tile, else the global two-pass kernel.
-    // BIODIFF_SWEEP_PATH=global|smem|smem_plain and BIODIFF_RMAX force choices.
+    // Per axis: the async persistent tile kernel (x: bulk copies, y/z: TMA)
+    // when the line fits in shared memory and the rows are 16-byte aligned,
+    // else the plain whole-line tile, else the global two-pass kernel.
+    // BIODIFF_SWEEP_PATH=global|smem_plain forces a path (A/B measurements).
     const std::string force = env_or("BIODIFF_SWEEP_PATH", "auto");
-    const int force_rmax = std::atoi(env_or("BIODIFF_RMAX", "-1"));
     const int rowlen = mesh_.nx * S_;
     const bool aligned = (rowlen % 2) == 0;
     constexpr int kMaxSmem = 227 * 1024;
     for (int ax = 0; ax < 3; ++ax) {
-        const int n = ax == 0 ? mesh_.nx : ax == 1 ? mesh_.ny : mesh_.nz;
         const bool fits_lanes = !(ax == 0 && S_ > kernels::kLanes);
         const bool async_ok = fits_lanes && aligned && (ax == 0 || tmap_ok_[ax]);
-        int ns_plain = n;
-        const int plain_bytes = fits_lanes ? sweep_smem_bytes(ax, 0, &ns_plain) : kMaxSmem + 1;
-        int best_r = -1, best_chains = 0, best_ns = n;
-        if (async_ok && force != "smem_plain" && force != "global") {
-            for (int r : {0, 32, 64, 96}) {
-                if (force_rmax >= 0 && r != force_rmax) continue;
-                int ns = n;
-                const int bytes = sweep_smem_bytes(ax, r, &ns);
-                if (bytes > kMaxSmem) continue;
-                if (r > 0 && ns == n) continue; // no register tail: same as r = 0
-                int blocks = 0;
-                launch_tiled(ax, r, false, true, bytes, &blocks);
-                const int lanes = ax == 0 ? std::max(1, kernels::kLanes / S_) * S_ : kernels::kLanes;
-                const int chains = blocks * lanes;
-                if (chains > best_chains) {
-                    best_chains = chains;
-                    best_r = r;
-                    best_ns = ns;
-                }
-            }
-        }
-        SweepPath p;
-        if (best_r >= 0 && (force == "auto" || force == "smem")) {
+        const int bulk_bytes = sweep_smem_bytes(ax, true);
+        const int plain_bytes = sweep_smem_bytes(ax, false);
+        SweepPath p = SweepPath::global;
+        if (async_ok && bulk_bytes <= kMaxSmem && force != "smem_plain" && force != "global")
             p = SweepPath::smem_bulk;
-            rmax_[ax] = best_r;
-            ns_[ax] = best_ns;
-        } else if (plain_bytes <= kMaxSmem && force != "global") {
+        else if (fits_lanes && plain_bytes <= kMaxSmem && force != "global")
             p = SweepPath::smem_plain;
-            rmax_[ax] = 0;
-            ns_[ax] = n;
-        } else {
-            p = SweepPath::global;
-        }
         path_[ax] = p;
     }
 }
 
-// Shared memory of the tile kernels for a register tail of up to `rmax`
-// positions; *ns receives the positions kept in shared memory.
-int DeviceSession::sweep_smem_bytes(int axis, int rmax, int* ns) const
+// Dynamic shared memory of the tile kernels (bulk: chunk slots + mbarriers;
+// plain: whole lines).
+int DeviceSession::sweep_smem_bytes(int axis, bool bulk) const
 {
     const int n = axis == 0 ? mesh_.nx : axis == 1 ? mesh_.ny : mesh_.nz;
-    int keep = n;
-    if (rmax > 0) {
-        const int rest = n - rmax;
-        keep = rest <= 0 ? 0 : ((rest + kernels::kChunk - 1) / kernels::kChunk) * kernels::kChunk;
-        keep = std::min(keep, n);
-    }
-    *ns = keep;
-    const int nchs = (keep + kernels::kChunk - 1) / kernels::kChunk;
+    const int nch = (n + kernels::kChunk - 1) / kernels::kChunk;
+    const int pad = ((S_ + 1) / 2) * 2;
     if (axis == 0) {
         const int L = std::max(1, kernels::kLanes / S_);
-        const int pitch = ((keep * S_ + 15) / 16) * 16 + ((S_ + 1) / 2) * 2;
-        return kernels::bar_bytes(nchs) + L * pitch * 8;
+        if (bulk) return kernels::bar_bytes(nch) + nch * L * (kernels::kChunk * S_ + pad) * 8;
+        return L * (((n * S_ + 15) / 16) * 16 + pad) * 8;
     }
-    return kernels::bar_bytes(nchs) + kernels::kLanes * nchs * kernels::kChunk * 8;
+    if (bulk) return kernels::bar_bytes(nch) + nch * kernels::kChunk * kernels::kLanes * 8;
+    return kernels::kLanes * n * 8;
 }
 
 void DeviceSession::invalidate_graphs()
@@ -261,7 +223,8 @@ void DeviceSession::set_workspace(Axis axis, int n, int dims, double dt, const d
     w.dinv = dalloc_copy(dinv, static_cast<std::size_t>(n) * S_, st);
     w.cb = dalloc_copy(cb, static_cast<std::size_t>(n) * S_, st);
     std::vector<double> dc, cc;
-    w.settle = std::getenv("BIODIFF_NO_SETTLE") ? n : settle_row(n, S_, dinv, cb, dc, cc);
+    w.settle = settle_row(n, S_, dinv, cb, dc, cc);
+    if (std::getenv("BIODIFF_NO_SETTLE")) w.settle = n;
     w.dconst = dalloc_copy(dc.data(), dc.size(), st);
     w.cconst = dalloc_copy(cc.data(), cc.size(), st);
     ck(cudaStreamSynchronize(st), "sync"); // host staging vectors go out of scope
@@ -556,14 +519,8 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
     const bool do_clamp = clamp && shell_mask_ != 0;
     const kernels::Coef coef{w.q, w.dinv, w.cb, w.dconst, w.cconst, w.settle};
     const SweepPath p = path_[ax];
+    const bool bulk = p == SweepPath::smem_bulk;
     begin_kernel(ax);
-    if (p == SweepPath::smem_bulk) {
-        int ns = 0;
-        const int smem = sweep_smem_bytes(ax, rmax_[ax], &ns);
-        launch_tiled(ax, rmax_[ax], do_clamp, false, smem, nullptr);
-        end_kernel(ax);
-        return;
-    }
     if (p == SweepPath::global) {
         kernels::GlobalSweep g{rho_, w.q, w.dinv, w.cb, ax, mesh_.nx, mesh_.ny, mesh_.nz, S, w.n, 0, cl};
         g.chains = mesh_.voxel_count() * S / w.n;
@@ -573,81 +530,17 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
             kernels::sweep_global<true><<<static_cast<unsigned>(grid), block, 0, st>>>(g);
         else
             kernels::sweep_global<false><<<static_cast<unsigned>(grid), block, 0, st>>>(g);
-    } else if (ax == 0) {
-        kernels::XSweep x{};
-        x.rho = rho_;
-        x.coef = coef;
-        x.lines = static_cast<long long>(mesh_.ny) * mesh_.nz;
-        x.nx = mesh_.nx;
-        x.ny = mesh_.ny;
-        x.nz = mesh_.nz;
-        x.S = S;
-        x.rowlen = rowlen;
-        x.pitch = ((rowlen + 15) / 16) * 16 + ((S + 1) / 2) * 2;
-        x.L = std::max(1, kernels::kLanes / S);
-        x.clamp = cl;
-        const int nch = (mesh_.nx + kernels::kChunk - 1) / kernels::kChunk;
-        const int smem = kernels::bar_bytes(nch) + x.L * x.pitch * 8;
-        const long long grid = (x.lines + x.L - 1) / x.L;
-        auto launch = [&](auto kern) {
-            ck(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
-            kern<<<static_cast<unsigned>(grid), kernels::kLanes, smem, st>>>(x);
-        };
-        if (do_clamp)
-            launch(kernels::sweep_x_smem<true, false, 0>);
-        else
-            launch(kernels::sweep_x_smem<false, false, 0>);
-    } else {
-        kernels::StridedSweep y{};
-        y.rho = rho_;
-        y.coef = coef;
-        const long long row = rowlen;
-        const long long plane = row * mesh_.ny;
-        y.axis = ax;
-        if (ax == 1) {
-            y.stride = row;
-            y.outer_stride = plane;
-            y.n_outer = mesh_.nz;
-        } else {
-            y.stride = plane;
-            y.outer_stride = row;
-            y.n_outer = mesh_.ny;
-        }
-        y.n = w.n;
-        y.rowlen = rowlen;
-        y.tiles_per_row = (rowlen + kernels::kLanes - 1) / kernels::kLanes;
-        y.S = S;
-        y.nx = mesh_.nx;
-        y.clamp = cl;
-        y.ns = w.n;
-        const long long grid = static_cast<long long>(y.tiles_per_row) * y.n_outer;
-        const int smem = kernels::kLanes * w.n * 8;
-        ck(cudaFuncSetAttribute(kernels::sweep_yz_plain, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
-           "smem attr");
-        kernels::sweep_yz_plain<<<static_cast<unsigned>(grid), kernels::kLanes, smem, st>>>(y, do_clamp);
+        end_kernel(ax);
+        return;
     }
-    end_kernel(ax);
-}
-
-// The async tile kernels (x: bulk copies, y/z: TMA) with a register tail of
-// up to `rmax` positions. probe_only: report resident CTAs per SM instead.
-void DeviceSession::launch_tiled(int ax, int rmax, bool clamp, bool probe_only, int smem, int* blocks_per_sm)
-{
-    const DeviceWorkspace& w = ws_[ax];
-    auto st = static_cast<cudaStream_t>(stream_);
-    const int S = S_;
-    const int rowlen = mesh_.nx * S;
-    int ns = 0;
-    sweep_smem_bytes(ax, rmax, &ns);
-    kernels::Clamp cl{shell_values_, clamp ? shell_mask_ : 0ull};
-    const kernels::Coef coef{w.q, w.dinv, w.cb, w.dconst, w.cconst, w.settle};
-    auto go = [&](const void* fn, auto launch) {
+    const int smem = sweep_smem_bytes(ax, bulk);
+    // Persistent grid: as many CTAs as fit on the device at this smem size.
+    auto persistent_grid = [&](const void* fn, long long tiles) {
         ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
-        if (probe_only) {
-            ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fn, kernels::kLanes, smem), "occupancy");
-            return;
-        }
-        launch();
+        int per_sm = 0;
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kernels::kLanes, smem), "occupancy");
+        const long long g = static_cast<long long>(std::max(per_sm, 1)) * sm_count_;
+        return static_cast<unsigned>(std::min(g, tiles));
     };
     if (ax == 0) {
         kernels::XSweep x{};
@@ -658,58 +551,52 @@ void DeviceSession::launch_tiled(int ax, int rmax, bool clamp, bool probe_only, 
         x.ny = mesh_.ny;
         x.nz = mesh_.nz;
         x.S = S;
-        x.ns = ns;
         x.rowlen = rowlen;
-        x.pitch = ((ns * S + 15) / 16) * 16 + ((S + 1) / 2) * 2;
+        const int pad = ((S + 1) / 2) * 2;
+        x.cpitch = kernels::kChunk * S + pad;
+        x.pitch = ((rowlen + 15) / 16) * 16 + pad;
         x.L = std::max(1, kernels::kLanes / S);
+        x.tiles = (x.lines + x.L - 1) / x.L;
         x.clamp = cl;
-        const unsigned grid = static_cast<unsigned>((x.lines + x.L - 1) / x.L);
-        auto pick = [&](auto k) {
-            go(reinterpret_cast<const void*>(k), [&] { k<<<grid, kernels::kLanes, smem, st>>>(x); });
-        };
-        switch (rmax) {
-        case 0: clamp ? pick(kernels::sweep_x_smem<true, true, 0>) : pick(kernels::sweep_x_smem<false, true, 0>); break;
-        case 32: clamp ? pick(kernels::sweep_x_smem<true, true, 32>) : pick(kernels::sweep_x_smem<false, true, 32>); break;
-        case 64: clamp ? pick(kernels::sweep_x_smem<true, true, 64>) : pick(kernels::sweep_x_smem<false, true, 64>); break;
-        case 96: clamp ? pick(kernels::sweep_x_smem<true, true, 96>) : pick(kernels::sweep_x_smem<false, true, 96>); break;
-        default: throw state_error("unsupported register tail");
+        if (bulk) {
+            auto k = do_clamp ? kernels::sweep_x_bulk<true> : kernels::sweep_x_bulk<false>;
+            const unsigned grid = persistent_grid(reinterpret_cast<const void*>(k), x.tiles);
+            k<<<grid, kernels::kLanes, smem, st>>>(x);
+        } else {
+            ck(cudaFuncSetAttribute(kernels::sweep_x_plain, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+               "smem attr");
+            kernels::sweep_x_plain<<<static_cast<unsigned>(x.tiles), kernels::kLanes, smem, st>>>(x, do_clamp);
         }
+        end_kernel(ax);
         return;
     }
     kernels::StridedSweep y{};
     y.rho = rho_;
     y.coef = coef;
+    y.axis = ax;
     const long long row = rowlen;
     const long long plane = row * mesh_.ny;
-    y.axis = ax;
-    if (ax == 1) {
-        y.stride = row;
-        y.outer_stride = plane;
-        y.n_outer = mesh_.nz;
-    } else {
-        y.stride = plane;
-        y.outer_stride = row;
-        y.n_outer = mesh_.ny;
-    }
+    y.stride = ax == 1 ? row : plane;
+    y.outer_stride = ax == 1 ? plane : row;
+    y.n_outer = ax == 1 ? mesh_.nz : mesh_.ny;
     y.n = w.n;
-    y.ns = ns;
     y.rowlen = rowlen;
     y.tiles_per_row = (rowlen + kernels::kLanes - 1) / kernels::kLanes;
+    y.tiles = y.tiles_per_row * y.n_outer;
     y.S = S;
     y.nx = mesh_.nx;
     y.clamp = cl;
-    const unsigned grid = static_cast<unsigned>(static_cast<long long>(y.tiles_per_row) * y.n_outer);
-    const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(tmap_[ax]);
-    auto pick = [&](auto k) {
-        go(reinterpret_cast<const void*>(k), [&] { k<<<grid, kernels::kLanes, smem, st>>>(tm, y); });
-    };
-    switch (rmax) {
-    case 0: clamp ? pick(kernels::sweep_yz_tma<true, 0>) : pick(kernels::sweep_yz_tma<false, 0>); break;
-    case 32: clamp ? pick(kernels::sweep_yz_tma<true, 32>) : pick(kernels::sweep_yz_tma<false, 32>); break;
-    case 64: clamp ? pick(kernels::sweep_yz_tma<true, 64>) : pick(kernels::sweep_yz_tma<false, 64>); break;
-    case 96: clamp ? pick(kernels::sweep_yz_tma<true, 96>) : pick(kernels::sweep_yz_tma<false, 96>); break;
-    default: throw state_error("unsupported register tail");
+    if (bulk) {
+        const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(tmap_[ax]);
+        auto k = do_clamp ? kernels::sweep_yz_tma<true> : kernels::sweep_yz_tma<false>;
+        const unsigned grid = persistent_grid(reinterpret_cast<const void*>(k), y.tiles);
+        k<<<grid, kernels::kLanes, smem, st>>>(tm, y);
+    } else {
+        ck(cudaFuncSetAttribute(kernels::sweep_yz_plain, cudaFuncAttributeMaxDynamicSharedMemorySize, smem),
+           "smem attr");
+        kernels::sweep_yz_plain<<<static_cast<unsigned>(y.tiles), kernels::kLanes, smem, st>>>(y, do_clamp);
     }
+    end_kernel(ax);
 }
 
 void DeviceSession::launch_residual_dirichlet(bool all_entries)

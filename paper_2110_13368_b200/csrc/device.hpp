@@ -96,10 +96,8 @@ private:
     int dims_ = 0;
     double dt_ = 0.0;
     SweepPath path_[3] = {SweepPath::global, SweepPath::global, SweepPath::global};
-    int rmax_[3] = {0, 0, 0}; // register-tail capacity of the smem_bulk kernels (0/32/64/96)
-    int ns_[3] = {0, 0, 0};   // line positions kept in shared memory
-    int sweep_smem_bytes(int axis, int rmax, int* ns) const;
-    void launch_tiled(int axis, int rmax, bool clamp, bool probe_only, int smem, int* blocks_per_sm);
+    int sm_count_ = 148;
+    int sweep_smem_bytes(int axis, bool bulk) const;
 
     // Dirichlet: every entry (for apply_dirichlet), plus the split used by
     // the fused step: a per-substrate "whole boundary shell" rule evaluated in

@@ -50,63 +50,57 @@ __device__ __forceinline__ double bwd(double v, double next, double cb) { return
 
 // Per-lane view of one chain (line x substrate) resident in shared memory:
 // element m lives at col[m*step].
-// Per-lane view of one chain (line x substrate). Positions [0, ns) live in
-// shared memory at col[m*step]; positions [ns, n) (at most RMAX of them)
-// live in registers, loaded from / stored to HBM at gcol[m*gstep].
-// Keeping the tail of every line in registers shrinks the shared-memory tile
-// so more chains are resident per SM (the recurrences are latency-bound:
-// 3 dependent FP64 ops per forward element, 2 per backward element).
+// Per-lane constants of one chain (line x substrate).
 struct Chain {
-    double* col;
-    int step;
-    const double* gcol;
-    long long gstep;
     int S;
     const double* dinv; // coefficient column of this lane's substrate (stride S)
     const double* cb;
     double q, dc, cc;
-    int settle, n, ns;
+    int settle, n;
     bool clamp_s, face;
     double clamp_v;
 };
 
-// Forward elimination over shared-memory positions [m0, m1) (m0 >= 1).
+// Forward elimination over positions [m0, m1) (m0 >= 1); position m lives
+// at p[(m - m0) * step].
 template <bool CONSTC>
-__device__ __forceinline__ double fwd_range(const Chain& c, int m0, int m1, double prev)
+__device__ __forceinline__ double fwd_seg(const Chain& c, double* p, int step, int m0, int m1, double prev)
 {
     int m = m0;
-    for (; m + 8 <= m1; m += 8) {
+    for (; m + 8 <= m1; m += 8, p += 8 * step) {
         double v[8], d[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            v[u] = c.col[(m + u) * c.step];
+            v[u] = p[u * step];
             d[u] = CONSTC ? c.dc : __ldg(c.dinv + (m + u) * c.S);
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             prev = fwd(v[u], prev, c.q, d[u]);
-            c.col[(m + u) * c.step] = prev;
+            p[u * step] = prev;
         }
     }
-    for (; m < m1; ++m) {
-        prev = fwd(c.col[m * c.step], prev, c.q, CONSTC ? c.dc : __ldg(c.dinv + m * c.S));
-        c.col[m * c.step] = prev;
+    for (; m < m1; ++m, p += step) {
+        prev = fwd(*p, prev, c.q, CONSTC ? c.dc : __ldg(c.dinv + m * c.S));
+        *p = prev;
     }
     return prev;
 }
 
-// Back substitution over shared-memory positions mtop down to m0, storing
-// the (optionally clamped) result while the recurrence carries the
-// unclamped one (the clamp happens after all sweeps, solver.cpp:380).
+// Back substitution over positions mtop down to m0; position m lives at
+// p[(m - m0) * step]. Stores the (optionally clamped) result while the
+// recurrence carries the unclamped one: the clamp is applied after all
+// sweeps (solver.cpp:380), so it must not feed back into this sweep.
 template <bool CONSTC, bool CLAMP>
-__device__ __forceinline__ double bwd_range(const Chain& c, int mtop, int m0, double next)
+__device__ __forceinline__ double bwd_seg(const Chain& c, double* p, int step, int mtop, int m0, double next)
 {
     int m = mtop;
-    for (; m - 7 >= m0; m -= 8) {
+    double* q = p + (mtop - m0) * step;
+    for (; m - 7 >= m0; m -= 8, q -= 8 * step) {
         double v[8], b[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            v[u] = c.col[(m - u) * c.step];
+            v[u] = q[-u * step];
             b[u] = CONSTC ? c.cc : __ldg(c.cb + (m - u) * c.S);
         }
 #pragma unroll
@@ -114,352 +108,338 @@ __device__ __forceinline__ double bwd_range(const Chain& c, int mtop, int m0, do
             next = bwd(v[u], next, b[u]);
             double out = next;
             if (CLAMP && c.clamp_s && (c.face || (m - u) == 0)) out = c.clamp_v;
-            c.col[(m - u) * c.step] = out;
+            q[-u * step] = out;
         }
     }
-    for (; m >= m0; --m) {
-        next = bwd(c.col[m * c.step], next, CONSTC ? c.cc : __ldg(c.cb + m * c.S));
+    for (; m >= m0; --m, q -= step) {
+        next = bwd(*q, next, CONSTC ? c.cc : __ldg(c.cb + m * c.S));
         double out = next;
         if (CLAMP && c.clamp_s && (c.face || m == 0)) out = c.clamp_v;
-        c.col[m * c.step] = out;
+        *q = out;
     }
     return next;
 }
 
-__device__ __forceinline__ double coef_at(const Chain& c, const double* arr, double cst, int m)
+// The Thomas solve of one chain whose line is split in chunks of kChunk
+// positions; chunk k starts at ptr(k) (stride `step`). wait(k) blocks until
+// chunk k is in shared memory; flush(k) runs (on every lane) once chunk k
+// holds its final values.
+template <bool CLAMP, class Ptr, class Wait, class Flush>
+__device__ __forceinline__ void solve_chunked(const Chain& c, bool active, int step, Ptr ptr, Wait wait, Flush flush)
 {
-    return (m >= c.settle && m < c.n - 1) ? cst : __ldg(arr + m * c.S);
-}
-
-// The full Thomas solve of one chain. wait(ch) blocks until shared-memory
-// chunk ch has landed; flush(ch) is called by every lane once the chunk's
-// final values are in shared memory, to write it back.
-template <bool CLAMP, int RMAX, class Wait, class Flush>
-__device__ __forceinline__ void solve_chain(const Chain& c, bool active, Wait wait, Flush flush)
-{
-    const int n = c.n, ns = c.ns;
-    const int R = n - ns; // register-resident positions (<= RMAX)
-    const int nchs = (ns + kChunk - 1) / kChunk;
-    double rv[RMAX > 0 ? RMAX : 1];
-    if (RMAX > 0 && active) {
-#pragma unroll
-        for (int r = 0; r < RMAX; ++r)
-            if (r < R) rv[r] = __ldcs(c.gcol + static_cast<long long>(ns + r) * c.gstep);
-    }
-
-    // Forward elimination: shared-memory chunks, then the register tail.
+    const int n = c.n;
+    const int nch = (n + kChunk - 1) / kChunk;
     double prev = 0.0;
-    for (int ch = 0; ch < nchs; ++ch) {
-        wait(ch);
-        const int m0 = ch * kChunk;
-        const int m1 = min(ns, m0 + kChunk);
+    for (int k = 0; k < nch; ++k) {
+        wait(k);
+        const int m0 = k * kChunk;
+        const int m1 = min(n, m0 + kChunk);
         if (active) {
+            double* p = ptr(k);
             int m = m0;
             if (m == 0) {
-                prev = fwd_first(c.col[0], __ldg(c.dinv));
-                c.col[0] = prev;
+                prev = fwd_first(p[0], __ldg(c.dinv));
+                p[0] = prev;
                 m = 1;
+                p += step;
             }
             if (m >= c.settle && m1 <= n - 1)
-                prev = fwd_range<true>(c, m, m1, prev);
+                prev = fwd_seg<true>(c, p, step, m, m1, prev);
             else
-                prev = fwd_range<false>(c, m, m1, prev);
+                prev = fwd_seg<false>(c, p, step, m, m1, prev);
         }
     }
-    if (RMAX > 0 && active) {
-#pragma unroll
-        for (int r = 0; r < RMAX; ++r) {
-            if (r < R) {
-                const int m = ns + r;
-                const double d = coef_at(c, c.dinv, c.dc, m);
-                prev = (m == 0) ? fwd_first(rv[r], d) : fwd(rv[r], prev, c.q, d);
-                rv[r] = prev;
-            }
-        }
-    }
-
-    // Back substitution: register tail (stored straight to HBM), then the
-    // shared-memory chunks from the top.
-    double next = prev; // final value of position n-1
-    if (active) {
-        const double top = (CLAMP && c.clamp_s) ? c.clamp_v : next; // position n-1 is always a face
-        if (R > 0)
-            __stcs(const_cast<double*>(c.gcol) + static_cast<long long>(n - 1) * c.gstep, top);
-        else
-            c.col[(n - 1) * c.step] = top;
-    }
-    if (RMAX > 0 && active) {
-#pragma unroll
-        for (int r = RMAX - 1; r >= 0; --r) {
-            if (r < R - 1) {
-                const int m = ns + r;
-                next = bwd(rv[r], next, coef_at(c, c.cb, c.cc, m));
-                double out = next;
-                if (CLAMP && c.clamp_s && (c.face || m == 0)) out = c.clamp_v;
-                __stcs(const_cast<double*>(c.gcol) + static_cast<long long>(m) * c.gstep, out);
-            }
-        }
-    }
-    for (int ch = nchs - 1; ch >= 0; --ch) {
-        const int m0 = ch * kChunk;
-        int mtop = min(ns, m0 + kChunk) - 1;
-        if (R == 0 && ch == nchs - 1) --mtop; // n-1 already final
+    double next = prev; // final value of position n-1 (always a face)
+    if (CLAMP && active && c.clamp_s) ptr(nch - 1)[(n - 1 - (nch - 1) * kChunk) * step] = c.clamp_v;
+    for (int k = nch - 1; k >= 0; --k) {
+        const int m0 = k * kChunk;
+        int mtop = min(n, m0 + kChunk) - 1;
+        if (k == nch - 1) --mtop;
         if (active && mtop >= m0) {
             if (m0 >= c.settle)
-                next = bwd_range<true, CLAMP>(c, mtop, m0, next);
+                next = bwd_seg<true, CLAMP>(c, ptr(k), step, mtop, m0, next);
             else
-                next = bwd_range<false, CLAMP>(c, mtop, m0, next);
+                next = bwd_seg<false, CLAMP>(c, ptr(k), step, mtop, m0, next);
         }
-        flush(ch);
+        flush(k);
     }
 }
 
 // ---------------------------------------------------------------------------
-// y / z sweep with TMA. A CTA (one warp) owns 32 contiguous doubles of one
-// row — 32 (i,s) chains — and the whole line along the sweep axis. Line
-// positions [0, ns) sit in shared memory, tile[m*32 + lane]: one elected
-// lane issues 3-D tiled TMA loads of 32 x 32-position boxes (one mbarrier
-// each) so the forward recurrence starts on the first box, and TMA-stores
-// each finished box during the backward recurrence. Positions [ns, n) sit in
-// registers (coalesced 256-byte rows). HBM traffic: one read + one write per
-// value. Partial tiles at the row end / line end are handled by TMA bounds
-// (zero fill on load, clipped stores).
+// y / z sweep: persistent CTAs (one warp each, a few per SM) stream "tiles"
+// of 32 contiguous doubles of a row — 32 (i,s) chains — times the whole
+// line along the sweep axis. The line sits in shared memory as nch chunk
+// slots of 32 positions x 32 chains (8 KB), moved by 3-D tiled TMA
+// (UTMALDG / UTMASTG), one mbarrier per slot. HBM traffic: one read + one
+// write per value.
+//
+// Slot recycling: the back substitution finishes chunks top-down, and each
+// finished chunk's slot (once its TMA store has read it) immediately
+// receives the NEXT tile's chunk nch-1-k — the next tile's chunks therefore
+// arrive bottom-up while this tile is still being finished, and the next
+// forward pass starts without a cold-load bubble. Tiles alternate between
+// the identity and the reversed slot order.
 // ---------------------------------------------------------------------------
 struct StridedSweep {
     double* rho;
     Coef coef;
-    long long stride;       // doubles between consecutive positions along the axis
-    long long outer_stride; // doubles between consecutive outer indices
-    int axis;               // 1 = y (outer k), 2 = z (outer j)
-    int n;                  // line length
-    int ns;                 // positions kept in shared memory (multiple of kChunk, or n)
-    int n_outer;            // number of outer indices (ny for z, nz for y)
-    int rowlen;             // nx*S
+    int axis;    // 1 = y (outer k), 2 = z (outer j)
+    int n;       // line length
+    int n_outer; // number of outer indices (nz for y, ny for z)
+    int rowlen;  // nx*S
     int tiles_per_row;
+    int tiles;   // tiles_per_row * n_outer
     int S;
     int nx;
+    long long stride;       // (plain kernel) doubles between positions along the axis
+    long long outer_stride; // (plain kernel) doubles between outer indices
     Clamp clamp;
 };
 
-__device__ __forceinline__ Chain make_chain_yz(const StridedSweep& a, double* tile, int lane, int e0,
-                                               long long outer, bool active)
+__device__ __forceinline__ Chain make_chain(const Coef& coef, int S, int s, int n, const Clamp& cl, bool face)
 {
-    const int e = e0 + (active ? lane : 0);
-    const int s = e % a.S;
-    const int i = e / a.S;
     Chain c;
-    c.col = tile + lane;
-    c.step = kLanes;
-    c.gcol = a.rho + outer * a.outer_stride + e;
-    c.gstep = a.stride;
-    c.S = a.S;
-    c.dinv = a.coef.dinv + s;
-    c.cb = a.coef.cb + s;
-    c.q = a.coef.q[s];
-    c.dc = a.coef.dconst[s];
-    c.cc = a.coef.cconst[s];
-    c.settle = a.coef.settle;
-    c.n = a.n;
-    c.ns = a.ns;
-    c.clamp_s = (a.clamp.mask >> s) & 1ull;
-    c.clamp_v = c.clamp_s ? a.clamp.values[s] : 0.0;
-    c.face = (i == 0 || i == a.nx - 1 || outer == 0 || outer == a.n_outer - 1);
+    c.S = S;
+    c.dinv = coef.dinv + s;
+    c.cb = coef.cb + s;
+    c.q = coef.q[s];
+    c.dc = coef.dconst[s];
+    c.cc = coef.cconst[s];
+    c.settle = coef.settle;
+    c.n = n;
+    c.clamp_s = (cl.mask >> s) & 1ull;
+    c.clamp_v = c.clamp_s ? cl.values[s] : 0.0;
+    c.face = face;
     return c;
 }
 
-template <bool CLAMP, int RMAX>
+template <bool CLAMP>
 __global__ void __launch_bounds__(kLanes) sweep_yz_tma(const __grid_constant__ CUtensorMap tmap, StridedSweep a)
 {
     extern __shared__ __align__(128) unsigned char smem[];
-    const int nchs = (a.ns + kChunk - 1) / kChunk;
+    constexpr int kSlot = kChunk * kLanes; // doubles per slot
+    const int nch = (a.n + kChunk - 1) / kChunk;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
-    double* tile = reinterpret_cast<double*>(smem + bar_bytes(nchs));
+    double* slots = reinterpret_cast<double*>(smem + bar_bytes(nch));
     const int lane = threadIdx.x;
-    const int et = static_cast<int>(blockIdx.x % a.tiles_per_row);
-    const int outer = static_cast<int>(blockIdx.x / a.tiles_per_row);
-    const int e0 = et * kLanes;
-    const int width = min(kLanes, a.rowlen - e0);
-    // Tensor coordinates (dim0 = row element, dim1 = j, dim2 = k) of box ch.
-    auto coords = [&](int ch, int& c1, int& c2) {
-        if (a.axis == 2) {
-            c1 = outer;
-            c2 = ch * kChunk;
-        } else {
-            c1 = ch * kChunk;
-            c2 = outer;
-        }
+    int t = blockIdx.x;
+    if (t >= a.tiles) return;
+
+    // Box coordinates (dim0 = row element, dim1 = j, dim2 = k) of chunk k of tile t.
+    auto issue_load = [&](int tile, int k, int slot) {
+        const int e0 = (tile % a.tiles_per_row) * kLanes;
+        const int outer = tile / a.tiles_per_row;
+        const int c1 = a.axis == 2 ? outer : k * kChunk;
+        const int c2 = a.axis == 2 ? k * kChunk : outer;
+        ptx::mbar_arrive_expect_tx(&bars[slot], kSlot * 8);
+        ptx::tma_load_3d(slots + slot * kSlot, &tmap, e0, c1, c2, &bars[slot]);
     };
-    if (lane == 0 && nchs > 0) {
+    if (lane == 0) {
         ptx::tma_prefetch_desc(&tmap);
-        for (int ch = 0; ch < nchs; ++ch) ptx::mbar_init(&bars[ch], 1);
+        for (int k = 0; k < nch; ++k) ptx::mbar_init(&bars[k], 1);
         ptx::fence_mbar_init();
-        for (int ch = 0; ch < nchs; ++ch) {
-            int c1, c2;
-            coords(ch, c1, c2);
-            ptx::mbar_arrive_expect_tx(&bars[ch], kLanes * kChunk * 8);
-            ptx::tma_load_3d(tile + ch * kChunk * kLanes, &tmap, e0, c1, c2, &bars[ch]);
-        }
+        for (int k = 0; k < nch; ++k) issue_load(t, k, k);
     }
     __syncwarp();
-    const bool active = lane < width;
-    const Chain c = make_chain_yz(a, tile, lane, e0, outer, active);
-    solve_chain<CLAMP, RMAX>(
-        c, active, [&](int ch) { ptx::mbar_wait(&bars[ch], 0); },
-        [&](int ch) {
-            ptx::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-                int c1, c2;
-                coords(ch, c1, c2);
-                ptx::tma_store_3d(&tmap, e0, c1, c2, tile + ch * kChunk * kLanes);
-                ptx::bulk_commit();
-            }
-        });
-    if (lane == 0) ptx::bulk_wait_read_all();
+
+    for (int it = 0; t < a.tiles; ++it) {
+        const int tnext = t + gridDim.x;
+        const bool rev = it & 1;
+        const uint32_t phase = it & 1;
+        auto slot_of = [&](int k) { return rev ? nch - 1 - k : k; };
+        const int e0 = (t % a.tiles_per_row) * kLanes;
+        const int outer = t / a.tiles_per_row;
+        const int width = min(kLanes, a.rowlen - e0);
+        const bool active = lane < width;
+        const int e = e0 + (active ? lane : 0);
+        const int s = e % a.S, i = e / a.S;
+        const Chain c = make_chain(a.coef, a.S, s, a.n, a.clamp,
+                                   i == 0 || i == a.nx - 1 || outer == 0 || outer == a.n_outer - 1);
+        solve_chunked<CLAMP>(
+            c, active, kLanes, [&](int k) { return slots + slot_of(k) * kSlot + lane; },
+            [&](int k) { ptx::mbar_wait(&bars[slot_of(k)], phase); },
+            [&](int k) {
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    const int c1 = a.axis == 2 ? outer : k * kChunk;
+                    const int c2 = a.axis == 2 ? k * kChunk : outer;
+                    ptx::tma_store_3d(&tmap, e0, c1, c2, slots + slot_of(k) * kSlot);
+                    ptx::bulk_commit();
+                    if (tnext < a.tiles) {
+                        // The store of chunk k+1 (issued one step earlier) has
+                        // read its slot: recycle it for the next tile.
+                        if (k < nch - 1) {
+                            ptx::bulk_wait_read<1>();
+                            issue_load(tnext, nch - 1 - (k + 1), slot_of(k + 1));
+                        }
+                        if (k == 0) {
+                            ptx::bulk_wait_read<0>();
+                            issue_load(tnext, nch - 1, slot_of(0));
+                        }
+                    }
+                }
+            });
+        t = tnext;
+    }
+    if (lane == 0) ptx::bulk_wait_read<0>();
 }
 
-// Same tile without TMA (rows with an odd number of doubles cannot be
-// described by a tensor map: strides must be 16-byte multiples).
+// Whole line in shared memory without TMA (rows with an odd number of
+// doubles cannot be described by a tensor map: strides must be 16-byte
+// multiples). One tile per CTA.
 __global__ void __launch_bounds__(kLanes) sweep_yz_plain(StridedSweep a, bool clamp)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     double* tile = reinterpret_cast<double*>(smem);
     const int lane = threadIdx.x;
-    const int et = static_cast<int>(blockIdx.x % a.tiles_per_row);
+    const int e0 = static_cast<int>(blockIdx.x % a.tiles_per_row) * kLanes;
     const int outer = static_cast<int>(blockIdx.x / a.tiles_per_row);
-    const int e0 = et * kLanes;
     const int width = min(kLanes, a.rowlen - e0);
     double* base = a.rho + outer * a.outer_stride + e0;
     const bool active = lane < width;
     for (int m = 0; m < a.n; ++m)
         if (active) tile[m * kLanes + lane] = base[m * a.stride + lane];
     __syncwarp();
-    StridedSweep b = a;
-    b.ns = a.n;
-    const Chain c = make_chain_yz(b, tile, lane, e0, outer, active);
+    const int e = e0 + (active ? lane : 0);
+    const int s = e % a.S, i = e / a.S;
+    const Chain c = make_chain(a.coef, a.S, s, a.n, a.clamp,
+                               i == 0 || i == a.nx - 1 || outer == 0 || outer == a.n_outer - 1);
+    auto ptr = [&](int k) { return tile + k * kChunk * kLanes + lane; };
     auto none = [](int) {};
     if (clamp)
-        solve_chain<true, 0>(c, active, none, none);
+        solve_chunked<true>(c, active, kLanes, ptr, none, none);
     else
-        solve_chain<false, 0>(c, active, none, none);
+        solve_chunked<false>(c, active, kLanes, ptr, none, none);
     __syncwarp();
     for (int m = 0; m < a.n; ++m)
         if (active) base[m * a.stride + lane] = tile[m * kLanes + lane];
 }
 
 // ---------------------------------------------------------------------------
-// x sweep, tile of L whole x-lines (contiguous in HBM). Lane -> (line l,
-// substrate s). Positions [0, ns) sit in shared memory at
-// tile[l*pitch + i*S + s], pitch padded so the lanes of a half-warp hit
-// distinct banks; lane 0 issues one bulk copy per (line, chunk) — 1 KB at
-// S=4 — and the stores of each finished chunk. Positions [ns, nx) sit in
-// registers.
+// x sweep: persistent CTAs stream tiles of L whole x-lines (contiguous in
+// HBM). Lane -> (line l, substrate s). Chunk k (voxels 32k..32k+31 of every
+// line) sits in slot `slot_of(k)` as [l][cpitch], cpitch = 32*S padded so
+// the lanes of a half-warp hit distinct banks; lane 0 moves a chunk with one
+// bulk copy per line (1 KB at S=4). Same slot recycling as the y/z kernel.
 // ---------------------------------------------------------------------------
 struct XSweep {
     double* rho;
     Coef coef;
     long long lines; // ny*nz
+    long long tiles; // ceil(lines / L)
     int nx, ny, nz, S;
-    int ns;          // positions kept in shared memory (multiple of kChunk, or nx)
     int rowlen;      // nx*S
-    int pitch;       // smem doubles per line
+    int cpitch;      // smem doubles per line within a chunk slot
+    int pitch;       // (plain kernel) smem doubles per whole line
     int L;           // lines per tile (L*S <= 32)
     Clamp clamp;
 };
 
-__device__ __forceinline__ Chain make_chain_x(const XSweep& a, double* tile, int lane, long long line0, bool active)
-{
-    const int l = active ? lane / a.S : 0;
-    const int s = active ? lane % a.S : 0;
-    const long long line = line0 + l;
-    const int j = static_cast<int>(line % a.ny), k = static_cast<int>(line / a.ny);
-    Chain c;
-    c.col = tile + l * a.pitch + s;
-    c.step = a.S;
-    c.gcol = a.rho + line * a.rowlen + s;
-    c.gstep = a.S;
-    c.S = a.S;
-    c.dinv = a.coef.dinv + s;
-    c.cb = a.coef.cb + s;
-    c.q = a.coef.q[s];
-    c.dc = a.coef.dconst[s];
-    c.cc = a.coef.cconst[s];
-    c.settle = a.coef.settle;
-    c.n = a.nx;
-    c.ns = a.ns;
-    c.clamp_s = (a.clamp.mask >> s) & 1ull;
-    c.clamp_v = c.clamp_s ? a.clamp.values[s] : 0.0;
-    c.face = (j == 0 || j == a.ny - 1 || k == 0 || k == a.nz - 1);
-    return c;
-}
-
-template <bool CLAMP, bool BULK, int RMAX>
-__global__ void __launch_bounds__(kLanes) sweep_x_smem(XSweep a)
+template <bool CLAMP>
+__global__ void __launch_bounds__(kLanes) sweep_x_bulk(XSweep a)
 {
     extern __shared__ __align__(128) unsigned char smem[];
-    const int ns = BULK ? a.ns : a.nx;
-    const int nchs = (ns + kChunk - 1) / kChunk;
+    const int nch = (a.nx + kChunk - 1) / kChunk;
+    const int S = a.S;
+    const int slot_sz = a.L * a.cpitch;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
-    double* tile = reinterpret_cast<double*>(smem + bar_bytes(nchs));
+    double* slots = reinterpret_cast<double*>(smem + bar_bytes(nch));
+    const int lane = threadIdx.x;
+    long long t = blockIdx.x;
+    if (t >= a.tiles) return;
+
+    auto lines_in = [&](long long tile) {
+        return static_cast<int>(min(static_cast<long long>(a.L), a.lines - tile * a.L));
+    };
+    auto issue = [&](long long tile, int k, int slot, bool load) {
+        const int nl = lines_in(tile);
+        const int cnt = min(kChunk, a.nx - k * kChunk);
+        const int off = k * kChunk * S;
+        const uint32_t bytes = static_cast<uint32_t>(cnt * S * 8);
+        double* g = a.rho + tile * a.L * a.rowlen + off;
+        double* sm = slots + slot * slot_sz;
+        if (load) ptx::mbar_arrive_expect_tx(&bars[slot], nl * bytes);
+        for (int l = 0; l < nl; ++l) {
+            if (load)
+                ptx::bulk_g2s(sm + l * a.cpitch, g + static_cast<long long>(l) * a.rowlen, bytes, &bars[slot]);
+            else
+                ptx::bulk_s2g(g + static_cast<long long>(l) * a.rowlen, sm + l * a.cpitch, bytes);
+        }
+    };
+    if (lane == 0) {
+        for (int k = 0; k < nch; ++k) ptx::mbar_init(&bars[k], 1);
+        ptx::fence_mbar_init();
+        for (int k = 0; k < nch; ++k) issue(t, k, k, true);
+    }
+    __syncwarp();
+
+    for (int it = 0; t < a.tiles; ++it) {
+        const long long tnext = t + gridDim.x;
+        const bool rev = it & 1;
+        const uint32_t phase = it & 1;
+        auto slot_of = [&](int k) { return rev ? nch - 1 - k : k; };
+        const int nl = lines_in(t);
+        const bool active = lane < nl * S;
+        const int l = active ? lane / S : 0;
+        const int s = active ? lane % S : 0;
+        const long long line = t * a.L + l;
+        const int j = static_cast<int>(line % a.ny), kk = static_cast<int>(line / a.ny);
+        const Chain c = make_chain(a.coef, S, s, a.nx, a.clamp, j == 0 || j == a.ny - 1 || kk == 0 || kk == a.nz - 1);
+        solve_chunked<CLAMP>(
+            c, active, S, [&](int k) { return slots + slot_of(k) * slot_sz + l * a.cpitch + s; },
+            [&](int k) { ptx::mbar_wait(&bars[slot_of(k)], phase); },
+            [&](int k) {
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    issue(t, k, slot_of(k), false);
+                    ptx::bulk_commit();
+                    if (tnext < a.tiles) {
+                        if (k < nch - 1) {
+                            ptx::bulk_wait_read<1>();
+                            issue(tnext, nch - 1 - (k + 1), slot_of(k + 1), true);
+                        }
+                        if (k == 0) {
+                            ptx::bulk_wait_read<0>();
+                            issue(tnext, nch - 1, slot_of(0), true);
+                        }
+                    }
+                }
+            });
+        t = tnext;
+    }
+    if (lane == 0) ptx::bulk_wait_read<0>();
+}
+
+// Whole lines in shared memory without bulk copies (odd nx*S). One tile per CTA.
+__global__ void __launch_bounds__(kLanes) sweep_x_plain(XSweep a, bool clamp)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    double* tile = reinterpret_cast<double*>(smem);
     const int lane = threadIdx.x;
     const long long line0 = static_cast<long long>(blockIdx.x) * a.L;
     const int nl = static_cast<int>(min(static_cast<long long>(a.L), a.lines - line0));
     const int S = a.S;
     double* base = a.rho + line0 * a.rowlen;
-
-    if (BULK) {
-        if (lane == 0 && nchs > 0) {
-            for (int ch = 0; ch < nchs; ++ch) ptx::mbar_init(&bars[ch], 1);
-            ptx::fence_mbar_init();
-            for (int ch = 0; ch < nchs; ++ch) {
-                const int cnt = min(kChunk, ns - ch * kChunk);
-                const int off = ch * kChunk * S;
-                ptx::mbar_arrive_expect_tx(&bars[ch], static_cast<uint32_t>(nl * cnt * S * 8));
-                for (int l = 0; l < nl; ++l)
-                    ptx::bulk_g2s(tile + l * a.pitch + off, base + static_cast<long long>(l) * a.rowlen + off,
-                                  static_cast<uint32_t>(cnt * S * 8), &bars[ch]);
-            }
-        }
-        __syncwarp();
-    } else {
-        for (int idx = lane; idx < nl * a.rowlen; idx += kLanes) {
-            const int l = idx / a.rowlen, o = idx % a.rowlen;
-            tile[l * a.pitch + o] = base[idx];
-        }
-        __syncwarp();
-    }
-
+    for (int idx = lane; idx < nl * a.rowlen; idx += kLanes)
+        tile[(idx / a.rowlen) * a.pitch + idx % a.rowlen] = base[idx];
+    __syncwarp();
     const bool active = lane < nl * S;
-    XSweep b = a;
-    b.ns = ns;
-    const Chain c = make_chain_x(b, tile, lane, line0, active);
-    auto wait = [&](int ch) {
-        if (BULK) ptx::mbar_wait(&bars[ch], 0);
-    };
-    auto flush = [&](int ch) {
-        if (!BULK) return;
-        ptx::fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-            const int i0 = ch * kChunk;
-            const int cnt = min(kChunk, ns - i0);
-            const int off = i0 * S;
-            for (int l = 0; l < nl; ++l)
-                ptx::bulk_s2g(base + static_cast<long long>(l) * a.rowlen + off, tile + l * a.pitch + off,
-                              static_cast<uint32_t>(cnt * S * 8));
-            ptx::bulk_commit();
-        }
-    };
-    solve_chain<CLAMP, BULK ? RMAX : 0>(c, active, wait, flush);
-    if (BULK) {
-        if (lane == 0) ptx::bulk_wait_read_all();
-    } else {
-        __syncwarp();
-        for (int idx = lane; idx < nl * a.rowlen; idx += kLanes) {
-            const int ll = idx / a.rowlen, o = idx % a.rowlen;
-            base[idx] = tile[ll * a.pitch + o];
-        }
-    }
+    const int l = active ? lane / S : 0;
+    const int s = active ? lane % S : 0;
+    const long long line = line0 + l;
+    const int j = static_cast<int>(line % a.ny), kk = static_cast<int>(line / a.ny);
+    const Chain c = make_chain(a.coef, S, s, a.nx, a.clamp, j == 0 || j == a.ny - 1 || kk == 0 || kk == a.nz - 1);
+    auto ptr = [&](int k) { return tile + l * a.pitch + k * kChunk * S + s; };
+    auto none = [](int) {};
+    if (clamp)
+        solve_chunked<true>(c, active, S, ptr, none, none);
+    else
+        solve_chunked<false>(c, active, S, ptr, none, none);
+    __syncwarp();
+    for (int idx = lane; idx < nl * a.rowlen; idx += kLanes)
+        base[idx] = tile[(idx / a.rowlen) * a.pitch + idx % a.rowlen];
 }
 
 // ---------------------------------------------------------------------------
