@@ -172,12 +172,39 @@ void DeviceSession::choose_paths()
         const int bulk_bytes = sweep_smem_bytes(ax, true);
         const int plain_bytes = sweep_smem_bytes(ax, false);
         SweepPath p = SweepPath::global;
-        if (async_ok && bulk_bytes <= kMaxSmem && force != "smem_plain" && force != "global")
+        if (async_ok && ring_smem_bytes(ax) <= kMaxSmem && (force == "auto" || force == "ring"))
+            p = SweepPath::smem_ring;
+        else if (async_ok && bulk_bytes <= kMaxSmem && force != "smem_plain" && force != "global")
             p = SweepPath::smem_bulk;
         else if (fits_lanes && plain_bytes <= kMaxSmem && force != "global")
             p = SweepPath::smem_plain;
         path_[ax] = p;
     }
+}
+
+// Ring kernels: NS chunk slots (BIODIFF_RING_SLOTS, default 4) + mbarriers +
+// one checkpoint per chunk and lane.
+int DeviceSession::ring_slots(int axis) const
+{
+    const int n = axis == 0 ? mesh_.nx : axis == 1 ? mesh_.ny : mesh_.nz;
+    const int nch = (n + kernels::kChunk - 1) / kernels::kChunk;
+    const int want = std::max(2, std::atoi(env_or("BIODIFF_RING_SLOTS", "4")));
+    return std::min(nch, want);
+}
+
+int DeviceSession::ring_smem_bytes(int axis) const
+{
+    const int n = axis == 0 ? mesh_.nx : axis == 1 ? mesh_.ny : mesh_.nz;
+    const int nch = (n + kernels::kChunk - 1) / kernels::kChunk;
+    const int ns = ring_slots(axis);
+    int slot;
+    if (axis == 0) {
+        const int L = std::max(1, kernels::kLanes / S_);
+        slot = L * (kernels::kChunk * S_ + ((S_ + 1) / 2) * 2);
+    } else {
+        slot = kernels::kChunk * kernels::kLanes;
+    }
+    return kernels::bar_bytes(ns) + (ns * slot + nch * kernels::kLanes) * 8;
 }
 
 // Dynamic shared memory of the tile kernels (bulk: chunk slots + mbarriers;
@@ -533,7 +560,10 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
         end_kernel(ax);
         return;
     }
-    const int smem = sweep_smem_bytes(ax, bulk);
+    const bool ring = p == SweepPath::smem_ring;
+    const int smem = ring ? ring_smem_bytes(ax) : sweep_smem_bytes(ax, bulk);
+    const int n_ax = ax == 0 ? mesh_.nx : ax == 1 ? mesh_.ny : mesh_.nz;
+    const kernels::Ring rg{ring_slots(ax), (n_ax + kernels::kChunk - 1) / kernels::kChunk};
     // Persistent grid: as many CTAs as fit on the device at this smem size.
     auto persistent_grid = [&](const void* fn, long long tiles) {
         ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
@@ -558,7 +588,11 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
         x.L = std::max(1, kernels::kLanes / S);
         x.tiles = (x.lines + x.L - 1) / x.L;
         x.clamp = cl;
-        if (bulk) {
+        if (ring) {
+            auto k = do_clamp ? kernels::sweep_x_ring<true> : kernels::sweep_x_ring<false>;
+            ck(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
+            k<<<static_cast<unsigned>(x.tiles), kernels::kLanes, smem, st>>>(x, rg);
+        } else if (bulk) {
             auto k = do_clamp ? kernels::sweep_x_bulk<true> : kernels::sweep_x_bulk<false>;
             const unsigned grid = persistent_grid(reinterpret_cast<const void*>(k), x.tiles);
             k<<<grid, kernels::kLanes, smem, st>>>(x);
@@ -586,7 +620,12 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
     y.S = S;
     y.nx = mesh_.nx;
     y.clamp = cl;
-    if (bulk) {
+    if (ring) {
+        const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(tmap_[ax]);
+        auto k = do_clamp ? kernels::sweep_yz_ring<true> : kernels::sweep_yz_ring<false>;
+        ck(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
+        k<<<static_cast<unsigned>(y.tiles), kernels::kLanes, smem, st>>>(tm, y, rg);
+    } else if (bulk) {
         const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(tmap_[ax]);
         auto k = do_clamp ? kernels::sweep_yz_tma<true> : kernels::sweep_yz_tma<false>;
         const unsigned grid = persistent_grid(reinterpret_cast<const void*>(k), y.tiles);

@@ -30,7 +30,11 @@ struct DeviceWorkspace {
 
 // Which kernel implementation a sweep uses (chosen per axis at set-up; the
 // env var BIODIFF_SWEEP_PATH=smem|global forces one for A/B measurements).
-enum class SweepPath { smem_bulk, smem_plain, global };
+// smem_ring   : ring of chunk slots + backward recompute (default)
+// smem_bulk   : whole line resident in shared memory, persistent CTAs
+// smem_plain  : whole line resident, plain loads (rows not 16-byte aligned)
+// global      : one thread per chain straight from global memory
+enum class SweepPath { smem_ring, smem_bulk, smem_plain, global };
 
 // Host-side analysis of a workspace's coefficient columns: the first row
 // from which denom_inv and c_back are bit-constant up to row n-2 (max over
@@ -98,6 +102,8 @@ private:
     SweepPath path_[3] = {SweepPath::global, SweepPath::global, SweepPath::global};
     int sm_count_ = 148;
     int sweep_smem_bytes(int axis, bool bulk) const;
+    int ring_slots(int axis) const;
+    int ring_smem_bytes(int axis) const;
 
     // Dirichlet: every entry (for apply_dirichlet), plus the split used by
     // the fused step: a per-substrate "whole boundary shell" rule evaluated in

@@ -42,14 +42,22 @@ struct Coef {
 };
 
 __device__ __forceinline__ double fwd_first(double v, double d) { return __dmul_rn(v, d); }
+#ifndef BIODIFF_FMA
 __device__ __forceinline__ double fwd(double v, double prev, double q, double d)
 {
     return __dmul_rn(__dadd_rn(v, __dmul_rn(q, prev)), d);
 }
 __device__ __forceinline__ double bwd(double v, double next, double cb) { return __dadd_rn(v, __dmul_rn(cb, next)); }
+#else
+// Contracted variant (one rounding instead of two in v + q*prev and
+// v + cb*next): shorter dependent chains, not bit-identical to the reference.
+__device__ __forceinline__ double fwd(double v, double prev, double q, double d)
+{
+    return __dmul_rn(__fma_rn(q, prev, v), d);
+}
+__device__ __forceinline__ double bwd(double v, double next, double cb) { return __fma_rn(cb, next, v); }
+#endif
 
-// Per-lane view of one chain (line x substrate) resident in shared memory:
-// element m lives at col[m*step].
 // Per-lane constants of one chain (line x substrate).
 struct Chain {
     int S;
@@ -443,6 +451,210 @@ __global__ void __launch_bounds__(kLanes) sweep_x_plain(XSweep a, bool clamp)
 }
 
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// Ring-buffered sweeps with backward recompute (default tile path).
+//
+// The resident-line kernels above keep a whole line per chain in shared
+// memory, which caps residency at ~3 warps per SM (64 KB per 32 chains at
+// n = 256) and leaves the FP64 recurrences latency-bound. Here a warp keeps
+// only a ring of NS chunk slots (8 KB each) plus one checkpoint per chunk:
+//   forward : chunks stream through the ring (TMA / bulk loads, NS deep);
+//             the forward value at each chunk end is checkpointed;
+//   backward: the last NS chunks are still resident (their forward values
+//             are in the ring); every earlier chunk is reloaded (an L2 hit:
+//             it was read a few microseconds earlier) and its forward values
+//             recomputed from the previous chunk's checkpoint — the same
+//             operations in the same order, so the result is bit-identical —
+//             then back-substituted and stored.
+// HBM traffic stays one read + one write per value; L2 serves the reloads.
+// ---------------------------------------------------------------------------
+template <bool CLAMP, class Ptr, class Load, class Store>
+__device__ __forceinline__ void solve_ring(const Chain& c, bool active, int step, int NS, uint64_t* bars, double* ckpt,
+                                           int lane, Ptr ptr, Load load, Store store)
+{
+    const int n = c.n;
+    const int nch = (n + kChunk - 1) / kChunk;
+    uint32_t parity = 0; // expected phase parity per slot
+    auto wait_slot = [&](int s) {
+        ptx::mbar_wait(&bars[s], (parity >> s) & 1u);
+        parity ^= (1u << s);
+    };
+    if (lane == 0)
+        for (int k = 0; k < min(NS, nch); ++k) load(k, k);
+    __syncwarp();
+
+    // Forward elimination with per-chunk checkpoints.
+    double prev = 0.0;
+    for (int k = 0; k < nch; ++k) {
+        const int s = k % NS;
+        wait_slot(s);
+        const int m0 = k * kChunk;
+        const int m1 = min(n, m0 + kChunk);
+        if (active) {
+            double* p = ptr(s);
+            int m = m0;
+            if (m == 0) {
+                prev = fwd_first(p[0], __ldg(c.dinv));
+                p[0] = prev;
+                m = 1;
+                p += step;
+            }
+            if (m >= c.settle && m1 <= n - 1)
+                prev = fwd_seg<true>(c, p, step, m, m1, prev);
+            else
+                prev = fwd_seg<false>(c, p, step, m, m1, prev);
+            ckpt[k * kLanes + lane] = prev;
+        }
+        if (k + NS < nch) { // recycle the slot for chunk k+NS (chunk k will be recomputed)
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) load(k + NS, s);
+        }
+    }
+
+    // Back substitution, top chunk first.
+    double next = prev; // final value of position n-1 (always a face)
+    const int first_reloaded = nch - NS - 1; // highest chunk that must be reloaded
+    if (CLAMP && active && c.clamp_s) ptr((nch - 1) % NS)[((n - 1) - (nch - 1) * kChunk) * step] = c.clamp_v;
+    for (int k = nch - 1; k >= 0; --k) {
+        const int s = k % NS;
+        const int m0 = k * kChunk;
+        const int m1 = min(n, m0 + kChunk);
+        if (k <= first_reloaded) {
+            wait_slot(s);
+            if (active) { // recompute the forward values of chunk k
+                double* p = ptr(s);
+                int m = m0;
+                double f;
+                if (m == 0) {
+                    f = fwd_first(p[0], __ldg(c.dinv));
+                    p[0] = f;
+                    m = 1;
+                    p += step;
+                } else {
+                    f = ckpt[(k - 1) * kLanes + lane];
+                }
+                if (m >= c.settle && m1 <= n - 1)
+                    fwd_seg<true>(c, p, step, m, m1, f);
+                else
+                    fwd_seg<false>(c, p, step, m, m1, f);
+            }
+        }
+        int mtop = m1 - 1;
+        if (k == nch - 1) --mtop;
+        if (active && mtop >= m0) {
+            if (m0 >= c.settle)
+                next = bwd_seg<true, CLAMP>(c, ptr(s), step, mtop, m0, next);
+            else
+                next = bwd_seg<false, CLAMP>(c, ptr(s), step, mtop, m0, next);
+        }
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            store(k, s);
+            ptx::bulk_commit();
+            // The store of chunk k+1 (one step earlier) has read its slot by
+            // now: reload chunk k+1-NS into it for the recompute.
+            const int kr = k + 1 - NS;
+            if (k + 1 < nch && kr >= 0 && kr <= first_reloaded) {
+                ptx::bulk_wait_read<1>();
+                load(kr, kr % NS);
+            }
+        }
+    }
+    if (lane == 0) ptx::bulk_wait_read<0>();
+}
+
+struct Ring {
+    int ns;  // slots
+    int nch; // chunks per line
+};
+
+template <bool CLAMP>
+__global__ void __launch_bounds__(kLanes) sweep_yz_ring(const __grid_constant__ CUtensorMap tmap, StridedSweep a, Ring r)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    constexpr int kSlot = kChunk * kLanes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+    double* slots = reinterpret_cast<double*>(smem + bar_bytes(r.ns));
+    double* ckpt = slots + r.ns * kSlot;
+    const int lane = threadIdx.x;
+    const int t = blockIdx.x;
+    const int e0 = (t % a.tiles_per_row) * kLanes;
+    const int outer = t / a.tiles_per_row;
+    const int width = min(kLanes, a.rowlen - e0);
+    if (lane == 0) {
+        ptx::tma_prefetch_desc(&tmap);
+        for (int s = 0; s < r.ns; ++s) ptx::mbar_init(&bars[s], 1);
+        ptx::fence_mbar_init();
+    }
+    __syncwarp();
+    auto box = [&](int k, int& c1, int& c2) {
+        c1 = a.axis == 2 ? outer : k * kChunk;
+        c2 = a.axis == 2 ? k * kChunk : outer;
+    };
+    const bool active = lane < width;
+    const int e = e0 + (active ? lane : 0);
+    const int s = e % a.S, i = e / a.S;
+    const Chain c = make_chain(a.coef, a.S, s, a.n, a.clamp,
+                               i == 0 || i == a.nx - 1 || outer == 0 || outer == a.n_outer - 1);
+    solve_ring<CLAMP>(
+        c, active, kLanes, r.ns, bars, ckpt, lane, [&](int slot) { return slots + slot * kSlot + lane; },
+        [&](int k, int slot) {
+            int c1, c2;
+            box(k, c1, c2);
+            ptx::mbar_arrive_expect_tx(&bars[slot], kSlot * 8);
+            ptx::tma_load_3d(slots + slot * kSlot, &tmap, e0, c1, c2, &bars[slot]);
+        },
+        [&](int k, int slot) {
+            int c1, c2;
+            box(k, c1, c2);
+            ptx::tma_store_3d(&tmap, e0, c1, c2, slots + slot * kSlot);
+        });
+}
+
+template <bool CLAMP>
+__global__ void __launch_bounds__(kLanes) sweep_x_ring(XSweep a, Ring r)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int S = a.S;
+    const int slot_sz = a.L * a.cpitch;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+    double* slots = reinterpret_cast<double*>(smem + bar_bytes(r.ns));
+    double* ckpt = slots + r.ns * slot_sz;
+    const int lane = threadIdx.x;
+    const long long t = blockIdx.x;
+    const int nl = static_cast<int>(min(static_cast<long long>(a.L), a.lines - t * a.L));
+    if (lane == 0) {
+        for (int s = 0; s < r.ns; ++s) ptx::mbar_init(&bars[s], 1);
+        ptx::fence_mbar_init();
+    }
+    __syncwarp();
+    double* gbase = a.rho + t * a.L * a.rowlen;
+    const bool active = lane < nl * S;
+    const int l = active ? lane / S : 0;
+    const int sub = active ? lane % S : 0;
+    const long long line = t * a.L + l;
+    const int j = static_cast<int>(line % a.ny), kk = static_cast<int>(line / a.ny);
+    const Chain c = make_chain(a.coef, S, sub, a.nx, a.clamp, j == 0 || j == a.ny - 1 || kk == 0 || kk == a.nz - 1);
+    auto bytes_of = [&](int k) { return static_cast<uint32_t>(min(kChunk, a.nx - k * kChunk) * S * 8); };
+    solve_ring<CLAMP>(
+        c, active, S, r.ns, bars, ckpt, lane, [&](int slot) { return slots + slot * slot_sz + l * a.cpitch + sub; },
+        [&](int k, int slot) {
+            const uint32_t bytes = bytes_of(k);
+            ptx::mbar_arrive_expect_tx(&bars[slot], nl * bytes);
+            for (int ll = 0; ll < nl; ++ll)
+                ptx::bulk_g2s(slots + slot * slot_sz + ll * a.cpitch,
+                              gbase + static_cast<long long>(ll) * a.rowlen + k * kChunk * S, bytes, &bars[slot]);
+        },
+        [&](int k, int slot) {
+            const uint32_t bytes = bytes_of(k);
+            for (int ll = 0; ll < nl; ++ll)
+                ptx::bulk_s2g(gbase + static_cast<long long>(ll) * a.rowlen + k * kChunk * S,
+                              slots + slot * slot_sz + ll * a.cpitch, bytes);
+        });
+}
+
 // Any-axis sweep straight from global memory, one thread per chain. Used for
 // lines too long for a shared-memory tile. The forward intermediates are
 // written in place and re-read by the backward pass (L2-resident when the

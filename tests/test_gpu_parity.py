@@ -25,8 +25,15 @@ def _need_gpu():
 
 
 def _paths(monkeypatch, path):
+    """Selects a sweep kernel family (read at session creation): auto = ring
+    (4 slots), ringN = ring with N slots (more recompute), resident = whole
+    line in shared memory, smem_plain, global."""
+    monkeypatch.delenv("BIODIFF_RING_SLOTS", raising=False)
     if path == "auto":
         monkeypatch.delenv("BIODIFF_SWEEP_PATH", raising=False)
+    elif path.startswith("ring"):
+        monkeypatch.setenv("BIODIFF_SWEEP_PATH", "ring")
+        monkeypatch.setenv("BIODIFF_RING_SLOTS", path[4:])
     else:
         monkeypatch.setenv("BIODIFF_SWEEP_PATH", path)
 
@@ -38,7 +45,7 @@ SWEEP_SHAPES = [
 ]
 
 
-@pytest.mark.parametrize("path", ["auto", "global", "smem", "smem_plain"])
+@pytest.mark.parametrize("path", ["auto", "ring2", "ring3", "resident", "global", "smem_plain"])
 @pytest.mark.parametrize("shape,S", SWEEP_SHAPES)
 def test_single_sweep_bitwise(shape, S, path, monkeypatch):
     """diffusion_sweep (solver.cpp:330-347) along every active axis, every kernel path."""
@@ -59,7 +66,7 @@ def test_single_sweep_bitwise(shape, S, path, monkeypatch):
 
 
 @pytest.mark.parametrize("name", golden_names())
-@pytest.mark.parametrize("path", ["auto", "global"])
+@pytest.mark.parametrize("path", ["auto", "ring2", "resident", "global"])
 def test_golden_fixture_bitwise(name, path, monkeypatch):
     """Full runs vs the reference's own outputs (tests/golden, made by oracle/_ref)."""
     _paths(monkeypatch, path)
