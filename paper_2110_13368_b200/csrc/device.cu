@@ -188,7 +188,7 @@ int DeviceSession::ring_slots(int axis) const
 {
     const int n = axis == 0 ? mesh_.nx : axis == 1 ? mesh_.ny : mesh_.nz;
     const int nch = (n + kernels::kChunk - 1) / kernels::kChunk;
-    const int want = std::max(2, std::atoi(env_or("BIODIFF_RING_SLOTS", "4")));
+    const int want = std::max(2, std::atoi(env_or("BIODIFF_RING_SLOTS", "3")));
     return std::min(nch, want);
 }
 
@@ -563,7 +563,8 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
     const bool ring = p == SweepPath::smem_ring;
     const int smem = ring ? ring_smem_bytes(ax) : sweep_smem_bytes(ax, bulk);
     const int n_ax = ax == 0 ? mesh_.nx : ax == 1 ? mesh_.ny : mesh_.nz;
-    const kernels::Ring rg{ring_slots(ax), (n_ax + kernels::kChunk - 1) / kernels::kChunk};
+    const kernels::Ring rg{ring_slots(ax), (n_ax + kernels::kChunk - 1) / kernels::kChunk,
+                           std::atoi(env_or("BIODIFF_L2_HINTS", "1"))};
     // Persistent grid: as many CTAs as fit on the device at this smem size.
     auto persistent_grid = [&](const void* fn, long long tiles) {
         ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");

@@ -479,8 +479,10 @@ __device__ __forceinline__ void solve_ring(const Chain& c, bool active, int step
         ptx::mbar_wait(&bars[s], (parity >> s) & 1u);
         parity ^= (1u << s);
     };
+    // Forward loads of chunks that will be reloaded are kept in L2
+    // (evict_last); everything else streams (evict_first).
     if (lane == 0)
-        for (int k = 0; k < min(NS, nch); ++k) load(k, k);
+        for (int k = 0; k < min(NS, nch); ++k) load(k, k, k < nch - NS);
     __syncwarp();
 
     // Forward elimination with per-chunk checkpoints.
@@ -508,7 +510,7 @@ __device__ __forceinline__ void solve_ring(const Chain& c, bool active, int step
         if (k + NS < nch) { // recycle the slot for chunk k+NS (chunk k will be recomputed)
             ptx::fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) load(k + NS, s);
+            if (lane == 0) load(k + NS, s, k + NS < nch - NS);
         }
     }
 
@@ -558,7 +560,7 @@ __device__ __forceinline__ void solve_ring(const Chain& c, bool active, int step
             const int kr = k + 1 - NS;
             if (k + 1 < nch && kr >= 0 && kr <= first_reloaded) {
                 ptx::bulk_wait_read<1>();
-                load(kr, kr % NS);
+                load(kr, kr % NS, false);
             }
         }
     }
@@ -566,8 +568,9 @@ __device__ __forceinline__ void solve_ring(const Chain& c, bool active, int step
 }
 
 struct Ring {
-    int ns;  // slots
-    int nch; // chunks per line
+    int ns;    // slots
+    int nch;   // chunks per line
+    int hints; // use L2 eviction-priority hints
 };
 
 template <bool CLAMP>
@@ -598,18 +601,25 @@ __global__ void __launch_bounds__(kLanes) sweep_yz_ring(const __grid_constant__ 
     const int s = e % a.S, i = e / a.S;
     const Chain c = make_chain(a.coef, a.S, s, a.n, a.clamp,
                                i == 0 || i == a.nx - 1 || outer == 0 || outer == a.n_outer - 1);
+    const uint64_t keep_pol = ptx::policy_evict_last(), stream_pol = ptx::policy_evict_first();
     solve_ring<CLAMP>(
         c, active, kLanes, r.ns, bars, ckpt, lane, [&](int slot) { return slots + slot * kSlot + lane; },
-        [&](int k, int slot) {
+        [&](int k, int slot, bool keep) {
             int c1, c2;
             box(k, c1, c2);
             ptx::mbar_arrive_expect_tx(&bars[slot], kSlot * 8);
-            ptx::tma_load_3d(slots + slot * kSlot, &tmap, e0, c1, c2, &bars[slot]);
+            if (r.hints)
+                ptx::tma_load_3d_hint(slots + slot * kSlot, &tmap, e0, c1, c2, &bars[slot], keep ? keep_pol : stream_pol);
+            else
+                ptx::tma_load_3d(slots + slot * kSlot, &tmap, e0, c1, c2, &bars[slot]);
         },
         [&](int k, int slot) {
             int c1, c2;
             box(k, c1, c2);
-            ptx::tma_store_3d(&tmap, e0, c1, c2, slots + slot * kSlot);
+            if (r.hints)
+                ptx::tma_store_3d_hint(&tmap, e0, c1, c2, slots + slot * kSlot, stream_pol);
+            else
+                ptx::tma_store_3d(&tmap, e0, c1, c2, slots + slot * kSlot);
         });
 }
 
@@ -637,21 +647,33 @@ __global__ void __launch_bounds__(kLanes) sweep_x_ring(XSweep a, Ring r)
     const long long line = t * a.L + l;
     const int j = static_cast<int>(line % a.ny), kk = static_cast<int>(line / a.ny);
     const Chain c = make_chain(a.coef, S, sub, a.nx, a.clamp, j == 0 || j == a.ny - 1 || kk == 0 || kk == a.nz - 1);
+    const uint64_t keep_pol = ptx::policy_evict_last(), stream_pol = ptx::policy_evict_first();
     auto bytes_of = [&](int k) { return static_cast<uint32_t>(min(kChunk, a.nx - k * kChunk) * S * 8); };
     solve_ring<CLAMP>(
         c, active, S, r.ns, bars, ckpt, lane, [&](int slot) { return slots + slot * slot_sz + l * a.cpitch + sub; },
-        [&](int k, int slot) {
+        [&](int k, int slot, bool keep) {
             const uint32_t bytes = bytes_of(k);
             ptx::mbar_arrive_expect_tx(&bars[slot], nl * bytes);
-            for (int ll = 0; ll < nl; ++ll)
-                ptx::bulk_g2s(slots + slot * slot_sz + ll * a.cpitch,
-                              gbase + static_cast<long long>(ll) * a.rowlen + k * kChunk * S, bytes, &bars[slot]);
+            const uint64_t pol = keep ? keep_pol : stream_pol;
+            for (int ll = 0; ll < nl; ++ll) {
+                double* d = slots + slot * slot_sz + ll * a.cpitch;
+                const double* g = gbase + static_cast<long long>(ll) * a.rowlen + k * kChunk * S;
+                if (r.hints)
+                    ptx::bulk_g2s_hint(d, g, bytes, &bars[slot], pol);
+                else
+                    ptx::bulk_g2s(d, g, bytes, &bars[slot]);
+            }
         },
         [&](int k, int slot) {
             const uint32_t bytes = bytes_of(k);
-            for (int ll = 0; ll < nl; ++ll)
-                ptx::bulk_s2g(gbase + static_cast<long long>(ll) * a.rowlen + k * kChunk * S,
-                              slots + slot * slot_sz + ll * a.cpitch, bytes);
+            for (int ll = 0; ll < nl; ++ll) {
+                double* g = gbase + static_cast<long long>(ll) * a.rowlen + k * kChunk * S;
+                const double* d = slots + slot * slot_sz + ll * a.cpitch;
+                if (r.hints)
+                    ptx::bulk_s2g_hint(g, d, bytes, stream_pol);
+                else
+                    ptx::bulk_s2g(g, d, bytes);
+            }
         });
 }
 
