@@ -564,7 +564,7 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
     const int smem = ring ? ring_smem_bytes(ax) : sweep_smem_bytes(ax, bulk);
     const int n_ax = ax == 0 ? mesh_.nx : ax == 1 ? mesh_.ny : mesh_.nz;
     const kernels::Ring rg{ring_slots(ax), (n_ax + kernels::kChunk - 1) / kernels::kChunk,
-                           std::atoi(env_or("BIODIFF_L2_HINTS", "1"))};
+                           std::atoi(env_or("BIODIFF_L2_HINTS", "0"))};
     // Persistent grid: as many CTAs as fit on the device at this smem size.
     auto persistent_grid = [&](const void* fn, long long tiles) {
         ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
