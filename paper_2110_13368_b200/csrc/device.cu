@@ -146,6 +146,8 @@ DeviceSession::~DeviceSession()
     dfree(agent_secretion_);
     dfree(agent_uptake_);
     dfree(agent_saturation_);
+    dfree(agent_add_);
+    dfree(agent_den_);
     for (auto& pe : pending_events_) {
         cudaEventDestroy(static_cast<cudaEvent_t>(pe.second.first));
         cudaEventDestroy(static_cast<cudaEvent_t>(pe.second.second));
@@ -382,7 +384,14 @@ void DeviceSession::set_agents(const AgentPopulation& agents)
     gv.reserve(groups.size());
     go.reserve(groups.size() + 1);
     std::int64_t m = 0;
-    for (const auto& [voxel, idxs] : groups) {
+    // Longest groups first (dense tumour cores): distinct voxels commute, so
+    // the group order is free; it only shortens the kernel's tail.
+    std::vector<std::size_t> gorder(groups.size());
+    for (std::size_t g = 0; g < gorder.size(); ++g) gorder[g] = g;
+    std::stable_sort(gorder.begin(), gorder.end(),
+                     [&](std::size_t a, std::size_t b) { return groups[a].second.size() > groups[b].second.size(); });
+    for (std::size_t gi : gorder) {
+        const auto& [voxel, idxs] = groups[gi];
         if (voxel < 0 || voxel >= mesh_.voxel_count())
             throw state_error("agent voxel " + std::to_string(voxel) + " outside the mesh; rebuild the voxel grouping");
         gv.push_back(voxel);
@@ -407,6 +416,9 @@ void DeviceSession::set_agents(const AgentPopulation& agents)
     dfree(agent_secretion_);
     dfree(agent_uptake_);
     dfree(agent_saturation_);
+    dfree(agent_add_);
+    dfree(agent_den_);
+    factors_valid_ = false;
     groups_ = static_cast<std::int64_t>(gv.size());
     n_agents_ = m;
     group_voxel_ = dalloc_copy(gv.data(), gv.size(), st);
@@ -415,6 +427,10 @@ void DeviceSession::set_agents(const AgentPopulation& agents)
     agent_secretion_ = dalloc_copy(sec.data(), sec.size(), st);
     agent_uptake_ = dalloc_copy(upt.data(), upt.size(), st);
     agent_saturation_ = dalloc_copy(sat.data(), sat.size(), st);
+    if (m > 0) {
+        ck(cudaMalloc(&agent_add_, sizeof(double) * m * S), "cudaMalloc");
+        ck(cudaMalloc(&agent_den_, sizeof(double) * m * S), "cudaMalloc");
+    }
     ck(cudaStreamSynchronize(st), "sync");
     agents_ = agents;
     invalidate_graphs();
@@ -653,17 +669,36 @@ void DeviceSession::launch_residual_dirichlet(bool all_entries)
     end_kernel(kDirichlet);
 }
 
+// (Re)computes the per-agent update factors when dt changes. Outside any
+// graph capture: advance() calls it before capturing.
+void DeviceSession::ensure_source_factors(double dt)
+{
+    std::uint64_t bits;
+    std::memcpy(&bits, &dt, sizeof(bits));
+    if (n_agents_ == 0 || (factors_valid_ && bits == factors_dt_bits_)) return;
+    const double inv_voxel_volume = 1.0 / mesh_.voxel_volume(); // agents.cpp:518
+    const long long total = n_agents_ * S_;
+    const int block = 256;
+    begin_kernel(kAux);
+    kernels::sources_factors<<<static_cast<unsigned>((total + block - 1) / block), block, 0,
+                               static_cast<cudaStream_t>(stream_)>>>(S_, n_agents_, agent_volume_, agent_secretion_,
+                                                                      agent_uptake_, agent_saturation_, dt,
+                                                                      inv_voxel_volume, agent_add_, agent_den_);
+    end_kernel(kAux);
+    factors_dt_bits_ = bits;
+    factors_valid_ = true;
+}
+
 void DeviceSession::launch_sources(double dt)
 {
     if (groups_ == 0) return;
-    const double inv_voxel_volume = 1.0 / mesh_.voxel_volume(); // agents.cpp:518
+    ensure_source_factors(dt);
     const long long total = groups_ * S_;
     const int block = 128;
     begin_kernel(kSources);
     kernels::sources_groups<<<static_cast<unsigned>((total + block - 1) / block), block, 0,
-                              static_cast<cudaStream_t>(stream_)>>>(
-        rho_, S_, groups_, group_voxel_, group_offsets_, agent_volume_, agent_secretion_, agent_uptake_,
-        agent_saturation_, dt, inv_voxel_volume);
+                              static_cast<cudaStream_t>(stream_)>>>(rho_, S_, groups_, group_voxel_, group_offsets_,
+                                                                    agent_add_, agent_den_);
     end_kernel(kSources);
 }
 
@@ -715,6 +750,7 @@ void DeviceSession::advance(std::int64_t steps, double dt, bool with_sources)
     if (std::memcmp(&dt, &dt_, sizeof(double)) != 0)
         throw state_error("advance dt does not match the solver workspace dt");
     auto st = static_cast<cudaStream_t>(stream_);
+    if (with_sources) ensure_source_factors(dt); // not inside the graph capture
     if (timing_ || std::getenv("BIODIFF_NO_GRAPH")) {
         for (std::int64_t s = 0; s < steps; ++s) step_body(with_sources, dt);
         return;
@@ -761,13 +797,13 @@ void DeviceSession::cross_check(const double* other, std::int64_t count, double 
     const unsigned long long init[4] = {0ull, 0ull, ~0ull, 0ull};
     ck(cudaMemcpyAsync(scratch, init, sizeof(init), cudaMemcpyHostToDevice, st), "H2D");
     ck(cudaMemcpyAsync(b, other, sizeof(double) * count, cudaMemcpyHostToDevice, st), "H2D");
-    begin_kernel(kDirichlet + 0); // accounted with the auxiliary kernels
+    begin_kernel(kAux);
     kernels::cross_check_max<<<148 * 4, 256, 0, st>>>(rho_, b, count, scratch, scratch + 1, abs_tol, rel_tol,
                                                       reinterpret_cast<int*>(scratch + 3));
-    end_kernel(kDirichlet);
-    begin_kernel(kDirichlet);
+    end_kernel(kAux);
+    begin_kernel(kAux);
     kernels::cross_check_argmax<<<148 * 4, 256, 0, st>>>(rho_, b, count, scratch, scratch + 2);
-    end_kernel(kDirichlet);
+    end_kernel(kAux);
     unsigned long long out[4];
     ck(cudaMemcpyAsync(out, scratch, sizeof(out), cudaMemcpyDeviceToHost, st), "D2H");
     ck(cudaStreamSynchronize(st), "sync");

@@ -12,7 +12,7 @@
 
 namespace biodiff_b200 {
 
-enum KernelClass { kSweepX = 0, kSweepY = 1, kSweepZ = 2, kDirichlet = 3, kSources = 4, kNumKernelClasses = 5 };
+enum KernelClass { kSweepX = 0, kSweepY = 1, kSweepZ = 2, kDirichlet = 3, kSources = 4, kAux = 5, kNumKernelClasses = 6 };
 
 // Device-side copy of one SolverWorkspace (solver.hpp:24-33).
 struct DeviceWorkspace {
@@ -129,6 +129,11 @@ private:
     double* agent_secretion_ = nullptr;
     double* agent_uptake_ = nullptr;
     double* agent_saturation_ = nullptr;
+    double* agent_add_ = nullptr;     // [N*S] (f*sec)*target for factors_dt_
+    double* agent_den_ = nullptr;     // [N*S] 1 + f*(sec+upt)
+    std::uint64_t factors_dt_bits_ = 0;
+    bool factors_valid_ = false;
+    void ensure_source_factors(double dt);
 
     // Launch accounting / timing.
     std::int64_t launches_ = 0;

@@ -796,9 +796,30 @@ __global__ void dirichlet_entries(double* rho, int S, long long count, const int
 // substrate); the group's agents are applied in ascending-id order. The
 // substrates of one agent update independently, so (group, s) threads
 // reproduce the reference's agent-outer / substrate-inner loop bitwise.
+// Per-agent, per-substrate factors of the implicit update for one dt:
+// add = (f*sec)*target and den = 1 + f*(sec+upt), f = (dt*V)*inv_vox
+// (agents.cpp:538-543). They do not depend on the density, so computing them
+// once per dt and reusing them is bit-identical to the reference.
+__global__ void sources_factors(int S, long long agents, const double* volume, const double* secretion,
+                                const double* uptake, const double* saturation, double dt, double inv_voxel_volume,
+                                double* add, double* den)
+{
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= agents * S) return;
+    const long long m = t / S;
+    const double f = __dmul_rn(__dmul_rn(dt, volume[m]), inv_voxel_volume);
+    const double sec = secretion[t];
+    add[t] = __dmul_rn(__dmul_rn(f, sec), saturation[t]);
+    den[t] = __dadd_rn(1.0, __dmul_rn(f, __dadd_rn(sec, uptake[t])));
+}
+
+// One thread per (voxel group, substrate); the group's agents are applied in
+// ascending-id order: x <- (x + add) / den. Agents of distinct voxels commute
+// and substrates are independent, so (group, s) threads reproduce the
+// reference's agent-outer / substrate-inner loop bitwise. Groups are stored
+// longest-first so the dense-core voxels start early.
 __global__ void sources_groups(double* rho, int S, long long groups, const int64_t* group_voxel,
-                               const int64_t* group_offsets, const double* volume, const double* secretion,
-                               const double* uptake, const double* saturation, double dt, double inv_voxel_volume)
+                               const int64_t* group_offsets, const double* add, const double* den)
 {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= groups * S) return;
@@ -806,15 +827,19 @@ __global__ void sources_groups(double* rho, int S, long long groups, const int64
     const int s = static_cast<int>(t % S);
     double* r = rho + group_voxel[g] * S + s;
     double x = *r;
+    long long m = group_offsets[g];
     const long long a1 = group_offsets[g + 1];
-    for (long long m = group_offsets[g]; m < a1; ++m) {
-        const double f = __dmul_rn(__dmul_rn(dt, volume[m]), inv_voxel_volume);
-        const double sec = secretion[m * S + s];
-        const double upt = uptake[m * S + s];
-        const double num = __dadd_rn(x, __dmul_rn(__dmul_rn(f, sec), saturation[m * S + s]));
-        const double den = __dadd_rn(1.0, __dmul_rn(f, __dadd_rn(sec, upt)));
-        x = __ddiv_rn(num, den);
+    for (; m + 4 <= a1; m += 4) {
+        double a[4], d[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            a[u] = add[(m + u) * S + s];
+            d[u] = den[(m + u) * S + s];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x = __ddiv_rn(__dadd_rn(x, a[u]), d[u]);
     }
+    for (; m < a1; ++m) x = __ddiv_rn(__dadd_rn(x, add[m * S + s]), den[m * S + s]);
     *r = x;
 }
 
