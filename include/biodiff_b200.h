@@ -167,6 +167,32 @@ int biodiff_launch_count(biodiff_session* session, int64_t* launches);
 int biodiff_cross_check(biodiff_session* session, const double* other, int64_t count, double abs_tol,
                         double rel_tol, double* max_abs, double* max_rel, int64_t* worst_index, int32_t* pass);
 
+/* ---- z-slab decomposition across GPUs (new — the reference
+ * has no domain decomposition) ------------------------------
+ * A z-slab session owns global planes [z0, z1) of `global_mesh` (its field
+ * holds nx*ny*(z1-z0)*S values). set_substrates / set_dirichlet / set_agents
+ * take the GLOBAL inputs (global voxel indices, all agents) and keep the
+ * slab's share. The z sweep is a partitioned solve: zero-inflow slab solves
+ * plus two nearest-neighbour plane exchanges and an inflow correction (see
+ * paper_2110_13368_b200/csrc/slab.cu). Slabs with two neighbours must be thick
+ * enough that the cross-slab coupling is below 2^-60 (status 1 otherwise). */
+int biodiff_zslab_create(const biodiff_mesh* global_mesh, int32_t substrates, int32_t z0, int32_t z1, int32_t device,
+                         biodiff_session** out);
+int biodiff_zslab_info(biodiff_session* session, int32_t* z0, int32_t* z1, int32_t* nz_global);
+
+/* One slab per process: NCCL communicator over all slabs (rank = slab index,
+ * ordered by z). biodiff_nccl_unique_id fills 128 bytes on rank 0, to be
+ * broadcast by the caller. biodiff_advance then runs the exchanges on the
+ * session stream. */
+int biodiff_nccl_unique_id(uint8_t* out);
+int biodiff_zslab_connect_nccl(biodiff_session* session, const uint8_t* unique_id, int32_t nranks, int32_t rank);
+
+/* Several slabs in one process (one or more GPUs): link them in z order and
+ * advance them together (device/peer copies move the planes). */
+int biodiff_zslab_link_local(biodiff_session** sessions, int32_t count);
+int biodiff_zslab_group_advance(biodiff_session** sessions, int32_t count, int64_t steps, double dt,
+                                int32_t with_sources);
+
 #ifdef __cplusplus
 }
 #endif

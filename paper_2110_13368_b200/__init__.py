@@ -120,6 +120,12 @@ _SIGNATURES = {
     "biodiff_event_elapsed": (ctypes.c_int, [_vp, _i32, _i32, _P(_d)]),
     "biodiff_launch_count": (ctypes.c_int, [_vp, _P(_i64)]),
     "biodiff_cross_check": (ctypes.c_int, [_vp, _P(_d), _i64, _d, _d, _P(_d), _P(_d), _P(_i64), _P(_i32)]),
+    "biodiff_zslab_create": (ctypes.c_int, [_P(Mesh), _i32, _i32, _i32, _i32, _P(_vp)]),
+    "biodiff_zslab_info": (ctypes.c_int, [_vp, _P(_i32), _P(_i32), _P(_i32)]),
+    "biodiff_nccl_unique_id": (ctypes.c_int, [_P(ctypes.c_uint8)]),
+    "biodiff_zslab_connect_nccl": (ctypes.c_int, [_vp, _P(ctypes.c_uint8), _i32, _i32]),
+    "biodiff_zslab_link_local": (ctypes.c_int, [_P(_vp), _i32]),
+    "biodiff_zslab_group_advance": (ctypes.c_int, [_P(_vp), _i32, _i64, _d, _i32]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGNATURES)
@@ -214,12 +220,41 @@ class Session:
     replaces WorkerPool& (backend.hpp:34). Mirrors the reference entry
     points; the field stays on the device until :meth:`download_field`."""
 
-    def __init__(self, mesh: Mesh, substrates: int, device: int = 0):
+    def __init__(self, mesh: Mesh, substrates: int, device: int = 0, zslab=None):
+        """zslab=(z0, z1): a z-slab session owning global planes [z0, z1) of
+        `mesh` (the global mesh); its field holds only those planes."""
         self.mesh = mesh
         self.S = int(substrates)
+        self.zslab = None
         h = _vp()
-        _check(lib().biodiff_session_create(ctypes.byref(mesh), self.S, device, ctypes.byref(h)))
+        if zslab is None:
+            _check(lib().biodiff_session_create(ctypes.byref(mesh), self.S, device, ctypes.byref(h)))
+        else:
+            z0, z1 = (int(z) for z in zslab)
+            _check(lib().biodiff_zslab_create(ctypes.byref(mesh), self.S, z0, z1, device, ctypes.byref(h)))
+            self.zslab = (z0, z1)
         self._h = h
+
+    # -- z-slab transports ---------------------------------------------------
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = (ctypes.c_uint8 * 128)()
+        _check(lib().biodiff_nccl_unique_id(buf))
+        return bytes(buf)
+
+    def connect_nccl(self, unique_id: bytes, nranks: int, rank: int):
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(unique_id)
+        _check(lib().biodiff_zslab_connect_nccl(self._h, buf, nranks, rank))
+
+    @staticmethod
+    def link_local(sessions):
+        arr = (_vp * len(sessions))(*[s._h for s in sessions])
+        _check(lib().biodiff_zslab_link_local(arr, len(sessions)))
+
+    @staticmethod
+    def group_advance(sessions, steps: int, dt: float, with_sources: bool = True):
+        arr = (_vp * len(sessions))(*[s._h for s in sessions])
+        _check(lib().biodiff_zslab_group_advance(arr, len(sessions), int(steps), dt, 1 if with_sources else 0))
 
     # -- lifetime -------------------------------------------------------
     def close(self):
@@ -241,6 +276,8 @@ class Session:
 
     @property
     def value_count(self) -> int:
+        if self.zslab is not None:
+            return int(self.mesh.nx) * int(self.mesh.ny) * (self.zslab[1] - self.zslab[0]) * self.S
         return self.mesh.voxel_count * self.S
 
     # -- set-up ---------------------------------------------------------

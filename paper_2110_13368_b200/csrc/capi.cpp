@@ -9,7 +9,9 @@
 
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstring>
+#include <optional>
 #include <memory>
 #include <new>
 #include <string>
@@ -18,8 +20,10 @@ using namespace biodiff_b200;
 
 struct biodiff_session {
     std::unique_ptr<DeviceSession> dev;
-    CartesianMesh mesh;
+    CartesianMesh mesh; // the GLOBAL mesh (for a z-slab, dev->mesh() is the slab)
     int S = 0;
+    bool slab = false;
+    int z0 = 0, z1 = 0; // slab planes [z0, z1)
 };
 
 namespace {
@@ -102,6 +106,56 @@ Axis to_axis(int32_t a)
 void need(const void* p, const char* what)
 {
     if (!p) throw std::invalid_argument(std::string("null pointer: ") + what);
+}
+
+// Uploads SolverWorkspaces built on the GLOBAL mesh. For a z-slab the z
+// workspace is sliced to the slab's rows (the global factorisation, so the
+// zero-inflow slab solve is the reference recurrence minus the inflow terms)
+// and the slab's unit-inflow responses are computed:
+//   phi_m : forward value at row m for d_in = 1 (zero RHS), Phi = its back substitution
+//   psi_m : back-substituted value at row m for x_in = 1 (zero RHS)
+void upload_workspaces(biodiff_session* s, const SolverWorkspaces& ws)
+{
+    DeviceSession& d = *s->dev;
+    if (!s->slab) {
+        d.set_workspaces(ws);
+        return;
+    }
+    if (!ws.x) throw state_error("solver workspaces not built");
+    const int S = s->S;
+    auto put = [&](const std::optional<SolverWorkspace>& w) {
+        if (w) d.set_workspace(w->axis, w->n, w->dims, w->dt, w->off_diag.data(), w->denom_inv.data(), w->c_back.data());
+    };
+    put(ws.x);
+    put(ws.y);
+    if (!ws.z) return;
+    const SolverWorkspace& z = *ws.z;
+    const int n = s->z1 - s->z0;
+    std::vector<double> dinv(z.denom_inv.begin() + static_cast<std::ptrdiff_t>(s->z0) * S,
+                             z.denom_inv.begin() + static_cast<std::ptrdiff_t>(s->z1) * S);
+    std::vector<double> cb(z.c_back.begin() + static_cast<std::ptrdiff_t>(s->z0) * S,
+                           z.c_back.begin() + static_cast<std::ptrdiff_t>(s->z1) * S);
+    d.set_workspace(Axis::z, n, z.dims, z.dt, z.off_diag.data(), dinv.data(), cb.data());
+    std::vector<double> phi(static_cast<std::size_t>(n) * S), Phi(phi.size()), psi(phi.size()), phi_last(S);
+    for (int sub = 0; sub < S; ++sub) {
+        const double q = z.off_diag[sub];
+        auto at = [&](int m) { return static_cast<std::size_t>(m) * S + sub; };
+        double f = 1.0;
+        for (int m = 0; m < n; ++m) {
+            f = (0.0 + q * f) * dinv[at(m)];
+            phi[at(m)] = f;
+        }
+        Phi[at(n - 1)] = phi[at(n - 1)];
+        for (int m = n - 2; m >= 0; --m) Phi[at(m)] = phi[at(m)] + cb[at(m)] * Phi[at(m + 1)];
+        double g = cb[at(n - 1)] * 1.0; // zero on the last slab (global last row has c_back = 0)
+        psi[at(n - 1)] = g;
+        for (int m = n - 2; m >= 0; --m) {
+            g = cb[at(m)] * g;
+            psi[at(m)] = g;
+        }
+        phi_last[sub] = phi[at(n - 1)];
+    }
+    d.set_slab_spikes(Phi.data(), psi.data(), phi_last.data());
 }
 
 } // namespace
@@ -194,7 +248,7 @@ int biodiff_set_substrates(biodiff_session* session, const double* diffusion, co
             if (decay[s] < 0.0) throw config_error("substrate has negative decay rate");
             params.push_back({"s" + std::to_string(s), diffusion[s], decay[s], 0.0});
         }
-        dev(session).set_workspaces(SolverWorkspaces::build(session->mesh, params, dt));
+        upload_workspaces(session, SolverWorkspaces::build(session->mesh, params, dt));
     });
 }
 
@@ -225,7 +279,17 @@ int biodiff_set_dirichlet(biodiff_session* session, int64_t count, const int64_t
         for (int64_t e = 0; e < count; ++e)
             map.add(voxel[e], std::vector<std::uint8_t>(mask + e * S, mask + (e + 1) * S),
                     std::vector<double>(values + e * S, values + (e + 1) * S), session->mesh.voxel_count(), S);
-        d.set_dirichlet(map);
+        if (!session->slab) {
+            d.set_dirichlet(map);
+        } else { // keep the slab's entries, in local voxel indices
+            const std::int64_t plane = static_cast<std::int64_t>(session->mesh.nx) * session->mesh.ny;
+            const std::int64_t lo = session->z0 * plane, hi = session->z1 * plane;
+            DirichletMap local;
+            for (const auto& e : map.entries())
+                if (e.voxel >= lo && e.voxel < hi)
+                    local.add(e.voxel - lo, e.mask, e.values, hi - lo, S);
+            d.set_dirichlet(local);
+        }
     });
 }
 
@@ -255,7 +319,13 @@ int biodiff_set_agents(biodiff_session* session, int64_t n, const int64_t* ids, 
             c.uptake_rates.assign(uptake + a * S, uptake + (a + 1) * S);
             c.saturation_densities.assign(saturation + a * S, saturation + (a + 1) * S);
         }
-        d.set_agents(AgentPopulation(std::move(agents), session->mesh, S));
+        AgentPopulation pop(std::move(agents), session->mesh, S); // global validation + grouping
+        if (!session->slab) {
+            d.set_agents(pop);
+        } else {
+            const std::int64_t plane = static_cast<std::int64_t>(session->mesh.nx) * session->mesh.ny;
+            d.set_agents_range(pop, session->z0 * plane, session->z1 * plane);
+        }
     });
 }
 
@@ -380,6 +450,83 @@ int biodiff_cross_check(biodiff_session* session, const double* other, int64_t c
         dev(session).cross_check(other, count, abs_tol, rel_tol, max_abs, max_rel, &w, &p);
         *worst_index = w;
         *pass = p ? 1 : 0;
+    });
+}
+
+// ---- z-slab decomposition -------------------------------------------------
+
+int biodiff_zslab_create(const biodiff_mesh* global_mesh, int32_t substrates, int32_t z0, int32_t z1, int32_t device,
+                         biodiff_session** out)
+{
+    return guarded([&] {
+        need(out, "out");
+        *out = nullptr;
+        auto s = std::make_unique<biodiff_session>();
+        s->mesh = to_mesh(global_mesh);
+        if (z0 < 0 || z1 > s->mesh.nz || z0 >= z1) throw config_error("z-slab planes must satisfy 0 <= z0 < z1 <= nz");
+        s->S = substrates;
+        s->slab = true;
+        s->z0 = z0;
+        s->z1 = z1;
+        CartesianMesh local = s->mesh;
+        local.nz = z1 - z0;
+        local.z_min = s->mesh.z_min + z0 * s->mesh.dz;
+        local.z_max = s->mesh.z_min + z1 * s->mesh.dz;
+        s->dev = std::make_unique<DeviceSession>(local, substrates, device);
+        s->dev->configure_slab(s->mesh.nz, z0);
+        *out = s.release();
+    });
+}
+
+int biodiff_zslab_info(biodiff_session* session, int32_t* z0, int32_t* z1, int32_t* nz_global)
+{
+    return guarded([&] {
+        need(z0, "z0");
+        need(z1, "z1");
+        need(nz_global, "nz_global");
+        dev(session);
+        *z0 = session->slab ? session->z0 : 0;
+        *z1 = session->slab ? session->z1 : session->mesh.nz;
+        *nz_global = session->mesh.nz;
+    });
+}
+
+int biodiff_nccl_unique_id(uint8_t* out)
+{
+    return guarded([&] {
+        need(out, "out");
+        nccl_unique_id(out);
+    });
+}
+
+int biodiff_zslab_connect_nccl(biodiff_session* session, const uint8_t* unique_id, int32_t nranks, int32_t rank)
+{
+    return guarded([&] {
+        need(unique_id, "unique_id");
+        if (!session || !session->slab) throw state_error("not a z-slab session");
+        dev(session).connect_nccl(unique_id, nranks, rank);
+    });
+}
+
+int biodiff_zslab_link_local(biodiff_session** sessions, int32_t count)
+{
+    return guarded([&] {
+        need(sessions, "sessions");
+        std::vector<DeviceSession*> v;
+        for (int32_t p = 0; p < count; ++p) v.push_back(&dev(sessions[p]));
+        DeviceSession::link_local(v);
+    });
+}
+
+int biodiff_zslab_group_advance(biodiff_session** sessions, int32_t count, int64_t steps, double dt,
+                                int32_t with_sources)
+{
+    return guarded([&] {
+        need(sessions, "sessions");
+        if (steps < 0) throw std::invalid_argument("step count must be non-negative");
+        std::vector<DeviceSession*> v;
+        for (int32_t p = 0; p < count; ++p) v.push_back(&dev(sessions[p]));
+        DeviceSession::group_advance(v, steps, dt, with_sources != 0);
     });
 }
 

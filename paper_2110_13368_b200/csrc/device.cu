@@ -109,6 +109,7 @@ DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int devi
     if (prop.major != 10)
         throw state_error(std::string("device ") + prop.name + " is not sm_100 (Blackwell B200); this build targets sm_100a only");
     sm_count_ = prop.multiProcessorCount;
+    nzg_ = mesh.nz;
     cudaStream_t st;
     ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
     stream_ = st;
@@ -148,6 +149,7 @@ DeviceSession::~DeviceSession()
     dfree(agent_saturation_);
     dfree(agent_add_);
     dfree(agent_den_);
+    release_slab();
     for (auto& pe : pending_events_) {
         cudaEventDestroy(static_cast<cudaEvent_t>(pe.second.first));
         cudaEventDestroy(static_cast<cudaEvent_t>(pe.second.second));
@@ -305,7 +307,7 @@ void DeviceSession::set_dirichlet(const DirichletMap& map)
         }
     }
     // Shell analysis.
-    const std::int64_t nboundary = mesh_.boundary_voxel_count();
+    const std::int64_t nboundary = boundary_count_local();
     std::uint64_t shell = 0;
     std::vector<double> shell_vals(S, 0.0);
     if (S <= 64 && nboundary > 0) {
@@ -316,7 +318,7 @@ void DeviceSession::set_dirichlet(const DirichletMap& map)
             for (std::int64_t e = 0; e < count && same; ++e) {
                 if (!mask[e * S + s]) continue;
                 const auto ijk = mesh_.voxel_ijk(vox[e]);
-                if (!mesh_.is_boundary_voxel(ijk[0], ijk[1], ijk[2])) continue;
+                if (!is_boundary_local(ijk[0], ijk[1], ijk[2])) continue;
                 const double v = vals[e * S + s];
                 if (first) {
                     v0 = v;
@@ -337,7 +339,7 @@ void DeviceSession::set_dirichlet(const DirichletMap& map)
     std::vector<double> rvals;
     for (std::int64_t e = 0; e < count; ++e) {
         const auto ijk = mesh_.voxel_ijk(vox[e]);
-        const bool boundary = mesh_.is_boundary_voxel(ijk[0], ijk[1], ijk[2]);
+        const bool boundary = is_boundary_local(ijk[0], ijk[1], ijk[2]);
         bool any = false;
         for (int s = 0; s < S; ++s) {
             const bool covered = boundary && ((shell >> s) & 1ull);
@@ -391,7 +393,9 @@ void DeviceSession::set_agents(const AgentPopulation& agents)
     std::stable_sort(gorder.begin(), gorder.end(),
                      [&](std::size_t a, std::size_t b) { return groups[a].second.size() > groups[b].second.size(); });
     for (std::size_t gi : gorder) {
-        const auto& [voxel, idxs] = groups[gi];
+        const auto& [gvoxel, idxs] = groups[gi];
+        if (set_agents_filtered_ && (gvoxel < filter_lo_ || gvoxel >= filter_hi_)) continue;
+        const index_t voxel = set_agents_filtered_ ? gvoxel - filter_lo_ : gvoxel;
         if (voxel < 0 || voxel >= mesh_.voxel_count())
             throw state_error("agent voxel " + std::to_string(voxel) + " outside the mesh; rebuild the voxel grouping");
         gv.push_back(voxel);
@@ -558,7 +562,7 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
     auto st = static_cast<cudaStream_t>(stream_);
     const int S = S_;
     const int rowlen = mesh_.nx * S;
-    kernels::Clamp cl{shell_values_, clamp ? shell_mask_ : 0ull};
+    kernels::Clamp cl{shell_values_, clamp ? shell_mask_ : 0ull, z0_, nzg_};
     const bool do_clamp = clamp && shell_mask_ != 0;
     const kernels::Coef coef{w.q, w.dinv, w.cb, w.dconst, w.cconst, w.settle};
     const SweepPath p = path_[ax];
@@ -637,6 +641,8 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
     y.S = S;
     y.nx = mesh_.nx;
     y.clamp = cl;
+    y.exp_bottom = (slab_ && ax == 2) ? plane_bottom_ : nullptr;
+    y.exp_top = (slab_ && ax == 2) ? plane_top_ : nullptr;
     if (ring) {
         const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(tmap_[ax]);
         auto k = do_clamp ? kernels::sweep_yz_ring<true> : kernels::sweep_yz_ring<false>;
@@ -718,6 +724,12 @@ void DeviceSession::apply_dirichlet()
 // solver.cpp:371-381 with the clamp fused into the last active sweep.
 void DeviceSession::step_body(bool with_sources, double dt)
 {
+    if (slab_ && nccl_comm_) { // one slab per rank: exchanges on this stream (slab.cu)
+        slab_step_nccl(with_sources, dt);
+        return;
+    }
+    if (slab_ && (prev_slab_ || next_slab_))
+        throw state_error("in-process z-slabs advance together: use the group advance");
     const Axis last = ws_[2].active ? Axis::z : ws_[1].active ? Axis::y : Axis::x;
     launch_sweep(Axis::x, last == Axis::x);
     if (ws_[1].active) launch_sweep(Axis::y, last == Axis::y);
@@ -751,7 +763,7 @@ void DeviceSession::advance(std::int64_t steps, double dt, bool with_sources)
         throw state_error("advance dt does not match the solver workspace dt");
     auto st = static_cast<cudaStream_t>(stream_);
     if (with_sources) ensure_source_factors(dt); // not inside the graph capture
-    if (timing_ || std::getenv("BIODIFF_NO_GRAPH")) {
+    if (timing_ || slab_ || std::getenv("BIODIFF_NO_GRAPH")) {
         for (std::int64_t s = 0; s < steps; ++s) step_body(with_sources, dt);
         return;
     }

@@ -42,6 +42,9 @@ enum class SweepPath { smem_ring, smem_bulk, smem_plain, global };
 int settle_row(int n, int S, const double* dinv, const double* cb, std::vector<double>& dconst,
                std::vector<double>& cconst);
 
+// NCCL unique id (NCCL_UNIQUE_ID_BYTES = 128 bytes) for connect_nccl.
+void nccl_unique_id(unsigned char* out);
+
 class DeviceSession {
 public:
     DeviceSession(const CartesianMesh& mesh, int substrates, int device);
@@ -80,7 +83,56 @@ public:
     void cross_check(const double* other, std::int64_t count, double abs_tol, double rel_tol, double* max_abs,
                      double* max_rel, std::int64_t* worst, bool* pass);
 
+    // ---- z-slab decomposition --------------------------
+    // This session holds global planes [z0, z0 + mesh().nz) of a mesh with
+    // nz_global planes. Must be called before any set_* call.
+    void configure_slab(int nz_global, int z0);
+    bool is_slab() const { return slab_; }
+    int slab_z0() const { return z0_; }
+    int slab_nz_global() const { return nzg_; }
+    // Global-mesh boundary test for a local voxel (z faces are global).
+    bool is_boundary_local(int i, int j, int k_local) const;
+    std::int64_t boundary_count_local() const;
+    // Responses to a unit inflow at the slab top (Phi, back-substituted) and
+    // bottom (psi), [n*S], and the forward response at the last row [S].
+    void set_slab_spikes(const double* Phi, const double* psi, const double* phi_last);
+    // Neighbour transports: NCCL (one slab per rank) or in-process.
+    void connect_nccl(const unsigned char* unique_id, int nranks, int rank);
+    static void link_local(const std::vector<DeviceSession*>& slabs);
+    static void group_advance(const std::vector<DeviceSession*>& slabs, std::int64_t steps, double dt,
+                              bool with_sources);
+    void set_agents_range(const AgentPopulation& agents, std::int64_t vox_lo, std::int64_t vox_hi);
+
 private:
+    bool slab_ = false;
+    int nzg_ = 0;
+    int z0_ = 0;
+    double* slab_phi_ = nullptr;       // [n_local*S] Phi (response to D_{p-1})
+    double* slab_psi_ = nullptr;       // [n_local*S] Psi (response to X_{p+1})
+    double* slab_philast_ = nullptr;   // [S] forward response at the last row
+    double* plane_bottom_ = nullptr;   // exported zero-inflow forward value of the last row
+    double* plane_top_ = nullptr;      // exported zero-inflow unclamped x_hat of row 0
+    double* plane_din_ = nullptr;      // D_{p-1} received (0 on slab 0)
+    double* plane_dout_ = nullptr;     // D_p, sent to slab p+1
+    double* plane_xin_ = nullptr;      // X_{p+1} received (0 on the last slab)
+    double* plane_xtop_ = nullptr;     // X_p, sent to slab p-1
+    void* nccl_comm_ = nullptr;
+    int nccl_rank_ = 0, nccl_ranks_ = 1;
+    DeviceSession* prev_slab_ = nullptr; // in-process transport
+    DeviceSession* next_slab_ = nullptr;
+    bool has_prev() const { return nccl_comm_ ? nccl_rank_ > 0 : prev_slab_ != nullptr; }
+    bool has_next() const { return nccl_comm_ ? nccl_rank_ < nccl_ranks_ - 1 : next_slab_ != nullptr; }
+    void slab_phase_sweeps();
+    void slab_phase_fwdfix();
+    void slab_phase_topfix();
+    void slab_phase_finish(bool with_sources, double dt);
+    void slab_step_nccl(bool with_sources, double dt);
+    void nccl_exchange(double* send, int send_peer, double* recv, int recv_peer);
+    std::int64_t plane_count() const { return static_cast<std::int64_t>(mesh_.nx) * mesh_.ny * S_; }
+    bool set_agents_filtered_ = false; // set_agents keeps groups with voxel in [filter_lo_, filter_hi_)
+    std::int64_t filter_lo_ = 0, filter_hi_ = 0;
+    void release_slab();
+
     void check_ready(Axis axis) const;
     void launch_sweep(Axis axis, bool clamp);
     void launch_residual_dirichlet(bool all_entries);

@@ -25,7 +25,16 @@ __host__ __device__ constexpr int bar_bytes(int nch) { return ((nch * 8 + 127) /
 struct Clamp {
     const double* values;    // [S] shell clamp values
     unsigned long long mask; // bit s: substrate s clamped on every boundary voxel
+    int k0;                  // global z index of local plane 0 (z-slab), else 0
+    int nzg;                 // global nz
 };
+
+// Is local plane k on a global z face?
+__device__ __forceinline__ bool kface(int k_local, const Clamp& cl)
+{
+    const int k = k_local + cl.k0;
+    return k == 0 || k == cl.nzg - 1;
+}
 
 // Thomas coefficients of one axis. The precomputed pivots settle to
 // bit-constant values a few dozen rows into the line (SURVEY.md §7 hard part
@@ -65,7 +74,8 @@ struct Chain {
     const double* cb;
     double q, dc, cc;
     int settle, n;
-    bool clamp_s, face;
+    bool clamp_s, face;     // clamped substrate; lane's line lies on a mesh face
+    bool face_lo, face_hi;  // line positions 0 / n-1 lie on a mesh face (false at interior z-slab cuts)
     double clamp_v;
 };
 
@@ -115,14 +125,14 @@ __device__ __forceinline__ double bwd_seg(const Chain& c, double* p, int step, i
         for (int u = 0; u < 8; ++u) {
             next = bwd(v[u], next, b[u]);
             double out = next;
-            if (CLAMP && c.clamp_s && (c.face || (m - u) == 0)) out = c.clamp_v;
+            if (CLAMP && c.clamp_s && (c.face || ((m - u) == 0 && c.face_lo))) out = c.clamp_v;
             q[-u * step] = out;
         }
     }
     for (; m >= m0; --m, q -= step) {
         next = bwd(*q, next, CONSTC ? c.cc : __ldg(c.cb + m * c.S));
         double out = next;
-        if (CLAMP && c.clamp_s && (c.face || m == 0)) out = c.clamp_v;
+        if (CLAMP && c.clamp_s && (c.face || (m == 0 && c.face_lo))) out = c.clamp_v;
         *q = out;
     }
     return next;
@@ -157,8 +167,9 @@ __device__ __forceinline__ void solve_chunked(const Chain& c, bool active, int s
                 prev = fwd_seg<false>(c, p, step, m, m1, prev);
         }
     }
-    double next = prev; // final value of position n-1 (always a face)
-    if (CLAMP && active && c.clamp_s) ptr(nch - 1)[(n - 1 - (nch - 1) * kChunk) * step] = c.clamp_v;
+    double next = prev; // final value of position n-1
+    if (CLAMP && active && c.clamp_s && (c.face || c.face_hi))
+        ptr(nch - 1)[(n - 1 - (nch - 1) * kChunk) * step] = c.clamp_v;
     for (int k = nch - 1; k >= 0; --k) {
         const int m0 = k * kChunk;
         int mtop = min(n, m0 + kChunk) - 1;
@@ -202,6 +213,8 @@ struct StridedSweep {
     long long stride;       // (plain kernel) doubles between positions along the axis
     long long outer_stride; // (plain kernel) doubles between outer indices
     Clamp clamp;
+    double* exp_bottom;     // z-slab plane exports (ring kernel, z axis), or nullptr
+    double* exp_top;
 };
 
 __device__ __forceinline__ Chain make_chain(const Coef& coef, int S, int s, int n, const Clamp& cl, bool face)
@@ -218,11 +231,26 @@ __device__ __forceinline__ Chain make_chain(const Coef& coef, int S, int s, int 
     c.clamp_s = (cl.mask >> s) & 1ull;
     c.clamp_v = c.clamp_s ? cl.values[s] : 0.0;
     c.face = face;
+    c.face_lo = true;
+    c.face_hi = true;
+    return c;
+}
+
+// Chain of a y/z tile lane: column (i, s) at outer index `outer` (k for y,
+// j for z). Along z the line ends are global faces only on the first/last slab.
+__device__ __forceinline__ Chain make_chain_yz(const StridedSweep& a, int s, int i, int outer)
+{
+    const bool outer_face = a.axis == 2 ? (outer == 0 || outer == a.n_outer - 1) : kface(outer, a.clamp);
+    Chain c = make_chain(a.coef, a.S, s, a.n, a.clamp, i == 0 || i == a.nx - 1 || outer_face);
+    if (a.axis == 2) {
+        c.face_lo = a.clamp.k0 == 0;
+        c.face_hi = a.clamp.k0 + a.n == a.clamp.nzg;
+    }
     return c;
 }
 
 template <bool CLAMP>
-__global__ void __launch_bounds__(kLanes) sweep_yz_tma(const __grid_constant__ CUtensorMap tmap, StridedSweep a)
+static __global__ void __launch_bounds__(kLanes) sweep_yz_tma(const __grid_constant__ CUtensorMap tmap, StridedSweep a)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int kSlot = kChunk * kLanes; // doubles per slot
@@ -261,8 +289,7 @@ __global__ void __launch_bounds__(kLanes) sweep_yz_tma(const __grid_constant__ C
         const bool active = lane < width;
         const int e = e0 + (active ? lane : 0);
         const int s = e % a.S, i = e / a.S;
-        const Chain c = make_chain(a.coef, a.S, s, a.n, a.clamp,
-                                   i == 0 || i == a.nx - 1 || outer == 0 || outer == a.n_outer - 1);
+        const Chain c = make_chain_yz(a, s, i, outer);
         solve_chunked<CLAMP>(
             c, active, kLanes, [&](int k) { return slots + slot_of(k) * kSlot + lane; },
             [&](int k) { ptx::mbar_wait(&bars[slot_of(k)], phase); },
@@ -296,7 +323,7 @@ __global__ void __launch_bounds__(kLanes) sweep_yz_tma(const __grid_constant__ C
 // Whole line in shared memory without TMA (rows with an odd number of
 // doubles cannot be described by a tensor map: strides must be 16-byte
 // multiples). One tile per CTA.
-__global__ void __launch_bounds__(kLanes) sweep_yz_plain(StridedSweep a, bool clamp)
+static __global__ void __launch_bounds__(kLanes) sweep_yz_plain(StridedSweep a, bool clamp)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     double* tile = reinterpret_cast<double*>(smem);
@@ -311,8 +338,7 @@ __global__ void __launch_bounds__(kLanes) sweep_yz_plain(StridedSweep a, bool cl
     __syncwarp();
     const int e = e0 + (active ? lane : 0);
     const int s = e % a.S, i = e / a.S;
-    const Chain c = make_chain(a.coef, a.S, s, a.n, a.clamp,
-                               i == 0 || i == a.nx - 1 || outer == 0 || outer == a.n_outer - 1);
+    const Chain c = make_chain_yz(a, s, i, outer);
     auto ptr = [&](int k) { return tile + k * kChunk * kLanes + lane; };
     auto none = [](int) {};
     if (clamp)
@@ -345,7 +371,7 @@ struct XSweep {
 };
 
 template <bool CLAMP>
-__global__ void __launch_bounds__(kLanes) sweep_x_bulk(XSweep a)
+static __global__ void __launch_bounds__(kLanes) sweep_x_bulk(XSweep a)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     const int nch = (a.nx + kChunk - 1) / kChunk;
@@ -393,7 +419,7 @@ __global__ void __launch_bounds__(kLanes) sweep_x_bulk(XSweep a)
         const int s = active ? lane % S : 0;
         const long long line = t * a.L + l;
         const int j = static_cast<int>(line % a.ny), kk = static_cast<int>(line / a.ny);
-        const Chain c = make_chain(a.coef, S, s, a.nx, a.clamp, j == 0 || j == a.ny - 1 || kk == 0 || kk == a.nz - 1);
+        const Chain c = make_chain(a.coef, S, s, a.nx, a.clamp, j == 0 || j == a.ny - 1 || kface(kk, a.clamp));
         solve_chunked<CLAMP>(
             c, active, S, [&](int k) { return slots + slot_of(k) * slot_sz + l * a.cpitch + s; },
             [&](int k) { ptx::mbar_wait(&bars[slot_of(k)], phase); },
@@ -421,7 +447,7 @@ __global__ void __launch_bounds__(kLanes) sweep_x_bulk(XSweep a)
 }
 
 // Whole lines in shared memory without bulk copies (odd nx*S). One tile per CTA.
-__global__ void __launch_bounds__(kLanes) sweep_x_plain(XSweep a, bool clamp)
+static __global__ void __launch_bounds__(kLanes) sweep_x_plain(XSweep a, bool clamp)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     double* tile = reinterpret_cast<double*>(smem);
@@ -438,7 +464,7 @@ __global__ void __launch_bounds__(kLanes) sweep_x_plain(XSweep a, bool clamp)
     const int s = active ? lane % S : 0;
     const long long line = line0 + l;
     const int j = static_cast<int>(line % a.ny), kk = static_cast<int>(line / a.ny);
-    const Chain c = make_chain(a.coef, S, s, a.nx, a.clamp, j == 0 || j == a.ny - 1 || kk == 0 || kk == a.nz - 1);
+    const Chain c = make_chain(a.coef, S, s, a.nx, a.clamp, j == 0 || j == a.ny - 1 || kface(kk, a.clamp));
     auto ptr = [&](int k) { return tile + l * a.pitch + k * kChunk * S + s; };
     auto none = [](int) {};
     if (clamp)
@@ -468,9 +494,19 @@ __global__ void __launch_bounds__(kLanes) sweep_x_plain(XSweep a, bool clamp)
 //             then back-substituted and stored.
 // HBM traffic stays one read + one write per value; L2 serves the reloads.
 // ---------------------------------------------------------------------------
+// Boundary-plane exports of the z-slab decomposition (nullptr members = off):
+// bottom[idx] <- forward value of the last row, top[idx] <- unclamped final
+// value of row 0.
+struct SlabExport {
+    double* bottom;
+    double* top;
+    long long idx;
+};
+
 template <bool CLAMP, class Ptr, class Load, class Store>
 __device__ __forceinline__ void solve_ring(const Chain& c, bool active, int step, int NS, uint64_t* bars, double* ckpt,
-                                           int lane, Ptr ptr, Load load, Store store)
+                                           int lane, Ptr ptr, Load load, Store store,
+                                           const SlabExport* exp = nullptr)
 {
     const int n = c.n;
     const int nch = (n + kChunk - 1) / kChunk;
@@ -514,10 +550,14 @@ __device__ __forceinline__ void solve_ring(const Chain& c, bool active, int step
         }
     }
 
+    // z-slab: the forward value of the last row goes to the next slab.
+    if (exp && active && exp->bottom) exp->bottom[exp->idx] = prev;
+
     // Back substitution, top chunk first.
-    double next = prev; // final value of position n-1 (always a face)
+    double next = prev; // final value of position n-1
     const int first_reloaded = nch - NS - 1; // highest chunk that must be reloaded
-    if (CLAMP && active && c.clamp_s) ptr((nch - 1) % NS)[((n - 1) - (nch - 1) * kChunk) * step] = c.clamp_v;
+    if (CLAMP && active && c.clamp_s && (c.face || c.face_hi))
+        ptr((nch - 1) % NS)[((n - 1) - (nch - 1) * kChunk) * step] = c.clamp_v;
     for (int k = nch - 1; k >= 0; --k) {
         const int s = k % NS;
         const int m0 = k * kChunk;
@@ -564,6 +604,8 @@ __device__ __forceinline__ void solve_ring(const Chain& c, bool active, int step
             }
         }
     }
+    // z-slab: the unclamped back-substituted value of row 0 goes to the previous slab.
+    if (exp && active && exp->top) exp->top[exp->idx] = next;
     if (lane == 0) ptx::bulk_wait_read<0>();
 }
 
@@ -574,7 +616,7 @@ struct Ring {
 };
 
 template <bool CLAMP>
-__global__ void __launch_bounds__(kLanes) sweep_yz_ring(const __grid_constant__ CUtensorMap tmap, StridedSweep a, Ring r)
+static __global__ void __launch_bounds__(kLanes) sweep_yz_ring(const __grid_constant__ CUtensorMap tmap, StridedSweep a, Ring r)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int kSlot = kChunk * kLanes;
@@ -599,9 +641,10 @@ __global__ void __launch_bounds__(kLanes) sweep_yz_ring(const __grid_constant__ 
     const bool active = lane < width;
     const int e = e0 + (active ? lane : 0);
     const int s = e % a.S, i = e / a.S;
-    const Chain c = make_chain(a.coef, a.S, s, a.n, a.clamp,
-                               i == 0 || i == a.nx - 1 || outer == 0 || outer == a.n_outer - 1);
+    const Chain c = make_chain_yz(a, s, i, outer);
     const uint64_t keep_pol = ptx::policy_evict_last(), stream_pol = ptx::policy_evict_first();
+    // Plane index of this column for the z-slab exports (z axis: outer = j).
+    const SlabExport ex{a.exp_bottom, a.exp_top, static_cast<long long>(outer) * a.rowlen + e};
     solve_ring<CLAMP>(
         c, active, kLanes, r.ns, bars, ckpt, lane, [&](int slot) { return slots + slot * kSlot + lane; },
         [&](int k, int slot, bool keep) {
@@ -620,11 +663,12 @@ __global__ void __launch_bounds__(kLanes) sweep_yz_ring(const __grid_constant__ 
                 ptx::tma_store_3d_hint(&tmap, e0, c1, c2, slots + slot * kSlot, stream_pol);
             else
                 ptx::tma_store_3d(&tmap, e0, c1, c2, slots + slot * kSlot);
-        });
+        },
+        &ex);
 }
 
 template <bool CLAMP>
-__global__ void __launch_bounds__(kLanes) sweep_x_ring(XSweep a, Ring r)
+static __global__ void __launch_bounds__(kLanes) sweep_x_ring(XSweep a, Ring r)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     const int S = a.S;
@@ -646,7 +690,7 @@ __global__ void __launch_bounds__(kLanes) sweep_x_ring(XSweep a, Ring r)
     const int sub = active ? lane % S : 0;
     const long long line = t * a.L + l;
     const int j = static_cast<int>(line % a.ny), kk = static_cast<int>(line / a.ny);
-    const Chain c = make_chain(a.coef, S, sub, a.nx, a.clamp, j == 0 || j == a.ny - 1 || kk == 0 || kk == a.nz - 1);
+    const Chain c = make_chain(a.coef, S, sub, a.nx, a.clamp, j == 0 || j == a.ny - 1 || kface(kk, a.clamp));
     const uint64_t keep_pol = ptx::policy_evict_last(), stream_pol = ptx::policy_evict_first();
     auto bytes_of = [&](int k) { return static_cast<uint32_t>(min(kChunk, a.nx - k * kChunk) * S * 8); };
     solve_ring<CLAMP>(
@@ -695,7 +739,7 @@ struct GlobalSweep {
 };
 
 template <bool CLAMP>
-__global__ void __launch_bounds__(128) sweep_global(GlobalSweep a)
+static __global__ void __launch_bounds__(128) sweep_global(GlobalSweep a)
 {
     const long long chain = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (chain >= a.chains) return;
@@ -761,10 +805,10 @@ __global__ void __launch_bounds__(128) sweep_global(GlobalSweep a)
         if (a.axis == 0) ii = mm;
         else if (a.axis == 1) jj = mm;
         else kk = mm;
-        return ii == 0 || ii == a.nx - 1 || jj == 0 || jj == a.ny - 1 || kk == 0 || kk == a.nz - 1;
+        return ii == 0 || ii == a.nx - 1 || jj == 0 || jj == a.ny - 1 || kface(kk, a.clamp);
     };
     double next = prev;
-    if (CLAMP && clamp_s) p[(n - 1) * stride] = clamp_v;
+    if (CLAMP && clamp_s && is_face(n - 1)) p[(n - 1) * stride] = clamp_v;
     m = n - 2;
     for (; m - 7 >= 0; m -= 8) {
         double v[8];
@@ -784,7 +828,7 @@ __global__ void __launch_bounds__(128) sweep_global(GlobalSweep a)
 
 // Masked overwrite of Dirichlet entries (solver.cpp:349-357); one thread per
 // (entry, substrate). Entries are unique voxels, so order is irrelevant.
-__global__ void dirichlet_entries(double* rho, int S, long long count, const int64_t* voxel,
+static __global__ void dirichlet_entries(double* rho, int S, long long count, const int64_t* voxel,
                                   const unsigned char* mask, const double* values)
 {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -800,7 +844,7 @@ __global__ void dirichlet_entries(double* rho, int S, long long count, const int
 // add = (f*sec)*target and den = 1 + f*(sec+upt), f = (dt*V)*inv_vox
 // (agents.cpp:538-543). They do not depend on the density, so computing them
 // once per dt and reusing them is bit-identical to the reference.
-__global__ void sources_factors(int S, long long agents, const double* volume, const double* secretion,
+static __global__ void sources_factors(int S, long long agents, const double* volume, const double* secretion,
                                 const double* uptake, const double* saturation, double dt, double inv_voxel_volume,
                                 double* add, double* den)
 {
@@ -818,7 +862,7 @@ __global__ void sources_factors(int S, long long agents, const double* volume, c
 // and substrates are independent, so (group, s) threads reproduce the
 // reference's agent-outer / substrate-inner loop bitwise. Groups are stored
 // longest-first so the dense-core voxels start early.
-__global__ void sources_groups(double* rho, int S, long long groups, const int64_t* group_voxel,
+static __global__ void sources_groups(double* rho, int S, long long groups, const int64_t* group_voxel,
                                const int64_t* group_offsets, const double* add, const double* den)
 {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -843,9 +887,64 @@ __global__ void sources_groups(double* rho, int S, long long groups, const int64
     *r = x;
 }
 
+// ---------------------------------------------------------------------------
+// z-slab partitioned solve. Slab p solved its z-lines with
+// zero inflow (x_hat). The true solution is
+//   x_m = x_hat_m + d_in * Phi_m + x_in * Psi_m
+// with d_in the forward value of the previous slab's last row, x_in the final
+// (unclamped) value of the next slab's first row, and Phi / Psi the
+// RHS-independent responses of this slab to a unit inflow at its top / bottom
+// (host-computed, per row and substrate). d_in / x_in come from the exact
+// interface recurrences below (no truncation of cross-slab couplings).
+// ---------------------------------------------------------------------------
+
+// Exact interface recurrences (two plane chains across the slabs):
+//   D_p = dhat_p(last row) + phi_p(last row) * D_{p-1}          (forward, p = 0..P-1)
+//   X_p = xhat_p(row 0) + Phi_p(row 0) * D_{p-1} + Psi_p(row 0) * X_{p+1}   (backward)
+// D_{-1} = X_P = 0. D_p is the true forward value of slab p's last row, X_p
+// the true unclamped final value of its first row.
+static __global__ void zslab_fwdfix(double* d_out, const double* dhat_bottom, const double* d_in,
+                                    const double* phi_last, long long plane, int S)
+{
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= plane) return;
+    d_out[t] = __dadd_rn(dhat_bottom[t], __dmul_rn(phi_last[t % S], d_in[t]));
+}
+
+static __global__ void zslab_topfix(double* x_out, const double* xhat_top, const double* d_in, const double* x_in,
+                                    const double* Phi, const double* Psi, long long plane, int S)
+{
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= plane) return;
+    const int s = static_cast<int>(t % S);
+    x_out[t] = __dadd_rn(__dadd_rn(xhat_top[t], __dmul_rn(Phi[s], d_in[t])), __dmul_rn(Psi[s], x_in[t]));
+}
+
+// Applies the inflow corrections to every value of the slab, skipping
+// shell-clamped voxels (their stored value is already the clamp).
+static __global__ void zslab_correct(double* rho, const double* d_in, const double* x_in, const double* phi, const double* psi,
+                              int nx, int ny, int nz_local, int S, Clamp cl)
+{
+    const long long plane = static_cast<long long>(nx) * ny * S;
+    const long long total = plane * nz_local;
+    for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long pi = t % plane;
+        const int k = static_cast<int>(t / plane);
+        const int s = static_cast<int>(pi % S);
+        if ((cl.mask >> s) & 1ull) {
+            const long long vox = pi / S;
+            const int i = static_cast<int>(vox % nx), j = static_cast<int>(vox / nx);
+            if (i == 0 || i == nx - 1 || j == 0 || j == ny - 1 || kface(k, cl)) continue;
+        }
+        const double corr = __dadd_rn(__dmul_rn(d_in[pi], phi[k * S + s]), __dmul_rn(x_in[pi], psi[k * S + s]));
+        rho[t] = __dadd_rn(rho[t], corr);
+    }
+}
+
 // cross_check (validation.cpp:112-137) reductions. Non-negative doubles
 // order like their bit patterns, so atomicMax on the bits is exact.
-__global__ void cross_check_max(const double* a, const double* b, long long n, unsigned long long* max_abs_bits,
+static __global__ void cross_check_max(const double* a, const double* b, long long n, unsigned long long* max_abs_bits,
                                 unsigned long long* max_rel_bits, double abs_tol, double rel_tol, int* fail)
 {
     double my_abs = 0.0, my_rel = 0.0;
@@ -872,7 +971,7 @@ __global__ void cross_check_max(const double* a, const double* b, long long n, u
     }
 }
 
-__global__ void cross_check_argmax(const double* a, const double* b, long long n, const unsigned long long* max_abs_bits,
+static __global__ void cross_check_argmax(const double* a, const double* b, long long n, const unsigned long long* max_abs_bits,
                                    unsigned long long* worst)
 {
     const double target = __longlong_as_double(static_cast<long long>(*max_abs_bits));

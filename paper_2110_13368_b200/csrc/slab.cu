@@ -1,0 +1,344 @@
+// z-slab decomposition of the LOD step across GPUs.
+//
+// Slab p owns global planes [z0, z1). The x and y sweeps are local. The z
+// sweep runs with zero inflow on the slab using the GLOBAL factorisation rows
+// (so it is exactly the reference's recurrence except for the two missing
+// inflow terms), exporting the zero-inflow forward value of its last row
+// (dhat) and the unclamped back-substituted value of its first row (xhat_0).
+// By linearity the true solution is
+//   x_m = xhat_m + D_{p-1} * Phi_m + X_{p+1} * Psi_m
+// where D_{p-1} is the true forward value of the previous slab's last row and
+// X_{p+1} the true final value of the next slab's first row; Phi / Psi are
+// the slab's responses to unit inflows (host-precomputed, RHS-independent).
+// D and X follow exactly from two plane recurrences across the slabs:
+//   forward : D_p = dhat_p + phi_p(last row) * D_{p-1}           p -> p+1
+//   backward: X_p = xhat_0,p + Phi_p(0) * D_{p-1} + Psi_p(0) * X_{p+1}   p -> p-1
+// No coupling is truncated, so there is no minimum slab thickness; the result
+// differs from the single-domain solve only by rounding. Per step each
+// interface moves two nx*ny*S planes (33.6 MB at 1024^2 x 4).
+// Transports: NCCL send/recv on the session stream (one slab per rank, the
+// multi-GPU path) or device/peer copies between sessions of one process.
+#include "device.hpp"
+#include "kernels.cuh"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+
+namespace biodiff_b200 {
+
+namespace {
+
+void ck(cudaError_t e, const char* what)
+{
+    if (e != cudaSuccess) throw state_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+// NCCL is resolved at run time (the process may already hold torch's copy);
+// the library has no link-time NCCL dependency.
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    std::string error;
+};
+
+NcclApi& nccl()
+{
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            a.error = std::string("cannot load libnccl.so.2: ") + dlerror();
+            return a;
+        }
+        auto sym = [&](const char* n) { return dlsym(h, n); };
+        a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
+        a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
+        a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+        a.Send = reinterpret_cast<decltype(a.Send)>(sym("ncclSend"));
+        a.Recv = reinterpret_cast<decltype(a.Recv)>(sym("ncclRecv"));
+        a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
+        a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
+        a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
+        if (!a.GetUniqueId || !a.CommInitRank || !a.Send || !a.Recv || !a.GroupStart || !a.GroupEnd)
+            a.error = "libnccl.so.2 lacks the point-to-point API";
+        return a;
+    }();
+    return api;
+}
+
+void nck(ncclResult_t r, const char* what)
+{
+    if (r != ncclSuccess)
+        throw state_error(std::string("NCCL error in ") + what + ": " +
+                          (nccl().GetErrorString ? nccl().GetErrorString(r) : "?"));
+}
+
+} // namespace
+
+void nccl_unique_id(unsigned char* out)
+{
+    NcclApi& a = nccl();
+    if (!a.error.empty()) throw state_error(a.error);
+    ncclUniqueId id;
+    nck(a.GetUniqueId(&id), "ncclGetUniqueId");
+    static_assert(sizeof(id) == NCCL_UNIQUE_ID_BYTES, "unexpected ncclUniqueId size");
+    std::memcpy(out, &id, sizeof(id));
+}
+
+void DeviceSession::configure_slab(int nz_global, int z0)
+{
+    if (slab_) throw state_error("session is already a z-slab");
+    if (z0 < 0 || z0 + mesh_.nz > nz_global) throw config_error("z-slab outside the global mesh");
+    if (ws_[0].active || ws_[1].active || ws_[2].active)
+        throw state_error("configure the z-slab before setting workspaces");
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    slab_ = true;
+    nzg_ = nz_global;
+    z0_ = z0;
+    const std::size_t bytes = sizeof(double) * plane_count();
+    for (double** p : {&plane_bottom_, &plane_top_, &plane_din_, &plane_dout_, &plane_xin_, &plane_xtop_}) {
+        ck(cudaMalloc(p, bytes), "cudaMalloc plane");
+        ck(cudaMemsetAsync(*p, 0, bytes, static_cast<cudaStream_t>(stream_)), "cudaMemset plane");
+    }
+    choose_paths();
+    if (nz_global > 1 && path_[2] != SweepPath::smem_ring)
+        throw config_error("z-slab needs the TMA ring z-sweep (rows with an even number of doubles)");
+}
+
+bool DeviceSession::is_boundary_local(int i, int j, int k_local) const
+{
+    const int k = k_local + z0_;
+    return i == 0 || i == mesh_.nx - 1 || j == 0 || j == mesh_.ny - 1 || k == 0 || k == nzg_ - 1;
+}
+
+std::int64_t DeviceSession::boundary_count_local() const
+{
+    std::int64_t n = 0;
+    const std::int64_t face = static_cast<std::int64_t>(mesh_.nx) * mesh_.ny;
+    const std::int64_t inner = static_cast<std::int64_t>(std::max(mesh_.nx - 2, 0)) * std::max(mesh_.ny - 2, 0);
+    for (int k = 0; k < mesh_.nz; ++k) {
+        const int kg = k + z0_;
+        n += (kg == 0 || kg == nzg_ - 1) ? face : face - inner;
+    }
+    return n;
+}
+
+void DeviceSession::set_slab_spikes(const double* Phi, const double* psi, const double* phi_last)
+{
+    if (!slab_) throw state_error("not a z-slab session");
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    auto st = static_cast<cudaStream_t>(stream_);
+    const std::size_t n = static_cast<std::size_t>(mesh_.nz) * S_;
+    if (!slab_phi_) ck(cudaMalloc(&slab_phi_, sizeof(double) * n), "cudaMalloc");
+    if (!slab_psi_) ck(cudaMalloc(&slab_psi_, sizeof(double) * n), "cudaMalloc");
+    if (!slab_philast_) ck(cudaMalloc(&slab_philast_, sizeof(double) * S_), "cudaMalloc");
+    ck(cudaMemcpyAsync(slab_phi_, Phi, sizeof(double) * n, cudaMemcpyHostToDevice, st), "H2D");
+    ck(cudaMemcpyAsync(slab_psi_, psi, sizeof(double) * n, cudaMemcpyHostToDevice, st), "H2D");
+    ck(cudaMemcpyAsync(slab_philast_, phi_last, sizeof(double) * S_, cudaMemcpyHostToDevice, st), "H2D");
+    ck(cudaStreamSynchronize(st), "sync");
+}
+
+void DeviceSession::connect_nccl(const unsigned char* unique_id, int nranks, int rank)
+{
+    if (!slab_) throw state_error("not a z-slab session");
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw config_error("bad NCCL rank / size");
+    NcclApi& a = nccl();
+    if (!a.error.empty()) throw state_error(a.error);
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof(id));
+    ncclComm_t comm;
+    nck(a.CommInitRank(&comm, nranks, id, rank), "ncclCommInitRank");
+    nccl_comm_ = comm;
+    nccl_rank_ = rank;
+    nccl_ranks_ = nranks;
+}
+
+void DeviceSession::nccl_exchange(double* send, int send_peer, double* recv, int recv_peer)
+{
+    if (!send && !recv) return;
+    NcclApi& a = nccl();
+    auto comm = static_cast<ncclComm_t>(nccl_comm_);
+    auto st = static_cast<cudaStream_t>(stream_);
+    const size_t count = static_cast<size_t>(plane_count());
+    nck(a.GroupStart(), "ncclGroupStart");
+    if (send) nck(a.Send(send, count, ncclFloat64, send_peer, comm, st), "ncclSend");
+    if (recv) nck(a.Recv(recv, count, ncclFloat64, recv_peer, comm, st), "ncclRecv");
+    nck(a.GroupEnd(), "ncclGroupEnd");
+}
+
+void DeviceSession::link_local(const std::vector<DeviceSession*>& slabs)
+{
+    for (std::size_t p = 0; p < slabs.size(); ++p) {
+        DeviceSession* s = slabs[p];
+        if (!s->slab_) throw state_error("link_local needs z-slab sessions");
+        if (p + 1 < slabs.size() && s->z0_ + s->mesh_.nz != slabs[p + 1]->z0_)
+            throw config_error("z-slabs must be contiguous and in order");
+        s->prev_slab_ = p > 0 ? slabs[p - 1] : nullptr;
+        s->next_slab_ = p + 1 < slabs.size() ? slabs[p + 1] : nullptr;
+    }
+}
+
+void DeviceSession::slab_phase_sweeps()
+{
+    check_ready(Axis::x);
+    launch_sweep(Axis::x, false);
+    if (ws_[1].active) launch_sweep(Axis::y, false);
+    if (ws_[2].active) launch_sweep(Axis::z, true);
+}
+
+// D_p = dhat_p + phi_last * D_{p-1} (needed only when a next slab exists).
+void DeviceSession::slab_phase_fwdfix()
+{
+    if (!has_next()) return;
+    if (!slab_philast_) throw state_error("z-slab spikes not set");
+    const long long plane = plane_count();
+    const int block = 256;
+    begin_kernel(kAux);
+    kernels::zslab_fwdfix<<<static_cast<unsigned>((plane + block - 1) / block), block, 0,
+                            static_cast<cudaStream_t>(stream_)>>>(plane_dout_, plane_bottom_, plane_din_,
+                                                                  slab_philast_, plane, S_);
+    end_kernel(kAux);
+}
+
+// X_p = xhat_top + Phi_0 * D_{p-1} + Psi_0 * X_{p+1} (needed only when a previous slab exists).
+void DeviceSession::slab_phase_topfix()
+{
+    if (!has_prev()) return;
+    if (!slab_phi_) throw state_error("z-slab spikes not set");
+    const long long plane = plane_count();
+    const int block = 256;
+    begin_kernel(kAux);
+    kernels::zslab_topfix<<<static_cast<unsigned>((plane + block - 1) / block), block, 0,
+                            static_cast<cudaStream_t>(stream_)>>>(plane_xtop_, plane_top_, plane_din_, plane_xin_,
+                                                                  slab_phi_, slab_psi_, plane, S_);
+    end_kernel(kAux);
+}
+
+void DeviceSession::slab_phase_finish(bool with_sources, double dt)
+{
+    if (has_prev() || has_next()) {
+        if (!slab_phi_) throw state_error("z-slab spikes not set");
+        kernels::Clamp cl{shell_values_, shell_mask_, z0_, nzg_};
+        begin_kernel(kAux);
+        kernels::zslab_correct<<<sm_count_ * 8, 256, 0, static_cast<cudaStream_t>(stream_)>>>(
+            rho_, plane_din_, plane_xin_, slab_phi_, slab_psi_, mesh_.nx, mesh_.ny, mesh_.nz, S_, cl);
+        end_kernel(kAux);
+    }
+    launch_residual_dirichlet(false);
+    if (with_sources) launch_sources(dt);
+}
+
+// One slab per rank: the two plane chains run on this stream through NCCL.
+void DeviceSession::slab_step_nccl(bool with_sources, double dt)
+{
+    slab_phase_sweeps();
+    nccl_exchange(nullptr, 0, has_prev() ? plane_din_ : nullptr, nccl_rank_ - 1); // D_{p-1}
+    slab_phase_fwdfix();
+    nccl_exchange(has_next() ? plane_dout_ : nullptr, nccl_rank_ + 1, nullptr, 0); // D_p
+    nccl_exchange(nullptr, 0, has_next() ? plane_xin_ : nullptr, nccl_rank_ + 1); // X_{p+1}
+    slab_phase_topfix();
+    nccl_exchange(has_prev() ? plane_xtop_ : nullptr, nccl_rank_ - 1, nullptr, 0); // X_p
+    slab_phase_finish(with_sources, dt);
+}
+
+// In-process slabs (one or several GPUs driven by one host thread): the same
+// phases, with the chains walked slab by slab and the planes moved by device
+// (or peer) copies ordered by events between the slab streams.
+void DeviceSession::group_advance(const std::vector<DeviceSession*>& slabs, std::int64_t steps, double dt,
+                                  bool with_sources)
+{
+    const std::size_t P = slabs.size();
+    if (P == 0) return;
+    for (auto* s : slabs)
+        if (!s->slab_) throw state_error("group advance needs z-slab sessions");
+    std::vector<cudaEvent_t> ev(P);
+    for (std::size_t p = 0; p < P; ++p) {
+        ck(cudaSetDevice(slabs[p]->device_), "cudaSetDevice");
+        ck(cudaEventCreateWithFlags(&ev[p], cudaEventDisableTiming), "cudaEventCreate");
+        if (with_sources) slabs[p]->ensure_source_factors(dt);
+    }
+    auto stream = [&](std::size_t p) { return static_cast<cudaStream_t>(slabs[p]->stream_); };
+    auto bytes = [&](std::size_t p) { return sizeof(double) * slabs[p]->plane_count(); };
+    auto on = [&](std::size_t p) { ck(cudaSetDevice(slabs[p]->device_), "cudaSetDevice"); };
+    auto mark = [&](std::size_t p) { ck(cudaEventRecord(ev[p], stream(p)), "cudaEventRecord"); };
+    auto wait_on = [&](std::size_t p, std::size_t q) { ck(cudaStreamWaitEvent(stream(p), ev[q], 0), "wait"); };
+    for (std::int64_t step = 0; step < steps; ++step) {
+        for (std::size_t p = 0; p < P; ++p) {
+            on(p);
+            slabs[p]->slab_phase_sweeps();
+        }
+        for (std::size_t p = 0; p < P; ++p) { // forward chain D_0 -> D_{P-1}
+            on(p);
+            if (p > 0) {
+                wait_on(p, p - 1);
+                ck(cudaMemcpyPeerAsync(slabs[p]->plane_din_, slabs[p]->device_, slabs[p - 1]->plane_dout_,
+                                       slabs[p - 1]->device_, bytes(p), stream(p)),
+                   "copy D");
+            }
+            slabs[p]->slab_phase_fwdfix();
+            mark(p);
+        }
+        for (std::size_t pp = P; pp-- > 0;) { // backward chain X_{P-1} -> X_0
+            on(pp);
+            if (pp + 1 < P) {
+                wait_on(pp, pp + 1);
+                ck(cudaMemcpyPeerAsync(slabs[pp]->plane_xin_, slabs[pp]->device_, slabs[pp + 1]->plane_xtop_,
+                                       slabs[pp + 1]->device_, bytes(pp), stream(pp)),
+                   "copy X");
+            }
+            slabs[pp]->slab_phase_topfix();
+            mark(pp);
+        }
+        for (std::size_t p = 0; p < P; ++p) {
+            on(p);
+            slabs[p]->slab_phase_finish(with_sources, dt);
+            mark(p);
+        }
+        for (std::size_t p = 0; p < P; ++p) { // next sweeps overwrite planes the neighbours read
+            on(p);
+            for (std::size_t q : {p - 1, p + 1})
+                if (q < P) wait_on(p, q);
+        }
+    }
+    for (std::size_t p = 0; p < P; ++p) {
+        on(p);
+        ck(cudaStreamSynchronize(stream(p)), "sync");
+        cudaEventDestroy(ev[p]);
+    }
+}
+
+void DeviceSession::release_slab()
+{
+    for (double** p : {&plane_bottom_, &plane_top_, &plane_din_, &plane_dout_, &plane_xin_, &plane_xtop_, &slab_phi_,
+                       &slab_psi_, &slab_philast_}) {
+        if (*p) cudaFree(*p);
+        *p = nullptr;
+    }
+    if (nccl_comm_ && nccl().CommDestroy) nccl().CommDestroy(static_cast<ncclComm_t>(nccl_comm_));
+    nccl_comm_ = nullptr;
+}
+
+void DeviceSession::set_agents_range(const AgentPopulation& agents, std::int64_t vox_lo, std::int64_t vox_hi)
+{
+    // Keep the groups whose (global) voxel lies in [vox_lo, vox_hi) and make
+    // their voxel indices local; the (voxel, id) order is preserved.
+    AgentPopulation local = agents;
+    set_agents_filtered_ = true;
+    filter_lo_ = vox_lo;
+    filter_hi_ = vox_hi;
+    set_agents(local);
+    set_agents_filtered_ = false;
+}
+
+} // namespace biodiff_b200
