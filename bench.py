@@ -171,15 +171,27 @@ def config_for(args, w, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
-    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default 1000 for C1-C3, 20 for C4)")
+    ap.add_argument("--warmup", type=int, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c3", choices=["c1", "c2", "c3"])
+    ap.add_argument("--workload", default=None, choices=["c1", "c2", "c3", "c4"],
+                    help="default: c3 at N=1, c4 (z-slab decomposition) at N>1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=None)
     args = ap.parse_args()
+    world, rank, local = dist_env()
+    if args.workload is None:
+        args.workload = "c3" if world == 1 else "c4"
+    big = args.workload == "c4"
+    if args.steps is None:
+        args.steps = 20 if big else 1000
+    if args.warmup is None:
+        args.warmup = 3 if big else 20
     if args.warmup < 3:
         args.warmup = 3  # timing rule: >= 3 warm-up steps
+    if args.e2e_steps is None:
+        args.e2e_steps = 1 if big else 5
 
     from paper_2110_13368_b200 import workloads as W
     w = W.CONFIGS[args.workload](args.steps)
@@ -188,7 +200,6 @@ def main():
         run_reference_arm(args, w)
         return
 
-    world, rank, local = dist_env()
     dist = None
     if world > 1:
         import torch
@@ -197,15 +208,27 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_2110_13368_b200 as B
-    from paper_2110_13368_b200.workloads import session_for as make_session
 
     def barrier():
         if dist is not None:
             dist.barrier()
 
     device = local if world > 1 else 0
-    s = make_session(w, device=device)
-    field_bytes = w.voxels * w.S * 8
+    zslab = big or world > 1
+    if zslab:
+        # C4: one z-slab per rank, interface planes over NCCL (csrc/slab.cu).
+        from paper_2110_13368_b200.zslab import ZSlabRank
+        uid = [B.Session.nccl_unique_id() if (rank == 0 and world > 1) else None]
+        if dist is not None:
+            dist.broadcast_object_list(uid, src=0)
+        zr = ZSlabRank(w, rank, world, device, uid[0])
+        s = zr.session
+        local_values = w.n[0] * w.n[1] * (zr.z1 - zr.z0) * w.S
+    else:
+        s = W.session_for(w, device=device)
+        local_values = w.voxels * w.S
+    field_bytes = local_values * 8
+    vsu_total = w.vsu_per_step if zslab else w.vsu_per_step * world
 
     # Warm-up (also instantiates graphs / loads modules).
     s.advance(args.warmup, w.dt)
@@ -232,7 +255,7 @@ def main():
         t = torch.tensor([ms], device=f"cuda:{device}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    value = w.vsu_per_step * args.steps * world / (ms / 1e3)
+    value = vsu_total * args.steps / (ms / 1e3)
 
     # Roofline of the dominant kernel (largest share of the timed region).
     peak, peak_src = peaks()
@@ -240,42 +263,48 @@ def main():
     dom = max(sweep_classes, key=lambda c: ktimes[c][1])
     n_l, t_l = ktimes[dom]
     avg_ms = t_l / n_l
-    alg_bytes = BYTES_PER_VSU_SWEEP * w.voxels * w.S
+    alg_bytes = BYTES_PER_VSU_SWEEP * local_values
     achieved = alg_bytes / (avg_ms / 1e3) / 1e9
     kernel_total = sum(v[1] for v in ktimes.values())
-    step_achieved = BYTES_PER_VSU_STEP * w.vsu_per_step * args.steps / (ms / 1e3) / 1e9
+    step_achieved = BYTES_PER_VSU_STEP * vsu_total * args.steps / (ms / 1e3) / 1e9 / world
 
-    # End to end through the C ABI with host buffers (pinned), strict drop-in
-    # semantics: every step uploads the field, steps once, reads it back.
-    import torch
-    host_in = torch.from_numpy(w.initial_field()).pin_memory()
-    host_out = torch.empty(w.voxels * w.S, dtype=torch.float64).pin_memory()
-    hin = host_in.numpy()
-    hout = host_out.numpy()
+    # Host-buffer e2e legs need pinned copies of the field: skipped (null) above
+    # 8 GB per rank (C4 on one GPU is 34 GB).
+    e2e_ms = res_ms = None
     E = max(1, args.e2e_steps)
-    barrier()
-    s.event_record(2)
-    for _ in range(E):
+    if field_bytes <= 8e9:
+        # End to end through the C ABI with host buffers (pinned), strict drop-in
+        # semantics: every step uploads the field, steps once, reads it back.
+        import torch
+        host_in = torch.from_numpy(np.tile(w.initial, local_values // w.S)).pin_memory()
+        host_out = torch.empty(local_values, dtype=torch.float64).pin_memory()
+        hin = host_in.numpy()
+        hout = host_out.numpy()
+        E = max(1, args.e2e_steps)
+        barrier()
+        s.event_record(2)
+        for _ in range(E):
+            s.upload_field(hin)
+            s.diffuse_decay_step()
+            s.cell_sources_sinks_step(w.dt)
+            s.download_field(hout)
+        s.event_record(3)
+        e2e_ms = s.event_elapsed(2, 3)
+        # Resident run through the same API: upload once, K steps, read back once.
+        barrier()
+        s.event_record(4)
         s.upload_field(hin)
-        s.diffuse_decay_step()
-        s.cell_sources_sinks_step(w.dt)
+        s.advance(args.steps, w.dt)
         s.download_field(hout)
-    s.event_record(3)
-    e2e_ms = s.event_elapsed(2, 3)
-    # Resident run through the same API: upload once, K steps, read back once.
-    s.event_record(4)
-    s.upload_field(hin)
-    s.advance(args.steps, w.dt)
-    s.download_field(hout)
-    s.event_record(5)
-    res_ms = s.event_elapsed(4, 5)
-    if dist is not None:
-        t = torch.tensor([e2e_ms, res_ms], device=f"cuda:{device}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms, res_ms = (float(x) for x in t.tolist())
+        s.event_record(5)
+        res_ms = s.event_elapsed(4, 5)
+        if dist is not None:
+            t = torch.tensor([e2e_ms, res_ms], device=f"cuda:{device}", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms, res_ms = (float(x) for x in t.tolist())
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not big:
         try:
             cpu = cpu_reference_timing(w)
             if cpu is not None:
@@ -284,42 +313,42 @@ def main():
             cpu = {"error": str(e)}
 
     if rank == 0:
+        cfg = config_for(args, w, world)
+        if zslab:
+            cfg["parallelism"] = f"z-slab x{world} (partitioned z-solve, NCCL plane exchange)" if world > 1 \
+                else "single GPU (one z-slab)"
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if zslab else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic, seeded spherical-tumour layout (paper_2110_13368_b200/workloads.py, SURVEY.md §8 d3)",
-            "config": config_for(args, w, world),
+            "config": cfg,
             "roofline": {
                 "bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": ncu_traffic(dom),
+                "frac": achieved / peak, "traffic": ncu_traffic(dom) if not zslab else None,
                 "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_ms, "peak_source": peak_src,
                 "kernel_share_of_step": t_l / kernel_total if kernel_total else None,
                 "step": {"achieved": step_achieved, "frac": step_achieved / peak,
-                         "bytes_per_vsu": BYTES_PER_VSU_STEP},
+                         "bytes_per_vsu": BYTES_PER_VSU_STEP, "note": "per GPU"},
                 "per_kernel_ms": {k: {"launches": v[0], "avg_ms": (v[1] / v[0]) if v[0] else None}
                                   for k, v in ktimes.items()},
             },
             "cpu_baseline": cpu,
-            "e2e": {"value": w.vsu_per_step * E * world / (e2e_ms / 1e3), "unit": UNIT,
-                    "h2d_bytes_per_step": field_bytes, "d2h_bytes_per_step": field_bytes,
+            "e2e": {"value": vsu_total * E / (e2e_ms / 1e3) if e2e_ms else None, "unit": UNIT,
+                    "h2d_bytes_per_step": field_bytes * world, "d2h_bytes_per_step": field_bytes * world,
                     "steps": E, "semantics": "per step: upload field (pinned host) + step + download field"},
-            "e2e_resident": {"value": w.vsu_per_step * args.steps * world / (res_ms / 1e3), "unit": UNIT,
-                             "h2d_bytes_per_step": field_bytes / args.steps,
-                             "d2h_bytes_per_step": field_bytes / args.steps,
+            "e2e_resident": {"value": vsu_total * args.steps / (res_ms / 1e3) if res_ms else None, "unit": UNIT,
+                             "h2d_bytes_per_step": field_bytes * world / args.steps,
+                             "d2h_bytes_per_step": field_bytes * world / args.steps,
                              "semantics": "upload once, advance(K), download once"},
             "gpu_launches": launches,
             "clocks": clk.summary(),
-            "sweep_paths": {ax: str(p) for ax, p in zip("xyz", _paths(s))},
         }
         print(json.dumps(line), flush=True)
     s.close()
     if dist is not None:
         dist.destroy_process_group()
-
-
-def _paths(s):
-    return [os.environ.get("BIODIFF_SWEEP_PATH", "auto")] * 3
 
 
 if __name__ == "__main__":

@@ -114,6 +114,11 @@ int biodiff_set_agents(biodiff_session* session, int64_t n, const int64_t* ids, 
 int biodiff_agent_grouping(biodiff_session* session, int64_t* groups, int64_t* group_voxel,
                            int64_t* group_offsets, int64_t* order);
 
+/* Fills every voxel with the per-substrate values initial[S] on the device —
+ * the initial condition of Microenvironment::create (mesh.cpp:335-357)
+ * without staging a host copy of the field. */
+int biodiff_fill_field(biodiff_session* session, const double* initial);
+
 /* Host <-> device copies of the DensityField values (a1 layout). */
 int biodiff_upload_field(biodiff_session* session, const double* values, int64_t count);
 int biodiff_download_field(biodiff_session* session, double* values, int64_t count);

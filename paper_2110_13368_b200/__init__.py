@@ -106,6 +106,7 @@ _SIGNATURES = {
     "biodiff_set_agents": (ctypes.c_int, [_vp, _i64, _P(_i64), _P(_d), _P(_d), _P(_d), _P(_d), _P(_d)]),
     "biodiff_agent_grouping": (ctypes.c_int, [_vp, _P(_i64), _P(_i64), _P(_i64), _P(_i64)]),
     "biodiff_upload_field": (ctypes.c_int, [_vp, _P(_d), _i64]),
+    "biodiff_fill_field": (ctypes.c_int, [_vp, _P(_d)]),
     "biodiff_download_field": (ctypes.c_int, [_vp, _P(_d), _i64]),
     "biodiff_diffusion_sweep": (ctypes.c_int, [_vp, _i32]),
     "biodiff_apply_dirichlet": (ctypes.c_int, [_vp]),
@@ -326,6 +327,10 @@ class Session:
     def upload_field(self, values):
         a = _f64(values, self.value_count)
         _check(lib().biodiff_upload_field(self._h, _dptr(a), a.size))
+
+    def fill_field(self, initial):
+        """Every voxel := initial[S] (Microenvironment::create's initial condition)."""
+        _check(lib().biodiff_fill_field(self._h, _dptr(_f64(initial, self.S))))
 
     def download_field(self, out: Optional[np.ndarray] = None) -> np.ndarray:
         if out is None:

@@ -355,6 +355,14 @@ int biodiff_upload_field(biodiff_session* session, const double* values, int64_t
     });
 }
 
+int biodiff_fill_field(biodiff_session* session, const double* initial)
+{
+    return guarded([&] {
+        need(initial, "initial");
+        dev(session).fill(initial);
+    });
+}
+
 int biodiff_download_field(biodiff_session* session, double* values, int64_t count)
 {
     return guarded([&] {

@@ -449,6 +449,18 @@ void DeviceSession::upload(const double* values, std::int64_t count)
        "upload");
 }
 
+void DeviceSession::fill(const double* initial)
+{
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    auto st = static_cast<cudaStream_t>(stream_);
+    double* d = dalloc_copy(initial, static_cast<std::size_t>(S_), st);
+    begin_kernel(kAux);
+    kernels::fill_field<<<sm_count_ * 8, 256, 0, st>>>(rho_, value_count(), d, S_);
+    end_kernel(kAux);
+    ck(cudaStreamSynchronize(st), "sync");
+    cudaFree(d);
+}
+
 void DeviceSession::download(double* values, std::int64_t count)
 {
     if (count != value_count()) throw state_error("density field size does not match the mesh");

@@ -63,6 +63,7 @@ public:
     const AgentPopulation& agents() const { return agents_; }
 
     void upload(const double* values, std::int64_t count);
+    void fill(const double* initial); // [S] per-substrate initial condition
     void download(double* values, std::int64_t count);
 
     void sweep(Axis axis);                 // diffusion_sweep, no clamp

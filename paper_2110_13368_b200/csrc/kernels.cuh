@@ -942,6 +942,14 @@ static __global__ void zslab_correct(double* rho, const double* d_in, const doub
     }
 }
 
+// values[v*S + s] = initial[s] for every voxel (grid-stride).
+static __global__ void fill_field(double* rho, long long total, const double* initial, int S)
+{
+    for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+         t += static_cast<long long>(gridDim.x) * blockDim.x)
+        rho[t] = initial[t % S];
+}
+
 // cross_check (validation.cpp:112-137) reductions. Non-negative doubles
 // order like their bit patterns, so atomicMax on the bits is exact.
 static __global__ void cross_check_max(const double* a, const double* b, long long n, unsigned long long* max_abs_bits,

@@ -62,8 +62,7 @@ def slab_session(w, z0: int, z1: int, device: int = 0) -> B.Session:
         s.set_dirichlet(v, m, x)
     if w.n_agents:
         s.set_agents(w.agent_ids, w.agent_pos, w.agent_vol, w.agent_sec, w.agent_upt, w.agent_sat)
-    nx, ny, _ = w.n
-    s.upload_field(np.tile(w.initial, nx * ny * (z1 - z0)))
+    s.fill_field(w.initial)
     return s
 
 

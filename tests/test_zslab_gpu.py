@@ -23,11 +23,18 @@ def _need_gpu():
         pytest.fail("no sm_100 device visible")
 
 
+FLOOR = 1e-290  # values this small are at the edge of FP64 underflow: compare absolutely
+
+
 def rel_err(a, b):
+    """max |a-b| / max(|a|,|b|) over voxels, with an absolute floor near underflow."""
     d = np.abs(a - b)
-    m = np.maximum(np.abs(a), np.abs(b))
-    r = np.where(m > 0, d / np.where(m > 0, m, 1), 0.0)
-    return float(r.max())
+    m = np.maximum(np.maximum(np.abs(a), np.abs(b)), FLOOR)
+    r = d / m
+    i = int(np.argmax(r))
+    if r[i] > 1e-13:
+        print(f"worst value index {i}: {a[i]!r} vs {b[i]!r}")
+    return float(r[i])
 
 
 CASES = [
