@@ -172,6 +172,20 @@ int biodiff_launch_count(biodiff_session* session, int64_t* launches);
 int biodiff_cross_check(biodiff_session* session, const double* other, int64_t count, double abs_tol,
                         double rel_tol, double* max_abs, double* max_rel, int64_t* worst_index, int32_t* pass);
 
+/* ---- ensembles (C5: independent replicas; new) -------------
+ * `replicas` independent microenvironments on the same mesh in one session,
+ * stacked replica-major: values[(r*voxels + v)*S + s]. Each replica has its
+ * own diffusion/decay (D[r*S + s], lambda[r*S + s]) and agents; Dirichlet
+ * entries use stacked voxel indices r*voxels + v. One kernel launch per sweep
+ * covers every replica. upload/download/fill act on the whole stack. */
+int biodiff_ensemble_create(const biodiff_mesh* mesh, int32_t substrates, int32_t replicas, int32_t device,
+                            biodiff_session** out);
+int biodiff_ensemble_set_substrates(biodiff_session* session, const double* diffusion, const double* decay,
+                                    double dt);
+int biodiff_ensemble_set_agents(biodiff_session* session, int64_t n, const int32_t* replica, const int64_t* ids,
+                                const double* positions, const double* volume, const double* secretion,
+                                const double* uptake, const double* saturation);
+
 /* ---- z-slab decomposition across GPUs (new — the reference
  * has no domain decomposition) ------------------------------
  * A z-slab session owns global planes [z0, z1) of `global_mesh` (its field

@@ -121,6 +121,10 @@ _SIGNATURES = {
     "biodiff_event_elapsed": (ctypes.c_int, [_vp, _i32, _i32, _P(_d)]),
     "biodiff_launch_count": (ctypes.c_int, [_vp, _P(_i64)]),
     "biodiff_cross_check": (ctypes.c_int, [_vp, _P(_d), _i64, _d, _d, _P(_d), _P(_d), _P(_i64), _P(_i32)]),
+    "biodiff_ensemble_create": (ctypes.c_int, [_P(Mesh), _i32, _i32, _i32, _P(_vp)]),
+    "biodiff_ensemble_set_substrates": (ctypes.c_int, [_vp, _P(_d), _P(_d), _d]),
+    "biodiff_ensemble_set_agents": (ctypes.c_int, [_vp, _i64, _P(_i32), _P(_i64), _P(_d), _P(_d), _P(_d), _P(_d),
+                                                   _P(_d)]),
     "biodiff_zslab_create": (ctypes.c_int, [_P(Mesh), _i32, _i32, _i32, _i32, _P(_vp)]),
     "biodiff_zslab_info": (ctypes.c_int, [_vp, _P(_i32), _P(_i32), _P(_i32)]),
     "biodiff_nccl_unique_id": (ctypes.c_int, [_P(ctypes.c_uint8)]),
@@ -221,14 +225,19 @@ class Session:
     replaces WorkerPool& (backend.hpp:34). Mirrors the reference entry
     points; the field stays on the device until :meth:`download_field`."""
 
-    def __init__(self, mesh: Mesh, substrates: int, device: int = 0, zslab=None):
+    def __init__(self, mesh: Mesh, substrates: int, device: int = 0, zslab=None, replicas: int = 1):
         """zslab=(z0, z1): a z-slab session owning global planes [z0, z1) of
-        `mesh` (the global mesh); its field holds only those planes."""
+        `mesh` (the global mesh); its field holds only those planes.
+        replicas > 1: an ensemble of independent microenvironments stacked
+        replica-major (values[(r*voxels + v)*S + s])."""
         self.mesh = mesh
         self.S = int(substrates)
         self.zslab = None
+        self.replicas = int(replicas)
         h = _vp()
-        if zslab is None:
+        if self.replicas > 1:
+            _check(lib().biodiff_ensemble_create(ctypes.byref(mesh), self.S, self.replicas, device, ctypes.byref(h)))
+        elif zslab is None:
             _check(lib().biodiff_session_create(ctypes.byref(mesh), self.S, device, ctypes.byref(h)))
         else:
             z0, z1 = (int(z) for z in zslab)
@@ -279,7 +288,22 @@ class Session:
     def value_count(self) -> int:
         if self.zslab is not None:
             return int(self.mesh.nx) * int(self.mesh.ny) * (self.zslab[1] - self.zslab[0]) * self.S
-        return self.mesh.voxel_count * self.S
+        return self.mesh.voxel_count * self.S * self.replicas
+
+    # -- ensembles ---------------------------------------------------------
+    def ensemble_set_substrates(self, diffusion, decay, dt: float):
+        """Per-replica SolverWorkspaces::build: diffusion/decay shaped [replicas, S]."""
+        n = self.replicas * self.S
+        _check(lib().biodiff_ensemble_set_substrates(self._h, _dptr(_f64(diffusion, n)), _dptr(_f64(decay, n)), dt))
+
+    def ensemble_set_agents(self, replica, ids, positions, volume, secretion, uptake, saturation):
+        rep = np.ascontiguousarray(np.asarray(replica, dtype=np.int32).ravel())
+        ids = np.ascontiguousarray(np.asarray(ids, dtype=np.int64).ravel())
+        n = ids.size
+        _check(lib().biodiff_ensemble_set_agents(
+            self._h, n, rep.ctypes.data_as(_P(_i32)), ids.ctypes.data_as(_P(_i64)), _dptr(_f64(positions, 3 * n)),
+            _dptr(_f64(volume, n)), _dptr(_f64(secretion, n * self.S)), _dptr(_f64(uptake, n * self.S)),
+            _dptr(_f64(saturation, n * self.S))))
 
     # -- set-up ---------------------------------------------------------
     def set_substrates(self, diffusion, decay, dt: float):

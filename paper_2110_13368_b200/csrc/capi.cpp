@@ -24,6 +24,7 @@ struct biodiff_session {
     int S = 0;
     bool slab = false;
     int z0 = 0, z1 = 0; // slab planes [z0, z1)
+    int replicas = 1;   // ensemble size (stacked replica-major)
 };
 
 namespace {
@@ -278,7 +279,8 @@ int biodiff_set_dirichlet(biodiff_session* session, int64_t count, const int64_t
         DirichletMap map;
         for (int64_t e = 0; e < count; ++e)
             map.add(voxel[e], std::vector<std::uint8_t>(mask + e * S, mask + (e + 1) * S),
-                    std::vector<double>(values + e * S, values + (e + 1) * S), session->mesh.voxel_count(), S);
+                    std::vector<double>(values + e * S, values + (e + 1) * S),
+                    session->mesh.voxel_count() * session->replicas, S);
         if (!session->slab) {
             d.set_dirichlet(map);
         } else { // keep the slab's entries, in local voxel indices
@@ -458,6 +460,102 @@ int biodiff_cross_check(biodiff_session* session, const double* other, int64_t c
         dev(session).cross_check(other, count, abs_tol, rel_tol, max_abs, max_rel, &w, &p);
         *worst_index = w;
         *pass = p ? 1 : 0;
+    });
+}
+
+// ---- ensembles ---------------------------------------------------------------
+
+int biodiff_ensemble_create(const biodiff_mesh* mesh, int32_t substrates, int32_t replicas, int32_t device,
+                            biodiff_session** out)
+{
+    return guarded([&] {
+        need(out, "out");
+        *out = nullptr;
+        auto s = std::make_unique<biodiff_session>();
+        s->mesh = to_mesh(mesh);
+        s->S = substrates;
+        s->replicas = replicas;
+        s->dev = std::make_unique<DeviceSession>(s->mesh, substrates, device, replicas);
+        *out = s.release();
+    });
+}
+
+// Per-replica SolverWorkspaces::build (solver.cpp:359-369), uploaded as
+// replicas consecutive coefficient sets per axis.
+int biodiff_ensemble_set_substrates(biodiff_session* session, const double* diffusion, const double* decay, double dt)
+{
+    return guarded([&] {
+        need(diffusion, "diffusion");
+        need(decay, "decay");
+        DeviceSession& d = dev(session);
+        const int S = d.substrates(), R = d.replicas();
+        std::vector<SolverWorkspaces> all;
+        for (int r = 0; r < R; ++r) {
+            std::vector<SubstrateParams> params;
+            for (int s = 0; s < S; ++s) {
+                const double D = diffusion[r * S + s], L = decay[r * S + s];
+                if (D < 0.0) throw config_error("substrate has negative diffusion coefficient");
+                if (L < 0.0) throw config_error("substrate has negative decay rate");
+                params.push_back({"s" + std::to_string(s), D, L, 0.0});
+            }
+            all.push_back(SolverWorkspaces::build(session->mesh, params, dt));
+        }
+        auto upload = [&](auto member) {
+            if (!(all[0].*member)) return;
+            const SolverWorkspace& w0 = *(all[0].*member);
+            std::vector<double> q, dinv, cb;
+            for (const auto& ws : all) {
+                const SolverWorkspace& w = *(ws.*member);
+                q.insert(q.end(), w.off_diag.begin(), w.off_diag.end());
+                dinv.insert(dinv.end(), w.denom_inv.begin(), w.denom_inv.end());
+                cb.insert(cb.end(), w.c_back.begin(), w.c_back.end());
+            }
+            d.set_workspace(w0.axis, w0.n, w0.dims, w0.dt, q.data(), dinv.data(), cb.data());
+        };
+        upload(&SolverWorkspaces::x);
+        upload(&SolverWorkspaces::y);
+        upload(&SolverWorkspaces::z);
+    });
+}
+
+// Agents of all replicas: replica[n] in [0, replicas); ids must be unique
+// within a replica. Each replica's population is validated and grouped as
+// AgentPopulation does (agents.cpp:448-509).
+int biodiff_ensemble_set_agents(biodiff_session* session, int64_t n, const int32_t* replica, const int64_t* ids,
+                                const double* positions, const double* volume, const double* secretion,
+                                const double* uptake, const double* saturation)
+{
+    return guarded([&] {
+        DeviceSession& d = dev(session);
+        const int S = d.substrates(), R = d.replicas();
+        if (n < 0) throw std::invalid_argument("negative agent count");
+        if (n > 0) {
+            need(replica, "replica");
+            need(ids, "ids");
+            need(positions, "positions");
+            need(volume, "volume");
+            need(secretion, "secretion");
+            need(uptake, "uptake");
+            need(saturation, "saturation");
+        }
+        std::vector<std::vector<CellAgent>> per(R);
+        for (int64_t a = 0; a < n; ++a) {
+            if (replica[a] < 0 || replica[a] >= R) throw std::invalid_argument("agent replica out of range");
+            CellAgent c;
+            c.id = ids[a];
+            c.position = {positions[3 * a], positions[3 * a + 1], positions[3 * a + 2]};
+            c.volume = volume[a];
+            c.secretion_rates.assign(secretion + a * S, secretion + (a + 1) * S);
+            c.uptake_rates.assign(uptake + a * S, uptake + (a + 1) * S);
+            c.saturation_densities.assign(saturation + a * S, saturation + (a + 1) * S);
+            per[replica[a]].push_back(std::move(c));
+        }
+        std::vector<AgentPopulation> pops;
+        pops.reserve(R);
+        for (int r = 0; r < R; ++r) pops.emplace_back(std::move(per[r]), session->mesh, S);
+        std::vector<const AgentPopulation*> ptrs;
+        for (const auto& p : pops) ptrs.push_back(&p);
+        d.set_agents_multi(ptrs);
     });
 }
 

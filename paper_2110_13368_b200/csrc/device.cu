@@ -78,26 +78,28 @@ void DeviceSession::build_tensor_maps()
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
     auto encode = reinterpret_cast<Encode>(fn);
-    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(rowlen), static_cast<cuuint64_t>(mesh_.ny),
-                                static_cast<cuuint64_t>(mesh_.nz)};
-    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(rowlen) * 8,
-                                   static_cast<cuuint64_t>(rowlen) * mesh_.ny * 8};
-    const cuuint32_t estr[3] = {1, 1, 1};
+    // 4-D view (row element, j, k, replica); replicas = 1 outside ensembles.
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(rowlen), static_cast<cuuint64_t>(mesh_.ny),
+                                static_cast<cuuint64_t>(mesh_.nz), static_cast<cuuint64_t>(replicas_)};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(rowlen) * 8, static_cast<cuuint64_t>(rowlen) * mesh_.ny * 8,
+                                   static_cast<cuuint64_t>(rowlen) * mesh_.ny * mesh_.nz * 8};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
     for (int ax = 1; ax <= 2; ++ax) {
-        const cuuint32_t box[3] = {static_cast<cuuint32_t>(kernels::kLanes),
+        const cuuint32_t box[4] = {static_cast<cuuint32_t>(kernels::kLanes),
                                    static_cast<cuuint32_t>(ax == 1 ? kernels::kChunk : 1),
-                                   static_cast<cuuint32_t>(ax == 2 ? kernels::kChunk : 1)};
-        CUresult r = encode(reinterpret_cast<CUtensorMap*>(tmap_[ax]), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, rho_,
+                                   static_cast<cuuint32_t>(ax == 2 ? kernels::kChunk : 1), 1};
+        CUresult r = encode(reinterpret_cast<CUtensorMap*>(tmap_[ax]), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, rho_,
                             dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         tmap_ok_[ax] = (r == CUDA_SUCCESS);
     }
 }
 
-DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int device)
-    : mesh_(mesh), S_(substrates), device_(device)
+DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int device, int replicas)
+    : mesh_(mesh), S_(substrates), device_(device), replicas_(replicas)
 {
     if (substrates < 1) throw config_error("a session needs at least one substrate");
+    if (replicas < 1) throw config_error("an ensemble needs at least one replica");
     if (mesh.nx < 1 || mesh.ny < 1 || mesh.nz < 1) throw config_error("mesh has an empty axis");
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
@@ -183,6 +185,10 @@ void DeviceSession::choose_paths()
         else if (fits_lanes && plain_bytes <= kMaxSmem && force != "global")
             p = SweepPath::smem_plain;
         path_[ax] = p;
+        const int n = ax == 0 ? mesh_.nx : ax == 1 ? mesh_.ny : mesh_.nz;
+        if (replicas_ > 1 && n > 1 && p != SweepPath::smem_ring)
+            throw config_error("ensembles need the ring sweep kernels (rows with an even number of doubles, lines "
+                               "that fit a shared-memory ring)");
     }
 }
 
@@ -250,11 +256,20 @@ void DeviceSession::set_workspace(Axis axis, int n, int dims, double dt, const d
     dfree(w.cb);
     dfree(w.dconst);
     dfree(w.cconst);
-    w.q = dalloc_copy(q, S_, st);
-    w.dinv = dalloc_copy(dinv, static_cast<std::size_t>(n) * S_, st);
-    w.cb = dalloc_copy(cb, static_cast<std::size_t>(n) * S_, st);
+    // Ensembles: replicas_ consecutive coefficient sets (q[R*S], dinv/cb[R*n*S]);
+    // the settle row is the max over replicas (warp-uniform in the kernels).
+    const std::size_t set = static_cast<std::size_t>(n) * S_;
+    w.q = dalloc_copy(q, static_cast<std::size_t>(S_) * replicas_, st);
+    w.dinv = dalloc_copy(dinv, set * replicas_, st);
+    w.cb = dalloc_copy(cb, set * replicas_, st);
     std::vector<double> dc, cc;
-    w.settle = settle_row(n, S_, dinv, cb, dc, cc);
+    w.settle = 0;
+    for (int r = 0; r < replicas_; ++r) {
+        std::vector<double> dcr, ccr;
+        w.settle = std::max(w.settle, settle_row(n, S_, dinv + r * set, cb + r * set, dcr, ccr));
+        dc.insert(dc.end(), dcr.begin(), dcr.end());
+        cc.insert(cc.end(), ccr.begin(), ccr.end());
+    }
     if (std::getenv("BIODIFF_NO_SETTLE")) w.settle = n;
     w.dconst = dalloc_copy(dc.data(), dc.size(), st);
     w.cconst = dalloc_copy(cc.data(), cc.size(), st);
@@ -299,7 +314,8 @@ void DeviceSession::set_dirichlet(const DirichletMap& map)
     std::vector<double> vals(count * S);
     for (std::int64_t e = 0; e < count; ++e) {
         const auto& d = entries[e];
-        if (d.voxel < 0 || d.voxel >= mesh_.voxel_count()) throw std::out_of_range("Dirichlet voxel outside mesh");
+        if (d.voxel < 0 || d.voxel >= mesh_.voxel_count() * replicas_)
+            throw std::out_of_range("Dirichlet voxel outside mesh");
         vox[e] = d.voxel;
         for (int s = 0; s < S; ++s) {
             mask[e * S + s] = d.mask[s] ? 1 : 0;
@@ -307,7 +323,7 @@ void DeviceSession::set_dirichlet(const DirichletMap& map)
         }
     }
     // Shell analysis.
-    const std::int64_t nboundary = boundary_count_local();
+    const std::int64_t nboundary = boundary_count_local() * replicas_;
     std::uint64_t shell = 0;
     std::vector<double> shell_vals(S, 0.0);
     if (S <= 64 && nboundary > 0) {
@@ -317,7 +333,7 @@ void DeviceSession::set_dirichlet(const DirichletMap& map)
             double v0 = 0.0;
             for (std::int64_t e = 0; e < count && same; ++e) {
                 if (!mask[e * S + s]) continue;
-                const auto ijk = mesh_.voxel_ijk(vox[e]);
+                const auto ijk = mesh_.voxel_ijk(vox[e] % mesh_.voxel_count());
                 if (!is_boundary_local(ijk[0], ijk[1], ijk[2])) continue;
                 const double v = vals[e * S + s];
                 if (first) {
@@ -338,7 +354,7 @@ void DeviceSession::set_dirichlet(const DirichletMap& map)
     std::vector<std::uint8_t> rmask;
     std::vector<double> rvals;
     for (std::int64_t e = 0; e < count; ++e) {
-        const auto ijk = mesh_.voxel_ijk(vox[e]);
+        const auto ijk = mesh_.voxel_ijk(vox[e] % mesh_.voxel_count());
         const bool boundary = is_boundary_local(ijk[0], ijk[1], ijk[2]);
         bool any = false;
         for (int s = 0; s < S; ++s) {
@@ -375,28 +391,45 @@ void DeviceSession::set_dirichlet(const DirichletMap& map)
 
 void DeviceSession::set_agents(const AgentPopulation& agents)
 {
+    set_agents_multi({&agents});
+    agents_ = agents;
+}
+
+// Ensembles: population r lives in replica r (voxel offset r * voxel_count).
+void DeviceSession::set_agents_multi(const std::vector<const AgentPopulation*>& pops)
+{
     ck(cudaSetDevice(device_), "cudaSetDevice");
     auto st = static_cast<cudaStream_t>(stream_);
     ck(cudaStreamSynchronize(st), "sync");
+    if (static_cast<int>(pops.size()) > replicas_) throw state_error("more agent populations than replicas");
     const int S = S_;
-    const auto& groups = agents.grouping();
-    const auto& all = agents.agents();
     std::vector<std::int64_t> gv, go;
     std::vector<double> vol, sec, upt, sat;
-    gv.reserve(groups.size());
-    go.reserve(groups.size() + 1);
     std::int64_t m = 0;
     // Longest groups first (dense tumour cores): distinct voxels commute, so
     // the group order is free; it only shortens the kernel's tail.
-    std::vector<std::size_t> gorder(groups.size());
-    for (std::size_t g = 0; g < gorder.size(); ++g) gorder[g] = g;
-    std::stable_sort(gorder.begin(), gorder.end(),
-                     [&](std::size_t a, std::size_t b) { return groups[a].second.size() > groups[b].second.size(); });
-    for (std::size_t gi : gorder) {
-        const auto& [gvoxel, idxs] = groups[gi];
+    struct G {
+        const AgentPopulation* pop;
+        std::size_t g;
+        std::int64_t offset;
+    };
+    std::vector<G> gorder;
+    for (std::size_t r = 0; r < pops.size(); ++r)
+        for (std::size_t g = 0; g < pops[r]->grouping().size(); ++g)
+            gorder.push_back({pops[r], g, static_cast<std::int64_t>(r) * mesh_.voxel_count()});
+    std::stable_sort(gorder.begin(), gorder.end(), [](const G& a, const G& b) {
+        return a.pop->grouping()[a.g].second.size() > b.pop->grouping()[b.g].second.size();
+    });
+    gv.reserve(gorder.size());
+    go.reserve(gorder.size() + 1);
+    for (const G& gr : gorder) {
+        const auto& all = gr.pop->agents();
+        const auto& [gvoxel, idxs] = gr.pop->grouping()[gr.g];
         if (set_agents_filtered_ && (gvoxel < filter_lo_ || gvoxel >= filter_hi_)) continue;
-        const index_t voxel = set_agents_filtered_ ? gvoxel - filter_lo_ : gvoxel;
-        if (voxel < 0 || voxel >= mesh_.voxel_count())
+        if (gvoxel < 0 || (!set_agents_filtered_ && gvoxel >= mesh_.voxel_count()))
+            throw state_error("agent voxel " + std::to_string(gvoxel) + " outside the mesh; rebuild the voxel grouping");
+        const index_t voxel = (set_agents_filtered_ ? gvoxel - filter_lo_ : gvoxel) + gr.offset;
+        if (voxel < 0 || voxel >= mesh_.voxel_count() * replicas_)
             throw state_error("agent voxel " + std::to_string(voxel) + " outside the mesh; rebuild the voxel grouping");
         gv.push_back(voxel);
         go.push_back(m);
@@ -436,7 +469,6 @@ void DeviceSession::set_agents(const AgentPopulation& agents)
         ck(cudaMalloc(&agent_den_, sizeof(double) * m * S), "cudaMalloc");
     }
     ck(cudaStreamSynchronize(st), "sync");
-    agents_ = agents;
     invalidate_graphs();
 }
 
@@ -576,7 +608,7 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
     const int rowlen = mesh_.nx * S;
     kernels::Clamp cl{shell_values_, clamp ? shell_mask_ : 0ull, z0_, nzg_};
     const bool do_clamp = clamp && shell_mask_ != 0;
-    const kernels::Coef coef{w.q, w.dinv, w.cb, w.dconst, w.cconst, w.settle};
+    const kernels::Coef coef{w.q, w.dinv, w.cb, w.dconst, w.cconst, w.settle, static_cast<long long>(w.n) * S};
     const SweepPath p = path_[ax];
     const bool bulk = p == SweepPath::smem_bulk;
     begin_kernel(ax);
@@ -609,7 +641,8 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
         kernels::XSweep x{};
         x.rho = rho_;
         x.coef = coef;
-        x.lines = static_cast<long long>(mesh_.ny) * mesh_.nz;
+        x.lines_per_rep = static_cast<long long>(mesh_.ny) * mesh_.nz;
+        x.lines = x.lines_per_rep * replicas_;
         x.nx = mesh_.nx;
         x.ny = mesh_.ny;
         x.nz = mesh_.nz;
@@ -649,7 +682,8 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
     y.n = w.n;
     y.rowlen = rowlen;
     y.tiles_per_row = (rowlen + kernels::kLanes - 1) / kernels::kLanes;
-    y.tiles = y.tiles_per_row * y.n_outer;
+    y.reps = replicas_;
+    y.tiles = y.tiles_per_row * y.n_outer * replicas_;
     y.S = S;
     y.nx = mesh_.nx;
     y.clamp = cl;

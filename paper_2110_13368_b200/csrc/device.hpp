@@ -47,14 +47,19 @@ void nccl_unique_id(unsigned char* out);
 
 class DeviceSession {
 public:
-    DeviceSession(const CartesianMesh& mesh, int substrates, int device);
+    // `replicas` > 1: an ensemble of independent microenvironments on the same
+    // mesh, stacked replica-major in one field (values[(r*nvox + v)*S + s]),
+    // each with its own coefficient set (C5).
+    DeviceSession(const CartesianMesh& mesh, int substrates, int device, int replicas = 1);
     ~DeviceSession();
     DeviceSession(const DeviceSession&) = delete;
     DeviceSession& operator=(const DeviceSession&) = delete;
 
     const CartesianMesh& mesh() const { return mesh_; }
     int substrates() const { return S_; }
-    std::int64_t value_count() const { return mesh_.voxel_count() * S_; }
+    int replicas() const { return replicas_; }
+    std::int64_t value_count() const { return mesh_.voxel_count() * S_ * replicas_; }
+    void set_agents_multi(const std::vector<const AgentPopulation*>& pops);
 
     void set_workspace(Axis axis, int n, int dims, double dt, const double* q, const double* dinv, const double* cb);
     void set_workspaces(const SolverWorkspaces& ws);
@@ -147,6 +152,7 @@ private:
     CartesianMesh mesh_;
     int S_ = 0;
     int device_ = 0;
+    int replicas_ = 1;
     void* stream_ = nullptr; // cudaStream_t
     double* rho_ = nullptr;
     DeviceWorkspace ws_[3];

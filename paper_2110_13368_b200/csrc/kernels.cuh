@@ -48,6 +48,7 @@ struct Coef {
     const double* dconst; // [S]
     const double* cconst; // [S]
     int settle;
+    long long rstride;    // ensembles: doubles between replicas' dinv/cb sets (n*S); q/dconst/cconst step S
 };
 
 __device__ __forceinline__ double fwd_first(double v, double d) { return __dmul_rn(v, d); }
@@ -207,7 +208,8 @@ struct StridedSweep {
     int n_outer; // number of outer indices (nz for y, ny for z)
     int rowlen;  // nx*S
     int tiles_per_row;
-    int tiles;   // tiles_per_row * n_outer
+    int tiles;   // tiles_per_row * n_outer * reps
+    int reps;    // ensemble replicas stacked along the 4th tensor dimension (ring kernel)
     int S;
     int nx;
     long long stride;       // (plain kernel) doubles between positions along the axis
@@ -217,15 +219,15 @@ struct StridedSweep {
     double* exp_top;
 };
 
-__device__ __forceinline__ Chain make_chain(const Coef& coef, int S, int s, int n, const Clamp& cl, bool face)
+__device__ __forceinline__ Chain make_chain(const Coef& coef, int S, int s, int n, const Clamp& cl, bool face, int r = 0)
 {
     Chain c;
     c.S = S;
-    c.dinv = coef.dinv + s;
-    c.cb = coef.cb + s;
-    c.q = coef.q[s];
-    c.dc = coef.dconst[s];
-    c.cc = coef.cconst[s];
+    c.dinv = coef.dinv + r * coef.rstride + s;
+    c.cb = coef.cb + r * coef.rstride + s;
+    c.q = coef.q[r * S + s];
+    c.dc = coef.dconst[r * S + s];
+    c.cc = coef.cconst[r * S + s];
     c.settle = coef.settle;
     c.n = n;
     c.clamp_s = (cl.mask >> s) & 1ull;
@@ -238,10 +240,10 @@ __device__ __forceinline__ Chain make_chain(const Coef& coef, int S, int s, int 
 
 // Chain of a y/z tile lane: column (i, s) at outer index `outer` (k for y,
 // j for z). Along z the line ends are global faces only on the first/last slab.
-__device__ __forceinline__ Chain make_chain_yz(const StridedSweep& a, int s, int i, int outer)
+__device__ __forceinline__ Chain make_chain_yz(const StridedSweep& a, int s, int i, int outer, int r = 0)
 {
     const bool outer_face = a.axis == 2 ? (outer == 0 || outer == a.n_outer - 1) : kface(outer, a.clamp);
-    Chain c = make_chain(a.coef, a.S, s, a.n, a.clamp, i == 0 || i == a.nx - 1 || outer_face);
+    Chain c = make_chain(a.coef, a.S, s, a.n, a.clamp, i == 0 || i == a.nx - 1 || outer_face, r);
     if (a.axis == 2) {
         c.face_lo = a.clamp.k0 == 0;
         c.face_hi = a.clamp.k0 + a.n == a.clamp.nzg;
@@ -268,7 +270,7 @@ static __global__ void __launch_bounds__(kLanes) sweep_yz_tma(const __grid_const
         const int c1 = a.axis == 2 ? outer : k * kChunk;
         const int c2 = a.axis == 2 ? k * kChunk : outer;
         ptx::mbar_arrive_expect_tx(&bars[slot], kSlot * 8);
-        ptx::tma_load_3d(slots + slot * kSlot, &tmap, e0, c1, c2, &bars[slot]);
+        ptx::tma_load_4d(slots + slot * kSlot, &tmap, e0, c1, c2, 0, &bars[slot]);
     };
     if (lane == 0) {
         ptx::tma_prefetch_desc(&tmap);
@@ -299,7 +301,7 @@ static __global__ void __launch_bounds__(kLanes) sweep_yz_tma(const __grid_const
                 if (lane == 0) {
                     const int c1 = a.axis == 2 ? outer : k * kChunk;
                     const int c2 = a.axis == 2 ? k * kChunk : outer;
-                    ptx::tma_store_3d(&tmap, e0, c1, c2, slots + slot_of(k) * kSlot);
+                    ptx::tma_store_4d(&tmap, e0, c1, c2, 0, slots + slot_of(k) * kSlot);
                     ptx::bulk_commit();
                     if (tnext < a.tiles) {
                         // The store of chunk k+1 (issued one step earlier) has
@@ -362,6 +364,7 @@ struct XSweep {
     Coef coef;
     long long lines; // ny*nz
     long long tiles; // ceil(lines / L)
+    long long lines_per_rep; // ny*nz (ensembles stack replicas along the lines)
     int nx, ny, nz, S;
     int rowlen;      // nx*S
     int cpitch;      // smem doubles per line within a chunk slot
@@ -616,21 +619,23 @@ struct Ring {
 };
 
 template <bool CLAMP>
-static __global__ void __launch_bounds__(kLanes) sweep_yz_ring(const __grid_constant__ CUtensorMap tmap, StridedSweep a, Ring r)
+static __global__ void __launch_bounds__(kLanes) sweep_yz_ring(const __grid_constant__ CUtensorMap tmap, StridedSweep a, Ring rg)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int kSlot = kChunk * kLanes;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
-    double* slots = reinterpret_cast<double*>(smem + bar_bytes(r.ns));
-    double* ckpt = slots + r.ns * kSlot;
+    double* slots = reinterpret_cast<double*>(smem + bar_bytes(rg.ns));
+    double* ckpt = slots + rg.ns * kSlot;
     const int lane = threadIdx.x;
     const int t = blockIdx.x;
     const int e0 = (t % a.tiles_per_row) * kLanes;
-    const int outer = t / a.tiles_per_row;
+    const int outer_all = t / a.tiles_per_row;
+    const int r = outer_all / a.n_outer; // ensemble replica
+    const int outer = outer_all % a.n_outer;
     const int width = min(kLanes, a.rowlen - e0);
     if (lane == 0) {
         ptx::tma_prefetch_desc(&tmap);
-        for (int s = 0; s < r.ns; ++s) ptx::mbar_init(&bars[s], 1);
+        for (int s = 0; s < rg.ns; ++s) ptx::mbar_init(&bars[s], 1);
         ptx::fence_mbar_init();
     }
     __syncwarp();
@@ -641,28 +646,29 @@ static __global__ void __launch_bounds__(kLanes) sweep_yz_ring(const __grid_cons
     const bool active = lane < width;
     const int e = e0 + (active ? lane : 0);
     const int s = e % a.S, i = e / a.S;
-    const Chain c = make_chain_yz(a, s, i, outer);
+    const Chain c = make_chain_yz(a, s, i, outer, r);
     const uint64_t keep_pol = ptx::policy_evict_last(), stream_pol = ptx::policy_evict_first();
     // Plane index of this column for the z-slab exports (z axis: outer = j).
     const SlabExport ex{a.exp_bottom, a.exp_top, static_cast<long long>(outer) * a.rowlen + e};
     solve_ring<CLAMP>(
-        c, active, kLanes, r.ns, bars, ckpt, lane, [&](int slot) { return slots + slot * kSlot + lane; },
+        c, active, kLanes, rg.ns, bars, ckpt, lane, [&](int slot) { return slots + slot * kSlot + lane; },
         [&](int k, int slot, bool keep) {
             int c1, c2;
             box(k, c1, c2);
             ptx::mbar_arrive_expect_tx(&bars[slot], kSlot * 8);
-            if (r.hints)
-                ptx::tma_load_3d_hint(slots + slot * kSlot, &tmap, e0, c1, c2, &bars[slot], keep ? keep_pol : stream_pol);
+            if (rg.hints)
+                ptx::tma_load_4d_hint(slots + slot * kSlot, &tmap, e0, c1, c2, r, &bars[slot],
+                                      keep ? keep_pol : stream_pol);
             else
-                ptx::tma_load_3d(slots + slot * kSlot, &tmap, e0, c1, c2, &bars[slot]);
+                ptx::tma_load_4d(slots + slot * kSlot, &tmap, e0, c1, c2, r, &bars[slot]);
         },
         [&](int k, int slot) {
             int c1, c2;
             box(k, c1, c2);
-            if (r.hints)
-                ptx::tma_store_3d_hint(&tmap, e0, c1, c2, slots + slot * kSlot, stream_pol);
+            if (rg.hints)
+                ptx::tma_store_4d_hint(&tmap, e0, c1, c2, r, slots + slot * kSlot, stream_pol);
             else
-                ptx::tma_store_3d(&tmap, e0, c1, c2, slots + slot * kSlot);
+                ptx::tma_store_4d(&tmap, e0, c1, c2, r, slots + slot * kSlot);
         },
         &ex);
 }
@@ -689,8 +695,10 @@ static __global__ void __launch_bounds__(kLanes) sweep_x_ring(XSweep a, Ring r)
     const int l = active ? lane / S : 0;
     const int sub = active ? lane % S : 0;
     const long long line = t * a.L + l;
-    const int j = static_cast<int>(line % a.ny), kk = static_cast<int>(line / a.ny);
-    const Chain c = make_chain(a.coef, S, sub, a.nx, a.clamp, j == 0 || j == a.ny - 1 || kface(kk, a.clamp));
+    const int rep = static_cast<int>(line / a.lines_per_rep); // ensemble replica of this lane's line
+    const long long rline = line % a.lines_per_rep;
+    const int j = static_cast<int>(rline % a.ny), kk = static_cast<int>(rline / a.ny);
+    const Chain c = make_chain(a.coef, S, sub, a.nx, a.clamp, j == 0 || j == a.ny - 1 || kface(kk, a.clamp), rep);
     const uint64_t keep_pol = ptx::policy_evict_last(), stream_pol = ptx::policy_evict_first();
     auto bytes_of = [&](int k) { return static_cast<uint32_t>(min(kChunk, a.nx - k * kChunk) * S * 8); };
     solve_ring<CLAMP>(

@@ -60,22 +60,23 @@ __device__ __forceinline__ void bulk_s2g(void* dst_gmem, const void* src_smem, u
                  : "memory");
 }
 
-// 3-D tiled TMA load (SASS UTMALDG): box at coordinates (c0, c1, c2) of the
+// 4-D tiled TMA load (SASS UTMALDG): box at coordinates (c0, c1, c2) of the
 // tensor map -> shared memory, completion signalled on `bar`.
-__device__ __forceinline__ void tma_load_3d(void* dst_smem, const void* tmap, int c0, int c1, int c2, uint64_t* bar)
+__device__ __forceinline__ void tma_load_4d(void* dst_smem, const void* tmap, int c0, int c1, int c2, int c3,
+                                            uint64_t* bar)
 {
     asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-        "[%5];" ::"r"(smem_addr(dst_smem)),
-        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar))
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+        "[%6];" ::"r"(smem_addr(dst_smem)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(bar))
         : "memory");
 }
 
-// 3-D tiled TMA store (SASS UTMASTG) tracked by this thread's bulk async-group.
-__device__ __forceinline__ void tma_store_3d(const void* tmap, int c0, int c1, int c2, const void* src_smem)
+// 4-D tiled TMA store (SASS UTMASTG) tracked by this thread's bulk async-group.
+__device__ __forceinline__ void tma_store_4d(const void* tmap, int c0, int c1, int c2, int c3, const void* src_smem)
 {
-    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(tmap),
-                 "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(src_smem))
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(tmap),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(src_smem))
                  : "memory");
 }
 
@@ -93,22 +94,24 @@ __device__ __forceinline__ uint64_t policy_evict_first()
     return p;
 }
 
-__device__ __forceinline__ void tma_load_3d_hint(void* dst_smem, const void* tmap, int c0, int c1, int c2,
+__device__ __forceinline__ void tma_load_4d_hint(void* dst_smem, const void* tmap, int c0, int c1, int c2, int c3,
                                                  uint64_t* bar, uint64_t policy)
 {
     asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, "
-        "{%2, %3, %4}], [%5], %6;" ::"r"(smem_addr(dst_smem)),
-        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar)), "l"(policy)
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, "
+        "{%2, %3, %4, %5}], [%6], %7;" ::"r"(smem_addr(dst_smem)),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(bar)), "l"(policy)
         : "memory");
 }
 
-__device__ __forceinline__ void tma_store_3d_hint(const void* tmap, int c0, int c1, int c2, const void* src_smem,
-                                                  uint64_t policy)
+__device__ __forceinline__ void tma_store_4d_hint(const void* tmap, int c0, int c1, int c2, int c3,
+                                                  const void* src_smem, uint64_t policy)
 {
-    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], [%4], %5;" ::"l"(tmap),
-                 "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(src_smem)), "l"(policy)
-                 : "memory");
+    asm volatile(
+        "cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%1, %2, %3, %4}], [%5], %6;" ::"l"(
+            tmap),
+        "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_addr(src_smem)), "l"(policy)
+        : "memory");
 }
 
 __device__ __forceinline__ void bulk_g2s_hint(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar,
