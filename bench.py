@@ -117,14 +117,14 @@ def cpu_reference_timing(w, sample_budget_s=20.0, max_steps=None):
     t1 = ref.run(1)  # warm-up step (also sizes the sample)
     n = max(1, min(int(sample_budget_s * 0.6 / max(t1, 1e-6)), 50 if max_steps is None else max_steps))
     t = ref.run(n)
-    out["value"] = w.vsu_per_step * n / t
+    out["value"] = w.voxels * w.S * n / t  # one microenvironment (replica 0 for C5)
     out["sample"] = f"{n} full steps of {w.name.split(':')[0]} on {cores} threads (reference WorkerPool parallel({cores}))"
     ref.close()
     ser = oracle.Reference(w, workers=0)
     t1s = ser.run(1)
     ns = max(1, min(int(sample_budget_s * 0.4 / max(t1s, 1e-6)), 10))
     ts = ser.run(ns)
-    out["single_core"] = {"value": w.vsu_per_step * ns / ts, "cores": 1,
+    out["single_core"] = {"value": w.voxels * w.S * ns / ts, "cores": 1,
                           "sample": f"{ns} full steps, BackendKind::serial()"}
     ser.close()
     return out
@@ -146,8 +146,11 @@ def run_reference_arm(args, w):
     budget = 120.0
     n = max(1, min(args.steps, int(budget / max(per, 1e-9))))
     t = ref.run(n)
-    value = w.vsu_per_step * n / t
-    sample = (f"{n} of {args.steps} requested full steps of {w.name.split(':')[0]} on {cores} threads "
+    # One microenvironment per reference run: for the C5 ensemble that is
+    # replica 0 (the replicas are independent; the reference runs them one by one).
+    value = w.voxels * w.S * n / t
+    what = "replica 0 of C5" if w.replicas > 1 else w.name.split(':')[0]
+    sample = (f"{n} of {args.steps} requested full steps of {what} on {cores} threads "
               f"(reference WorkerPool parallel({cores}), steady_clock around the step loop)")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
@@ -175,7 +178,7 @@ def main():
                     help="timed steps (default 1000 for C1-C3, 20 for C4)")
     ap.add_argument("--warmup", type=int, default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default=None, choices=["c1", "c2", "c3", "c4"],
+    ap.add_argument("--workload", default=None, choices=["c1", "c2", "c3", "c4", "c5"],
                     help="default: c3 at N=1, c4 (z-slab decomposition) at N>1")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
@@ -185,7 +188,7 @@ def main():
         args.workload = "c3" if world == 1 else "c4"
     big = args.workload == "c4"
     if args.steps is None:
-        args.steps = 20 if big else 1000
+        args.steps = 20 if big else (200 if args.workload == "c5" else 1000)
     if args.warmup is None:
         args.warmup = 3 if big else 20
     if args.warmup < 3:
@@ -214,8 +217,15 @@ def main():
             dist.barrier()
 
     device = local if world > 1 else 0
-    zslab = big or world > 1
-    if zslab:
+    ensemble = args.workload == "c5"
+    zslab = (big or world > 1) and not ensemble
+    if ensemble:
+        # C5: this rank's share of the 512 replicas in one stacked session; no communication.
+        from paper_2110_13368_b200.ensemble import ensemble_session, shard
+        lo, hi = shard(W.C5_REPLICAS, world, rank)
+        s = ensemble_session([W.c5_replica(r, args.steps) for r in range(lo, hi)], device=device)
+        local_values = w.voxels * w.S * (hi - lo)
+    elif zslab:
         # C4: one z-slab per rank, interface planes over NCCL (csrc/slab.cu).
         from paper_2110_13368_b200.zslab import ZSlabRank
         uid = [B.Session.nccl_unique_id() if (rank == 0 and world > 1) else None]
@@ -228,7 +238,7 @@ def main():
         s = W.session_for(w, device=device)
         local_values = w.voxels * w.S
     field_bytes = local_values * 8
-    vsu_total = w.vsu_per_step if zslab else w.vsu_per_step * world
+    vsu_total = w.vsu_per_step if (zslab or ensemble) else w.vsu_per_step * world
 
     # Warm-up (also instantiates graphs / loads modules).
     s.advance(args.warmup, w.dt)
@@ -317,10 +327,14 @@ def main():
         if zslab:
             cfg["parallelism"] = f"z-slab x{world} (partitioned z-solve, NCCL plane exchange)" if world > 1 \
                 else "single GPU (one z-slab)"
+        if ensemble:
+            cfg["parallelism"] = f"{W.C5_REPLICAS} replicas sharded over {world} GPU(s), no communication, " \
+                                 f"one stacked session per GPU"
+            cfg["l2"] = f"{W.C5_REPLICAS // world} replicas x {w.voxels * w.S * 8 / 1e6:.1f} MB per GPU"
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if zslab else "weak",
+            "scaling": "strong" if (zslab or ensemble) else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic, seeded spherical-tumour layout (paper_2110_13368_b200/workloads.py, SURVEY.md §8 d3)",
             "config": cfg,

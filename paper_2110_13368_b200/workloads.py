@@ -236,7 +236,18 @@ def c5_replica(r: int, steps=100):
     return w
 
 
-CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4}
+C5_REPLICAS = 512
+
+
+def c5(steps=200):
+    """C5 as a whole: replica 0 stands for the batch (vsu counts all 512)."""
+    w = c5_replica(0, steps)
+    w.name = f"C5: ensemble of {C5_REPLICAS} x (64^3 x 2 substrates, 1k cells), per-replica D/lambda and layouts"
+    w.replicas = C5_REPLICAS
+    return w
+
+
+CONFIGS = {"c1": c1, "c2": c2, "c3": c3, "c4": c4, "c5": c5}
 
 
 def session_for(w: Workload, device: int = 0):
