@@ -120,6 +120,9 @@ def ref_lib():
         L.ref_run.argtypes = [_vp, _i64, _d, ctypes.c_int, _P(_d)]
         L.ref_convergence.argtypes = [ctypes.c_int, ctypes.c_int, _P(_d), _P(_d), _P(_d), _P(ctypes.c_int)]
         L.ref_mutant_check.argtypes = [_P(ctypes.c_int)]
+        L.ref_format_double.argtypes = [_d, ctypes.c_char_p, ctypes.c_int]
+        L.ref_snapshot.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, _i64]
+        L.ref_snapshot.restype = _i64
         _ref = L
     return _ref
 
@@ -325,6 +328,16 @@ class Reference:
     def sources(self, dt):
         _rchk(ref_lib().ref_sources_step(self.h, dt))
 
+    def snapshot(self, table: bool, substrate: int, z_slice: int) -> str:
+        """validation.cpp:155-200 snapshot text of the current field."""
+        L = ref_lib()
+        need = L.ref_snapshot(self.h, 1 if table else 0, substrate, z_slice, None, 0)
+        if need < 0:
+            raise RefError(2, L.ref_last_error().decode())
+        buf = ctypes.create_string_buffer(int(need))
+        L.ref_snapshot(self.h, 1 if table else 0, substrate, z_slice, buf, need)
+        return buf.value.decode()
+
     def run(self, steps, with_sources=True):
         """Returns the steady_clock seconds of the step loop alone."""
         sec = _d()
@@ -336,6 +349,12 @@ def ref_convergence(kind: int, levels: int):
     o, st, er, p = _d(), np.zeros(levels), np.zeros(levels), ctypes.c_int()
     _rchk(ref_lib().ref_convergence(kind, levels, ctypes.byref(o), _dp(st), _dp(er), ctypes.byref(p)))
     return o.value, st, er, bool(p.value)
+
+
+def ref_format_double(v: float) -> str:
+    buf = ctypes.create_string_buffer(64)
+    _rchk(ref_lib().ref_format_double(v, buf, 64))
+    return buf.value.decode()
 
 
 def ref_mutant_check():

@@ -23,7 +23,10 @@
 #include "core/errors.hpp"
 #include "core/mesh.hpp"
 #include "core/solver.hpp"
+#include "core/text.hpp"
 #include "core/validation.hpp"
+
+#include <sstream>
 
 #include <chrono>
 #include <cstdint>
@@ -307,6 +310,35 @@ int ref_convergence(int kind, int levels, double* order, double* steps, double* 
         }
         *pass = r.pass ? 1 : 0;
     });
+}
+
+// text.cpp:9-14 format_double (shortest round trip, std::to_chars).
+int ref_format_double(double v, char* out, int cap)
+{
+    const std::string s = format_double(v);
+    if (static_cast<int>(s.size()) + 1 > cap) return 2;
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return 0;
+}
+
+// validation.cpp:155-200 write_snapshot_pgm / write_snapshot_table of the
+// current field into `out` (NUL-terminated); returns the byte count needed.
+int64_t ref_snapshot(void* h, int table, int substrate, int z_slice, char* out, int64_t cap)
+{
+    auto* c = static_cast<RefCtx*>(h);
+    std::ostringstream os;
+    try {
+        if (table)
+            write_snapshot_table(c->env.field, c->env.mesh, substrate, z_slice, os);
+        else
+            write_snapshot_pgm(c->env.field, c->env.mesh, substrate, z_slice, os);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
+    }
+    const std::string s = os.str();
+    if (out && static_cast<int64_t>(s.size()) + 1 <= cap) std::memcpy(out, s.c_str(), s.size() + 1);
+    return static_cast<int64_t>(s.size()) + 1;
 }
 
 // Method 3 mutant (validation.cpp:274-287): flags = {clean, crosscheck, table}.

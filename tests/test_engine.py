@@ -1,0 +1,52 @@
+"""Engine loop: clock accounting on CPU, the run on GPU."""
+import numpy as np
+import pytest
+
+import paper_2110_13368_b200 as B
+from oracle import Oracle
+from paper_2110_13368_b200 import workloads as W
+from paper_2110_13368_b200.engine import SimulationClock, run_simulation
+from tests.helpers import bits_equal, make_session
+
+
+def test_clock_defaults_and_ratio_validation():
+    c = SimulationClock(t_max=60.0)
+    assert (c.total_steps, c.per_mech, c.per_cell) == (6000, 10, 60)
+    assert SimulationClock(t_max=0.0).total_steps == 0
+    with pytest.raises(B.ConfigError):
+        SimulationClock(dt_diff=0.1, dt_mech=0.25)  # ratio 2.5
+    with pytest.raises(B.ConfigError):
+        SimulationClock(dt_diff=0.0)
+
+
+@pytest.mark.gpu
+def test_engine_step_accounting_and_result():
+    """60 sim-min at the defaults: exactly 6000 / 600 / 10 steps (SPEC.md:515 criterion 7);
+    the field equals 6000 plain steps."""
+    if B.device_count() == 0:
+        pytest.fail("no sm_100 device visible")
+    w = W.make("engine", (20, 18, 16), 2, 200, 6000, seed=4)
+    s = make_session(w)
+    mech, cell, snaps = [], [], []
+    m = run_simulation(s, SimulationClock(t_max=60.0), mech_hook=lambda c: mech.append(c.diffusion_steps),
+                       cell_hook=lambda c: cell.append(c.mechanics_steps), snapshot_interval=15.0,
+                       snapshot_hook=lambda t, f: snaps.append(t))
+    assert (m.diffusion_steps, m.mechanics_steps, m.cell_steps) == (6000, 600, 10)
+    assert len(mech) == 600 and mech[0] == 10 and cell == [60 * k for k in range(1, 11)]
+    assert snaps == [15.0, 30.0, 45.0, 60.0] and m.snapshots == 4
+    got = s.download_field()
+    ref = make_session(w)
+    ref.advance(6000, w.dt)
+    assert bits_equal(got, ref.download_field())
+    assert m.diffusion_seconds > 0 and all(line.count("=") == 1 for line in m.as_lines())
+
+
+@pytest.mark.gpu
+def test_engine_zero_time_keeps_initial_condition():
+    if B.device_count() == 0:
+        pytest.fail("no sm_100 device visible")
+    w = W.make("engine0", (10, 10, 10), 1, 0, 1)
+    s = make_session(w)
+    m = run_simulation(s, SimulationClock(t_max=0.0))
+    assert m.diffusion_steps == 0
+    assert np.array_equal(s.download_field(), w.initial_field())
