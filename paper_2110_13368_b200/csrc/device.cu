@@ -2,6 +2,7 @@
 // capture of the step loop, and the DeviceBackend glue of host.hpp.
 #include "device.hpp"
 #include "kernels.cuh"
+#include "ring.cuh"
 
 #include <cuda_runtime.h>
 
@@ -111,6 +112,7 @@ DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int devi
     if (prop.major != 10)
         throw state_error(std::string("device ") + prop.name + " is not sm_100 (Blackwell B200); this build targets sm_100a only");
     sm_count_ = prop.multiProcessorCount;
+    ring_persistent_ = std::atoi(env_or("BIODIFF_RING_PERSIST", "1")) != 0;
     nzg_ = mesh.nz;
     cudaStream_t st;
     ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -655,9 +657,15 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
         x.tiles = (x.lines + x.L - 1) / x.L;
         x.clamp = cl;
         if (ring) {
-            auto k = do_clamp ? kernels::sweep_x_ring<true> : kernels::sweep_x_ring<false>;
-            ck(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
-            k<<<static_cast<unsigned>(x.tiles), kernels::kLanes, smem, st>>>(x, rg);
+            if (ring_persistent_) {
+                auto k = do_clamp ? kernels::sweep_x_pring<true> : kernels::sweep_x_pring<false>;
+                const unsigned grid = persistent_grid(reinterpret_cast<const void*>(k), x.tiles);
+                k<<<grid, kernels::kLanes, smem, st>>>(x, rg);
+            } else {
+                auto k = do_clamp ? kernels::sweep_x_ring<true> : kernels::sweep_x_ring<false>;
+                ck(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
+                k<<<static_cast<unsigned>(x.tiles), kernels::kLanes, smem, st>>>(x, rg);
+            }
         } else if (bulk) {
             auto k = do_clamp ? kernels::sweep_x_bulk<true> : kernels::sweep_x_bulk<false>;
             const unsigned grid = persistent_grid(reinterpret_cast<const void*>(k), x.tiles);
@@ -691,9 +699,15 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
     y.exp_top = (slab_ && ax == 2) ? plane_top_ : nullptr;
     if (ring) {
         const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(tmap_[ax]);
-        auto k = do_clamp ? kernels::sweep_yz_ring<true> : kernels::sweep_yz_ring<false>;
-        ck(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
-        k<<<static_cast<unsigned>(y.tiles), kernels::kLanes, smem, st>>>(tm, y, rg);
+        if (ring_persistent_) {
+            auto k = do_clamp ? kernels::sweep_yz_pring<true> : kernels::sweep_yz_pring<false>;
+            const unsigned grid = persistent_grid(reinterpret_cast<const void*>(k), y.tiles);
+            k<<<grid, kernels::kLanes, smem, st>>>(tm, y, rg);
+        } else {
+            auto k = do_clamp ? kernels::sweep_yz_ring<true> : kernels::sweep_yz_ring<false>;
+            ck(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
+            k<<<static_cast<unsigned>(y.tiles), kernels::kLanes, smem, st>>>(tm, y, rg);
+        }
     } else if (bulk) {
         const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(tmap_[ax]);
         auto k = do_clamp ? kernels::sweep_yz_tma<true> : kernels::sweep_yz_tma<false>;

@@ -29,7 +29,11 @@ def _paths(monkeypatch, path):
     (4 slots), ringN = ring with N slots (more recompute), resident = whole
     line in shared memory, smem_plain, global."""
     monkeypatch.delenv("BIODIFF_RING_SLOTS", raising=False)
-    if path == "auto":
+    monkeypatch.delenv("BIODIFF_RING_PERSIST", raising=False)
+    if path == "ringnp":  # one tile per CTA (non-persistent ring)
+        monkeypatch.setenv("BIODIFF_RING_PERSIST", "0")
+        monkeypatch.delenv("BIODIFF_SWEEP_PATH", raising=False)
+    elif path == "auto":
         monkeypatch.delenv("BIODIFF_SWEEP_PATH", raising=False)
     elif path.startswith("ring"):
         monkeypatch.setenv("BIODIFF_SWEEP_PATH", "ring")
@@ -45,7 +49,7 @@ SWEEP_SHAPES = [
 ]
 
 
-@pytest.mark.parametrize("path", ["auto", "ring2", "ring3", "resident", "global", "smem_plain"])
+@pytest.mark.parametrize("path", ["auto", "ringnp", "ring2", "ring3", "resident", "global", "smem_plain"])
 @pytest.mark.parametrize("shape,S", SWEEP_SHAPES)
 def test_single_sweep_bitwise(shape, S, path, monkeypatch):
     """diffusion_sweep (solver.cpp:330-347) along every active axis, every kernel path."""
