@@ -112,7 +112,11 @@ DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int devi
     if (prop.major != 10)
         throw state_error(std::string("device ") + prop.name + " is not sm_100 (Blackwell B200); this build targets sm_100a only");
     sm_count_ = prop.multiProcessorCount;
-    ring_persistent_ = std::atoi(env_or("BIODIFF_RING_PERSIST", "1")) != 0;
+    // Persistent ring CTAs measured faster for x (C3: 234 -> 223 us) and
+    // slower for y/z (211 -> 229 us): default "x". "1"/"all", "0"/"none".
+    const std::string persist = env_or("BIODIFF_RING_PERSIST", "x");
+    ring_persist_x_ = persist != "0" && persist != "none";
+    ring_persist_yz_ = persist == "1" || persist == "all";
     nzg_ = mesh.nz;
     cudaStream_t st;
     ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -657,7 +661,7 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
         x.tiles = (x.lines + x.L - 1) / x.L;
         x.clamp = cl;
         if (ring) {
-            if (ring_persistent_) {
+            if (ring_persist_x_) {
                 auto k = do_clamp ? kernels::sweep_x_pring<true> : kernels::sweep_x_pring<false>;
                 const unsigned grid = persistent_grid(reinterpret_cast<const void*>(k), x.tiles);
                 k<<<grid, kernels::kLanes, smem, st>>>(x, rg);
@@ -699,7 +703,7 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
     y.exp_top = (slab_ && ax == 2) ? plane_top_ : nullptr;
     if (ring) {
         const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(tmap_[ax]);
-        if (ring_persistent_) {
+        if (ring_persist_yz_) {
             auto k = do_clamp ? kernels::sweep_yz_pring<true> : kernels::sweep_yz_pring<false>;
             const unsigned grid = persistent_grid(reinterpret_cast<const void*>(k), y.tiles);
             k<<<grid, kernels::kLanes, smem, st>>>(tm, y, rg);

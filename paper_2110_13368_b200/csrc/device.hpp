@@ -160,7 +160,8 @@ private:
     double dt_ = 0.0;
     SweepPath path_[3] = {SweepPath::global, SweepPath::global, SweepPath::global};
     int sm_count_ = 148;
-    bool ring_persistent_ = true; // persistent ring kernels (BIODIFF_RING_PERSIST=0: one tile per CTA)
+    bool ring_persist_x_ = true;   // persistent ring kernels per axis (BIODIFF_RING_PERSIST)
+    bool ring_persist_yz_ = false;
     int sweep_smem_bytes(int axis, bool bulk) const;
     int ring_slots(int axis) const;
     int ring_smem_bytes(int axis) const;
