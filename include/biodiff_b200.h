@@ -193,8 +193,9 @@ int biodiff_ensemble_set_agents(biodiff_session* session, int64_t n, const int32
  * take the GLOBAL inputs (global voxel indices, all agents) and keep the
  * slab's share. The z sweep is a partitioned solve: zero-inflow slab solves
  * plus two nearest-neighbour plane exchanges and an inflow correction (see
- * paper_2110_13368_b200/csrc/slab.cu). Slabs with two neighbours must be thick
- * enough that the cross-slab coupling is below 2^-60 (status 1 otherwise). */
+ * paper_2110_13368_b200/csrc/slab.cu). The interface recurrences are exact,
+ * so any slab thickness >= 1 plane is accepted; results match the single
+ * domain to rounding (the correction re-associates: not bit-identical). */
 int biodiff_zslab_create(const biodiff_mesh* global_mesh, int32_t substrates, int32_t z0, int32_t z1, int32_t device,
                          biodiff_session** out);
 int biodiff_zslab_info(biodiff_session* session, int32_t* z0, int32_t* z1, int32_t* nz_global);

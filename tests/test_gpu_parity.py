@@ -30,8 +30,8 @@ def _paths(monkeypatch, path):
     line in shared memory, smem_plain, global."""
     monkeypatch.delenv("BIODIFF_RING_SLOTS", raising=False)
     monkeypatch.delenv("BIODIFF_RING_PERSIST", raising=False)
-    if path == "ringnp":  # one tile per CTA (non-persistent ring)
-        monkeypatch.setenv("BIODIFF_RING_PERSIST", "0")
+    if path in ("ringnp", "ringall"):  # ring with no / every axis persistent
+        monkeypatch.setenv("BIODIFF_RING_PERSIST", "0" if path == "ringnp" else "all")
         monkeypatch.delenv("BIODIFF_SWEEP_PATH", raising=False)
     elif path == "auto":
         monkeypatch.delenv("BIODIFF_SWEEP_PATH", raising=False)
@@ -49,7 +49,7 @@ SWEEP_SHAPES = [
 ]
 
 
-@pytest.mark.parametrize("path", ["auto", "ringnp", "ring2", "ring3", "resident", "global", "smem_plain"])
+@pytest.mark.parametrize("path", ["auto", "ringnp", "ringall", "ring2", "ring3", "resident", "global", "smem_plain"])
 @pytest.mark.parametrize("shape,S", SWEEP_SHAPES)
 def test_single_sweep_bitwise(shape, S, path, monkeypatch):
     """diffusion_sweep (solver.cpp:330-347) along every active axis, every kernel path."""
