@@ -154,7 +154,8 @@ int biodiff_session_stream(biodiff_session* session, void** stream);
  * returns, per kernel class, the number of launches and the summed device
  * milliseconds since the last reset. Classes: 0 sweep_x, 1 sweep_y,
  * 2 sweep_z, 3 dirichlet, 4 sources, 5 aux (set-up kernels: per-dt source factors,
- * cross_check). Returns the number of classes in *n. */
+ * cross_check), 6 sweep_xy (the fused x+y sweep of 3-D steps). Returns the
+ * number of classes in *n. */
 int biodiff_set_kernel_timing(biodiff_session* session, int32_t enabled);
 int biodiff_kernel_times(biodiff_session* session, int32_t* n, int64_t* launches, double* milliseconds);
 

@@ -3,10 +3,13 @@
 #include "device.hpp"
 #include "kernels.cuh"
 #include "ring.cuh"
+#include "ring2.cuh"
+#include "xy2.cuh"
 
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -41,6 +44,12 @@ const char* env_or(const char* name, const char* dflt)
 {
     const char* v = std::getenv(name);
     return v ? v : dflt;
+}
+
+__global__ void smem_base_probe(unsigned* out)
+{
+    extern __shared__ __align__(1024) unsigned char smem[];
+    if (threadIdx.x == 0) *out = ptx::smem_addr(smem);
 }
 
 } // namespace
@@ -85,6 +94,21 @@ void DeviceSession::build_tensor_maps()
     const cuuint64_t strides[3] = {static_cast<cuuint64_t>(rowlen) * 8, static_cast<cuuint64_t>(rowlen) * mesh_.ny * 8,
                                    static_cast<cuuint64_t>(rowlen) * mesh_.ny * mesh_.nz * 8};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
+    // x (ring2): 4-D view (16 doubles, j, plane, 16-double piece of the line),
+    // box (16, L, 1, 2S) = one 32-position chunk of L lines, 128-byte swizzle.
+    if ((S_ == 1 || S_ == 2 || S_ == 4) && rowlen % 16 == 0) {
+        const cuuint64_t xd[4] = {16, static_cast<cuuint64_t>(mesh_.ny),
+                                  static_cast<cuuint64_t>(mesh_.nz) * static_cast<cuuint64_t>(replicas_),
+                                  static_cast<cuuint64_t>(rowlen / 16)};
+        const cuuint64_t xs[3] = {static_cast<cuuint64_t>(rowlen) * 8, static_cast<cuuint64_t>(rowlen) * mesh_.ny * 8,
+                                  128};
+        const cuuint32_t xb[4] = {16, static_cast<cuuint32_t>(kernels::kLanes / S_), 1,
+                                  static_cast<cuuint32_t>(2 * S_)};
+        CUresult r = encode(reinterpret_cast<CUtensorMap*>(tmap_[0]), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, rho_, xd, xs,
+                            xb, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        tmap_ok_[0] = (r == CUDA_SUCCESS);
+    }
     for (int ax = 1; ax <= 2; ++ax) {
         const cuuint32_t box[4] = {static_cast<cuuint32_t>(kernels::kLanes),
                                    static_cast<cuuint32_t>(ax == 1 ? kernels::kChunk : 1),
@@ -117,6 +141,7 @@ DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int devi
     const std::string persist = env_or("BIODIFF_RING_PERSIST", "x");
     ring_persist_x_ = persist != "0" && persist != "none";
     ring_persist_yz_ = persist == "1" || persist == "all";
+    xy_fused_ = std::atoi(env_or("BIODIFF_XY_FUSED", "0")) != 0;
     nzg_ = mesh.nz;
     cudaStream_t st;
     ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -125,8 +150,21 @@ DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int devi
     ck(cudaMemsetAsync(rho_, 0, sizeof(double) * value_count(), st), "cudaMemset field");
     ck(cudaMalloc(&shell_values_, sizeof(double) * S_), "cudaMalloc shell");
     ck(cudaMemsetAsync(shell_values_, 0, sizeof(double) * S_, st), "cudaMemset shell");
+    {   // Is the dynamic shared-memory base 1024-byte aligned (no slack needed for the swizzled slots)?
+        unsigned* probe = nullptr;
+        unsigned base = 1;
+        ck(cudaMalloc(&probe, sizeof(unsigned)), "cudaMalloc");
+        smem_base_probe<<<1, 32, 4096, st>>>(probe);
+        ck(cudaMemcpyAsync(&base, probe, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "probe");
+        ck(cudaStreamSynchronize(st), "sync");
+        cudaFree(probe);
+        smem_align_slack_ = (base % 1024 == 0) ? 0 : 1024;
+    }
     build_tensor_maps();
     choose_paths();
+    // Ticket + per-plane counters of the fused x+y kernel (allocated here:
+    // launches may be captured into graphs).
+    ck(cudaMalloc(&xy_ctr_, sizeof(unsigned) * (1 + static_cast<std::size_t>(mesh.nz) * replicas_)), "cudaMalloc");
 }
 
 DeviceSession::~DeviceSession()
@@ -149,6 +187,7 @@ DeviceSession::~DeviceSession()
     dfree(dir_res_mask_);
     dfree(dir_res_values_);
     dfree(shell_values_);
+    dfree(xy_ctr_);
     dfree(group_voxel_);
     dfree(group_offsets_);
     dfree(agent_volume_);
@@ -184,7 +223,9 @@ void DeviceSession::choose_paths()
         const int bulk_bytes = sweep_smem_bytes(ax, true);
         const int plain_bytes = sweep_smem_bytes(ax, false);
         SweepPath p = SweepPath::global;
-        if (async_ok && ring_smem_bytes(ax) <= kMaxSmem && (force == "auto" || force == "ring"))
+        if (ring2_ok(ax) && ring2_smem_bytes(ax) <= kMaxSmem && (force == "auto" || force == "ring2"))
+            p = SweepPath::smem_ring2;
+        else if (async_ok && ring_smem_bytes(ax) <= kMaxSmem && (force == "auto" || force == "ring" || force == "ring2"))
             p = SweepPath::smem_ring;
         else if (async_ok && bulk_bytes <= kMaxSmem && force != "smem_plain" && force != "global")
             p = SweepPath::smem_bulk;
@@ -192,7 +233,7 @@ void DeviceSession::choose_paths()
             p = SweepPath::smem_plain;
         path_[ax] = p;
         const int n = ax == 0 ? mesh_.nx : ax == 1 ? mesh_.ny : mesh_.nz;
-        if (replicas_ > 1 && n > 1 && p != SweepPath::smem_ring)
+        if (replicas_ > 1 && n > 1 && !is_ring(p))
             throw config_error("ensembles need the ring sweep kernels (rows with an even number of doubles, lines "
                                "that fit a shared-memory ring)");
     }
@@ -204,7 +245,10 @@ int DeviceSession::ring_slots(int axis) const
 {
     const int n = axis == 0 ? mesh_.nx : axis == 1 ? mesh_.ny : mesh_.nz;
     const int nch = (n + kernels::kChunk - 1) / kernels::kChunk;
-    const int want = std::max(2, std::atoi(env_or("BIODIFF_RING_SLOTS", "3")));
+    // x: 4 slots (deeper prefetch measured faster: C3 226 -> 217 us); y / z: 3
+    // (4 slots cost occupancy: 8 -> 6 CTAs per SM, slower).
+    const char* e = std::getenv("BIODIFF_RING_SLOTS");
+    const int want = e ? std::max(2, std::atoi(e)) : (axis == 0 ? 4 : 3);
     return std::min(nch, want);
 }
 
@@ -221,6 +265,22 @@ int DeviceSession::ring_smem_bytes(int axis) const
         slot = kernels::kChunk * kernels::kLanes;
     }
     return kernels::bar_bytes(ns) + (ns * slot + nch * kernels::kLanes) * 8;
+}
+
+// ring2 (ring2.cuh): x needs the swizzled 4-D map (S in {1, 2, 4}, rows a
+// multiple of 16 doubles); y / z the plain TMA maps.
+bool DeviceSession::ring2_ok(int axis) const
+{
+    if (!tmap_ok_[axis]) return false;
+    const int ns = ring_slots(axis);
+    return ns >= 1 && ns <= 4;
+}
+
+int DeviceSession::ring2_smem_bytes(int axis) const
+{
+    const int n = axis == 0 ? mesh_.nx : axis == 1 ? mesh_.ny : mesh_.nz;
+    const int nch = (n + kernels::kChunk - 1) / kernels::kChunk;
+    return kernels::ring2_smem_bytes(ring_slots(axis), nch) - 1024 + smem_align_slack_;
 }
 
 // Dynamic shared memory of the tile kernels (bulk: chunk slots + mbarriers;
@@ -630,6 +690,11 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
         end_kernel(ax);
         return;
     }
+    if (p == SweepPath::smem_ring2) {
+        launch_ring2(ax, do_clamp, cl, coef);
+        end_kernel(ax);
+        return;
+    }
     const bool ring = p == SweepPath::smem_ring;
     const int smem = ring ? ring_smem_bytes(ax) : sweep_smem_bytes(ax, bulk);
     const int n_ax = ax == 0 ? mesh_.nx : ax == 1 ? mesh_.ny : mesh_.nz;
@@ -725,6 +790,218 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
     end_kernel(ax);
 }
 
+bool DeviceSession::xy_fusable() const
+{
+    return xy_fused_ && ws_[1].active && path_[0] == SweepPath::smem_ring2 && path_[1] == SweepPath::smem_ring2;
+}
+
+namespace {
+
+template <int NS>
+const void* xy2_pick_s(int S)
+{
+    if (S == 1) return reinterpret_cast<const void*>(kernels::sweep_xy2<NS, 1>);
+    if (S == 2) return reinterpret_cast<const void*>(kernels::sweep_xy2<NS, 2>);
+    return reinterpret_cast<const void*>(kernels::sweep_xy2<NS, 4>);
+}
+
+const void* xy2_pick(int ns, int S)
+{
+    switch (ns) {
+    case 1: return xy2_pick_s<1>(S);
+    case 2: return xy2_pick_s<2>(S);
+    case 3: return xy2_pick_s<3>(S);
+    default: return xy2_pick_s<4>(S);
+    }
+}
+
+} // namespace
+
+// Lag (planes) between X(p) and Y(p) in the fused ticket order: enough
+// tickets that every x item of plane p has finished when Y(p) is handed out
+// (one resident wave ~ one item time, BIODIFF_XY_LAG_WAVES), or
+// BIODIFF_XY_LAG planes.
+static int xy_lag_for(long long resident, int xi, int yi, int planes)
+{
+    const double f = std::atof(env_or("BIODIFF_XY_LAG_WAVES", "1.25"));
+    long long lag = static_cast<long long>(std::ceil(f * static_cast<double>(resident) / (xi + yi)));
+    if (const char* e = std::getenv("BIODIFF_XY_LAG")) lag = std::atoll(e);
+    return static_cast<int>(std::max(1LL, std::min(lag, static_cast<long long>(planes))));
+}
+
+// x then y sweep of a 3-D step (no clamp: z is the last sweep): two ring
+// sweeps, or the fused x+y kernel through L2 (xy2.cuh) when
+// BIODIFF_XY_FUSED=1 (opt-in: measured slower on C3).
+void DeviceSession::launch_xy_sweeps()
+{
+    if (!xy_fusable()) {
+        launch_sweep(Axis::x, false);
+        if (ws_[1].active) launch_sweep(Axis::y, false);
+        return;
+    }
+    launch_xy2();
+}
+
+namespace {
+
+template <int NS, bool CLAMP>
+const void* yz_ring2_fn()
+{
+    return reinterpret_cast<const void*>(kernels::sweep_yz_ring2<NS, CLAMP>);
+}
+
+template <int NS, int S, bool CLAMP>
+const void* x_ring2_fn()
+{
+    return reinterpret_cast<const void*>(kernels::sweep_x_ring2<NS, S, CLAMP>);
+}
+
+template <bool CLAMP>
+const void* yz_ring2_pick(int ns)
+{
+    switch (ns) {
+    case 1: return yz_ring2_fn<1, CLAMP>();
+    case 2: return yz_ring2_fn<2, CLAMP>();
+    case 3: return yz_ring2_fn<3, CLAMP>();
+    default: return yz_ring2_fn<4, CLAMP>();
+    }
+}
+
+template <int S, bool CLAMP>
+const void* x_ring2_pick_ns(int ns)
+{
+    switch (ns) {
+    case 1: return x_ring2_fn<1, S, CLAMP>();
+    case 2: return x_ring2_fn<2, S, CLAMP>();
+    case 3: return x_ring2_fn<3, S, CLAMP>();
+    default: return x_ring2_fn<4, S, CLAMP>();
+    }
+}
+
+template <bool CLAMP>
+const void* x_ring2_pick(int ns, int S)
+{
+    if (S == 1) return x_ring2_pick_ns<1, CLAMP>(ns);
+    if (S == 2) return x_ring2_pick_ns<2, CLAMP>(ns);
+    return x_ring2_pick_ns<4, CLAMP>(ns);
+}
+
+} // namespace
+
+// ring2 launch (ring2.cuh): x persistent over per-plane line tiles (next
+// tile's chunks prefetched), y / z one tile per CTA unless
+// BIODIFF_RING_PERSIST=all.
+void DeviceSession::launch_ring2(int ax, bool do_clamp, const kernels::Clamp& cl, const kernels::Coef& coef)
+{
+    auto st = static_cast<cudaStream_t>(stream_);
+    const int ns = ring_slots(ax);
+    const int smem = ring2_smem_bytes(ax);
+    const int rowlen = mesh_.nx * S_;
+    const CUtensorMap& tm = *reinterpret_cast<const CUtensorMap*>(tmap_[ax]);
+    auto occupancy_grid = [&](const void* fn, long long tiles) {
+        ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
+        int per_sm = 0;
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kernels::kLanes, smem), "occupancy");
+        const long long g = static_cast<long long>(std::max(per_sm, 1)) * sm_count_;
+        return static_cast<unsigned>(std::min(g, tiles));
+    };
+    if (ax == 0) {
+        kernels::XSweep2 x{};
+        x.coef = coef;
+        x.nx = mesh_.nx;
+        x.ny = mesh_.ny;
+        x.nz = mesh_.nz;
+        x.S = S_;
+        x.planes = mesh_.nz * replicas_;
+        const int L = kernels::kLanes / S_;
+        x.xi = (mesh_.ny + L - 1) / L;
+        x.tiles = static_cast<long long>(x.xi) * x.planes;
+        x.clamp = cl;
+        const void* fn = do_clamp ? x_ring2_pick<true>(ns, S_) : x_ring2_pick<false>(ns, S_);
+        const unsigned grid = ring_persist_x_ ? occupancy_grid(fn, x.tiles) : static_cast<unsigned>(x.tiles);
+        if (!ring_persist_x_) ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
+        void* args[] = {const_cast<CUtensorMap*>(&tm), &x};
+        ck(cudaLaunchKernel(fn, dim3(grid), dim3(kernels::kLanes), args, smem, st), "launch x ring2");
+        return;
+    }
+    kernels::StridedSweep y{};
+    y.rho = rho_;
+    y.coef = coef;
+    y.axis = ax;
+    y.n = ax == 1 ? mesh_.ny : mesh_.nz;
+    y.n_outer = ax == 1 ? mesh_.nz : mesh_.ny;
+    y.rowlen = rowlen;
+    y.tiles_per_row = (rowlen + kernels::kLanes - 1) / kernels::kLanes;
+    y.reps = replicas_;
+    y.tiles = y.tiles_per_row * y.n_outer * replicas_;
+    y.S = S_;
+    y.nx = mesh_.nx;
+    y.clamp = cl;
+    y.exp_bottom = (slab_ && ax == 2) ? plane_bottom_ : nullptr;
+    y.exp_top = (slab_ && ax == 2) ? plane_top_ : nullptr;
+    const void* fn = do_clamp ? yz_ring2_pick<true>(ns) : yz_ring2_pick<false>(ns);
+    unsigned grid;
+    if (ring_persist_yz_) {
+        grid = occupancy_grid(fn, y.tiles);
+    } else {
+        ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
+        grid = static_cast<unsigned>(y.tiles);
+    }
+    void* args[] = {const_cast<CUtensorMap*>(&tm), &y};
+    ck(cudaLaunchKernel(fn, dim3(grid), dim3(kernels::kLanes), args, smem, st), "launch yz ring2");
+}
+
+// Fused x+y on ring2 (xy2.cuh).
+void DeviceSession::launch_xy2()
+{
+    auto st = static_cast<cudaStream_t>(stream_);
+    const int S = S_;
+    const DeviceWorkspace& wx = ws_[0];
+    const DeviceWorkspace& wy = ws_[1];
+    kernels::XYFused2 a{};
+    a.xcoef = kernels::Coef{wx.q, wx.dinv, wx.cb, wx.dconst, wx.cconst, wx.settle, static_cast<long long>(wx.n) * S};
+    a.ycoef = kernels::Coef{wy.q, wy.dinv, wy.cb, wy.dconst, wy.cconst, wy.settle, static_cast<long long>(wy.n) * S};
+    a.nx = mesh_.nx;
+    a.ny = mesh_.ny;
+    a.nz = mesh_.nz;
+    a.S = S;
+    a.rowlen = mesh_.nx * S;
+    a.planes = mesh_.nz * replicas_;
+    const int L = kernels::kLanes / S;
+    a.xi = (mesh_.ny + L - 1) / L;
+    a.yi = (a.rowlen + kernels::kLanes - 1) / kernels::kLanes;
+    kernels::StridedSweep& y = a.y;
+    y.coef = a.ycoef;
+    y.axis = 1;
+    y.n = mesh_.ny;
+    y.n_outer = mesh_.nz;
+    y.rowlen = a.rowlen;
+    y.S = S;
+    y.nx = mesh_.nx;
+    y.clamp = kernels::Clamp{shell_values_, 0ull, z0_, nzg_};
+    int ns = std::min(3, (std::max(mesh_.nx, mesh_.ny) + kernels::kChunk - 1) / kernels::kChunk);
+    if (const char* e = std::getenv("BIODIFF_XY_SLOTS")) ns = std::max(1, std::min(4, std::atoi(e)));
+    const int nch = (std::max(mesh_.nx, mesh_.ny) + kernels::kChunk - 1) / kernels::kChunk;
+    const int smem = kernels::ring2_smem_bytes(ns, nch) - 1024 + smem_align_slack_;
+    const void* fn = xy2_pick(ns, S);
+    ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
+    int per_sm = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kernels::kLanes, smem), "occupancy");
+    per_sm = std::max(per_sm, 1);
+    if (const char* e = std::getenv("BIODIFF_XY_CTAS_PER_SM")) per_sm = std::max(1, std::min(per_sm, std::atoi(e)));
+    const long long resident = static_cast<long long>(per_sm) * sm_count_;
+    const long long items = static_cast<long long>(a.planes) * (a.xi + a.yi);
+    a.lag = xy_lag_for(resident, a.xi, a.yi, a.planes);
+    xy_lag_ = a.lag;
+    a.ctr = xy_ctr_;
+    ck(cudaMemsetAsync(xy_ctr_, 0, sizeof(unsigned) * (1 + static_cast<std::size_t>(a.planes)), st), "memset");
+    const unsigned grid = static_cast<unsigned>(std::min(resident, items));
+    begin_kernel(kSweepXY);
+    void* args[] = {tmap_[0], tmap_[1], &a};
+    ck(cudaLaunchKernel(fn, dim3(grid), dim3(kernels::kLanes), args, smem, st), "launch xy2");
+    end_kernel(kSweepXY);
+}
+
 void DeviceSession::launch_residual_dirichlet(bool all_entries)
 {
     const std::int64_t count = all_entries ? dir_all_count_ : dir_res_count_;
@@ -795,8 +1072,12 @@ void DeviceSession::step_body(bool with_sources, double dt)
     if (slab_ && (prev_slab_ || next_slab_))
         throw state_error("in-process z-slabs advance together: use the group advance");
     const Axis last = ws_[2].active ? Axis::z : ws_[1].active ? Axis::y : Axis::x;
-    launch_sweep(Axis::x, last == Axis::x);
-    if (ws_[1].active) launch_sweep(Axis::y, last == Axis::y);
+    if (last == Axis::z) {
+        launch_xy_sweeps();
+    } else {
+        launch_sweep(Axis::x, last == Axis::x);
+        if (ws_[1].active) launch_sweep(Axis::y, last == Axis::y);
+    }
     if (ws_[2].active) launch_sweep(Axis::z, last == Axis::z);
     launch_residual_dirichlet(false);
     if (with_sources) launch_sources(dt);

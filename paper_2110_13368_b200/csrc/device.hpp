@@ -12,7 +12,23 @@
 
 namespace biodiff_b200 {
 
-enum KernelClass { kSweepX = 0, kSweepY = 1, kSweepZ = 2, kDirichlet = 3, kSources = 4, kAux = 5, kNumKernelClasses = 6 };
+namespace kernels {
+struct Clamp;
+struct Coef;
+} // namespace kernels
+using kernels_Clamp = kernels::Clamp;
+using kernels_Coef = kernels::Coef;
+
+enum KernelClass {
+    kSweepX = 0,
+    kSweepY = 1,
+    kSweepZ = 2,
+    kDirichlet = 3,
+    kSources = 4,
+    kAux = 5,
+    kSweepXY = 6, // fused x+y sweeps through L2 (xy2.cuh, opt-in)
+    kNumKernelClasses = 7
+};
 
 // Device-side copy of one SolverWorkspace (solver.hpp:24-33).
 struct DeviceWorkspace {
@@ -30,11 +46,15 @@ struct DeviceWorkspace {
 
 // Which kernel implementation a sweep uses (chosen per axis at set-up; the
 // env var BIODIFF_SWEEP_PATH=smem|global forces one for A/B measurements).
-// smem_ring   : ring of chunk slots + backward recompute (default)
+// smem_ring2  : ring of chunk slots, register-chunk bodies, compile-time slot
+//               count, x moved by one swizzled TMA box per chunk (default, ring2.cuh)
+// smem_ring   : ring of chunk slots + backward recompute (r01 kernels)
 // smem_bulk   : whole line resident in shared memory, persistent CTAs
 // smem_plain  : whole line resident, plain loads (rows not 16-byte aligned)
 // global      : one thread per chain straight from global memory
-enum class SweepPath { smem_ring, smem_bulk, smem_plain, global };
+enum class SweepPath { smem_ring2, smem_ring, smem_bulk, smem_plain, global };
+
+inline bool is_ring(SweepPath p) { return p == SweepPath::smem_ring2 || p == SweepPath::smem_ring; }
 
 // Host-side analysis of a workspace's coefficient columns: the first row
 // from which denom_inv and c_back are bit-constant up to row n-2 (max over
@@ -141,6 +161,10 @@ private:
 
     void check_ready(Axis axis) const;
     void launch_sweep(Axis axis, bool clamp);
+    void launch_ring2(int ax, bool do_clamp, const kernels_Clamp& cl, const kernels_Coef& coef);
+    void launch_xy_sweeps(); // x then y, no clamp (3-D steps): fused through L2 when enabled
+    bool xy_fusable() const;
+    void launch_xy2();
     void launch_residual_dirichlet(bool all_entries);
     void launch_sources(double dt);
     void step_body(bool with_sources, double dt);
@@ -162,9 +186,15 @@ private:
     int sm_count_ = 148;
     bool ring_persist_x_ = true;   // persistent ring kernels per axis (BIODIFF_RING_PERSIST)
     bool ring_persist_yz_ = false;
+    bool xy_fused_ = false;          // BIODIFF_XY_FUSED=1 (opt-in)
+    unsigned* xy_ctr_ = nullptr;     // ticket + per-plane x-done counters of the fused kernel
+    int xy_lag_ = 0;                 // chosen lag (planes) of the last fused launch
     int sweep_smem_bytes(int axis, bool bulk) const;
     int ring_slots(int axis) const;
     int ring_smem_bytes(int axis) const;
+    int ring2_smem_bytes(int axis) const;
+    int smem_align_slack_ = 1024; // extra dynamic smem to 1024-align the ring2 slots (0 when the base is aligned)
+    bool ring2_ok(int axis) const;
 
     // Dirichlet: every entry (for apply_dirichlet), plus the split used by
     // the fused step: a per-substrate "whole boundary shell" rule evaluated in
@@ -219,7 +249,7 @@ private:
     };
     std::map<GraphKey, std::pair<void*, int>> graphs_; // cudaGraphExec_t, kernels per replay
     void* slots_[16] = {};                              // cudaEvent_t for event_record()
-    alignas(64) unsigned char tmap_[3][128] = {};       // CUtensorMap per axis (y, z used)
+    alignas(64) unsigned char tmap_[3][128] = {};       // CUtensorMap per axis (x: swizzled 4-D view for ring2)
     bool tmap_ok_[3] = {false, false, false};
     void build_tensor_maps();
 };

@@ -111,7 +111,7 @@ void DeviceSession::configure_slab(int nz_global, int z0)
         ck(cudaMemsetAsync(*p, 0, bytes, static_cast<cudaStream_t>(stream_)), "cudaMemset plane");
     }
     choose_paths();
-    if (nz_global > 1 && path_[2] != SweepPath::smem_ring)
+    if (nz_global > 1 && !is_ring(path_[2]))
         throw config_error("z-slab needs the TMA ring z-sweep (rows with an even number of doubles)");
 }
 
@@ -192,9 +192,13 @@ void DeviceSession::link_local(const std::vector<DeviceSession*>& slabs)
 void DeviceSession::slab_phase_sweeps()
 {
     check_ready(Axis::x);
-    launch_sweep(Axis::x, false);
-    if (ws_[1].active) launch_sweep(Axis::y, false);
-    if (ws_[2].active) launch_sweep(Axis::z, true);
+    if (ws_[2].active) {
+        launch_xy_sweeps();
+        launch_sweep(Axis::z, true);
+    } else {
+        launch_sweep(Axis::x, false);
+        if (ws_[1].active) launch_sweep(Axis::y, false);
+    }
 }
 
 // D_p = dhat_p + phi_last * D_{p-1} (needed only when a next slab exists).

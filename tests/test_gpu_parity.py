@@ -25,12 +25,16 @@ def _need_gpu():
 
 
 def _paths(monkeypatch, path):
-    """Selects a sweep kernel family (read at session creation): auto = ring
-    (4 slots), ringN = ring with N slots (more recompute), resident = whole
-    line in shared memory, smem_plain, global."""
+    """Selects a sweep kernel family (read at session creation): auto = ring2
+    (register-chunk ring, x 4 slots, y/z 3), r2sN = ring2 with N slots,
+    ringN = the r01 ring kernels with N slots, resident = whole line in
+    shared memory, smem_plain, global."""
     monkeypatch.delenv("BIODIFF_RING_SLOTS", raising=False)
     monkeypatch.delenv("BIODIFF_RING_PERSIST", raising=False)
-    if path in ("ringnp", "ringall"):  # ring with no / every axis persistent
+    if path.startswith("r2s"):
+        monkeypatch.setenv("BIODIFF_SWEEP_PATH", "ring2")
+        monkeypatch.setenv("BIODIFF_RING_SLOTS", path[3:])
+    elif path in ("ringnp", "ringall"):  # ring with no / every axis persistent
         monkeypatch.setenv("BIODIFF_RING_PERSIST", "0" if path == "ringnp" else "all")
         monkeypatch.delenv("BIODIFF_SWEEP_PATH", raising=False)
     elif path == "auto":
@@ -49,7 +53,8 @@ SWEEP_SHAPES = [
 ]
 
 
-@pytest.mark.parametrize("path", ["auto", "ringnp", "ringall", "ring2", "ring3", "resident", "global", "smem_plain"])
+@pytest.mark.parametrize("path", ["auto", "ringnp", "ringall", "r2s2", "r2s4", "ring2", "ring3", "resident", "global",
+                                  "smem_plain"])
 @pytest.mark.parametrize("shape,S", SWEEP_SHAPES)
 def test_single_sweep_bitwise(shape, S, path, monkeypatch):
     """diffusion_sweep (solver.cpp:330-347) along every active axis, every kernel path."""
@@ -70,7 +75,7 @@ def test_single_sweep_bitwise(shape, S, path, monkeypatch):
 
 
 @pytest.mark.parametrize("name", golden_names())
-@pytest.mark.parametrize("path", ["auto", "ring2", "resident", "global"])
+@pytest.mark.parametrize("path", ["auto", "r2s2", "ring3", "resident", "global"])
 def test_golden_fixture_bitwise(name, path, monkeypatch):
     """Full runs vs the reference's own outputs (tests/golden, made by oracle/_ref)."""
     _paths(monkeypatch, path)
@@ -208,13 +213,18 @@ def test_advance_equals_stepwise_and_counts_launches():
     b.close()
 
 
-def test_kernel_timing_reports_every_class():
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_kernel_timing_reports_every_class(fused, monkeypatch):
+    monkeypatch.setenv("BIODIFF_XY_FUSED", fused)
     w = W.make("t", (64, 64, 64), 2, 1000, 1, seed=6, interior_clamps=10)
     s = make_session(w)
     s.set_kernel_timing(True)
     s.advance(3, w.dt)
     t = s.kernel_times()
-    assert t["sweep_x"][0] == t["sweep_y"][0] == t["sweep_z"][0] == 3
+    if fused == "1":  # x and y run as one fused launch per 3-D step (xy.cuh)
+        assert t["sweep_xy"][0] == t["sweep_z"][0] == 3 and t["sweep_x"][0] == t["sweep_y"][0] == 0
+    else:
+        assert t["sweep_x"][0] == t["sweep_y"][0] == t["sweep_z"][0] == 3 and t["sweep_xy"][0] == 0
     assert t["sources"][0] == 3 and t["dirichlet"][0] == 3
     assert all(ms > 0 for n, ms in t.values() if n)
     s.close()
@@ -268,4 +278,36 @@ def test_long_run_within_north_star_tolerance(cfg):
     rep = s.cross_check(want, 0.0, NORTH_STAR_REL_TOL)
     assert rep.passed, rep
     assert bits_equal(got, want), first_diff(got, want)
+    s.close()
+
+
+FUSED_ENVS = [
+    {"BIODIFF_XY_FUSED": "0"},                                                  # separate x and y ring sweeps
+    {"BIODIFF_XY_FUSED": "1"},                                                  # default lag
+    {"BIODIFF_XY_FUSED": "1", "BIODIFF_XY_LAG": "1"},                           # y items wait on counters
+    {"BIODIFF_XY_FUSED": "1", "BIODIFF_XY_LAG": "1000000"},                     # all x items, then all y items
+    {"BIODIFF_XY_FUSED": "1", "BIODIFF_XY_CTAS_PER_SM": "1", "BIODIFF_XY_LAG": "2"},  # few CTAs, many items each
+    {"BIODIFF_XY_FUSED": "1", "BIODIFF_XY_SLOTS": "2"},                         # two-slot ring
+]
+
+
+@pytest.mark.parametrize("env", FUSED_ENVS, ids=["unfused", "fused", "lag1", "lagmax", "1cta", "slots2"])
+@pytest.mark.parametrize("shape,S", SWEEP_SHAPES)
+def test_fused_xy_step_bitwise(shape, S, env, monkeypatch):
+    """The fused x+y kernel (ticketed items, per-plane release/acquire
+    counters) gives the oracle's bits for full steps at every lag setting."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    w = W.make("t", shape, S, 150, 1, seed=9, interior_clamps=4)
+    s = make_session(w)
+    s.advance(6, w.dt, with_sources=True)
+    got = s.download_field()
+    want = Oracle.run(w, 6)
+    assert bits_equal(got, want), first_diff(got, want)
+    s.set_kernel_timing(True)
+    s.diffuse_decay_step()
+    t = s.kernel_times()
+    assert t["sweep_xy"][0] + t["sweep_x"][0] == 1
+    if env.get("BIODIFF_XY_FUSED") != "1":
+        assert t["sweep_xy"][0] == 0
     s.close()
