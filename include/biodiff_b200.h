@@ -57,14 +57,14 @@ const char* biodiff_last_error(void);
 /* ABI version: major*10000 + minor*100 + patch. */
 int32_t biodiff_version(void);
 
-/* CartesianMesh::from_bounds (mesh.hpp:28-31, mesh.cpp:174-206). */
+/* CartesianMesh::from_bounds (mesh.hpp:28-31, mesh.cpp:12-44). */
 int biodiff_mesh_from_bounds(double x_min, double x_max, double y_min, double y_max, double z_min, double z_max,
                              double dx, double dy, double dz, biodiff_mesh* out);
 
-/* CartesianMesh::nearest_voxel (mesh.hpp:42-45, mesh.cpp:234-250). */
+/* CartesianMesh::nearest_voxel (mesh.hpp:42-45, mesh.cpp:72-88). */
 int biodiff_nearest_voxel(const biodiff_mesh* mesh, const double position[3], int64_t* voxel);
 
-/* precompute_thomas_coefficients (solver.hpp:35-40, solver.cpp:129-179) for
+/* precompute_thomas_coefficients (solver.hpp:35-40, solver.cpp:47-97) for
  * one axis: off_diag[S], denom_inv[n*S], c_back[n*S] with n the axis length.
  * D, lambda: per-substrate diffusion coefficient and decay rate. */
 int biodiff_precompute_thomas(const biodiff_mesh* mesh, int32_t substrates, const double* diffusion,
@@ -83,7 +83,7 @@ int biodiff_device_count(int32_t* count);
 int biodiff_session_create(const biodiff_mesh* mesh, int32_t substrates, int32_t device, biodiff_session** out);
 int biodiff_session_destroy(biodiff_session* session);
 
-/* SolverWorkspaces::build (solver.hpp:66-67, solver.cpp:359-369): builds the
+/* SolverWorkspaces::build (solver.hpp:66-67, solver.cpp:277-287): builds the
  * x/y/z workspaces on the host exactly as the reference does and uploads
  * their bits. D, lambda: per-substrate arrays of length S. */
 int biodiff_set_substrates(biodiff_session* session, const double* diffusion, const double* decay, double dt);
@@ -96,13 +96,13 @@ int biodiff_set_workspace(biodiff_session* session, int32_t axis, int32_t n, int
 /* Replaces the DirichletMap (mesh.hpp:124-141) with `count` entries:
  * voxel[count], mask[count*S] (nonzero = clamped), values[count*S]. Entries
  * may come in any order; duplicates merge as DirichletMap::add does
- * (mesh.cpp:300-321: later adds win per masked substrate). */
+ * (mesh.cpp:138-159: later adds win per masked substrate). */
 int biodiff_set_dirichlet(biodiff_session* session, int64_t count, const int64_t* voxel, const uint8_t* mask,
                           const double* values);
 
-/* Replaces the AgentPopulation (agents.hpp:389-424): validates as the
- * reference ctor does (agents.cpp:456-479) and builds the (voxel, id)
- * grouping on the host (agents.cpp:492-509). positions[3n], volume[n],
+/* Replaces the AgentPopulation (agents.hpp:30-65): validates as the
+ * reference ctor does (agents.cpp:20-43) and builds the (voxel, id)
+ * grouping on the host (agents.cpp:56-73). positions[3n], volume[n],
  * secretion/uptake/saturation[n*S]. */
 int biodiff_set_agents(biodiff_session* session, int64_t n, const int64_t* ids, const double* positions,
                        const double* volume, const double* secretion, const double* uptake,
@@ -110,12 +110,12 @@ int biodiff_set_agents(biodiff_session* session, int64_t n, const int64_t* ids, 
 
 /* Group count of the current agent grouping and a copy of it:
  * group_voxel[G], group_offsets[G+1], order[n] (agent indices in the
- * caller's order) — AgentPopulation::grouping() (agents.hpp:402-406). */
+ * caller's order) — AgentPopulation::grouping() (agents.hpp:43-47). */
 int biodiff_agent_grouping(biodiff_session* session, int64_t* groups, int64_t* group_voxel,
                            int64_t* group_offsets, int64_t* order);
 
 /* Fills every voxel with the per-substrate values initial[S] on the device —
- * the initial condition of Microenvironment::create (mesh.cpp:335-357)
+ * the initial condition of Microenvironment::create (mesh.cpp:173-195)
  * without staging a host copy of the field. */
 int biodiff_fill_field(biodiff_session* session, const double* initial);
 
@@ -123,17 +123,17 @@ int biodiff_fill_field(biodiff_session* session, const double* initial);
 int biodiff_upload_field(biodiff_session* session, const double* values, int64_t count);
 int biodiff_download_field(biodiff_session* session, double* values, int64_t count);
 
-/* diffusion_sweep (solver.hpp:51-52, solver.cpp:330-347) along one axis. */
+/* diffusion_sweep (solver.hpp:51-52, solver.cpp:248-265) along one axis. */
 int biodiff_diffusion_sweep(biodiff_session* session, int32_t axis);
 
-/* apply_dirichlet_conditions (solver.hpp:55, solver.cpp:349-357). */
+/* apply_dirichlet_conditions (solver.hpp:55, solver.cpp:267-275). */
 int biodiff_apply_dirichlet(biodiff_session* session);
 
-/* diffuse_decay_step (solver.hpp:72-73, solver.cpp:371-381): x, y, z sweeps
+/* diffuse_decay_step (solver.hpp:72-73, solver.cpp:289-299): x, y, z sweeps
  * (active axes) with the Dirichlet clamp fused into the last sweep. */
 int biodiff_diffuse_decay_step(biodiff_session* session);
 
-/* cell_sources_sinks_step (agents.hpp:431-432, agents.cpp:511-548). */
+/* cell_sources_sinks_step (agents.hpp:72-73, agents.cpp:75-112). */
 int biodiff_cell_sources_sinks_step(biodiff_session* session, double dt);
 
 /* The engine's inner loop: steps x [diffuse_decay_step;
@@ -167,7 +167,7 @@ int biodiff_event_elapsed(biodiff_session* session, int32_t begin, int32_t end, 
 /* Number of kernel launches issued by the session since creation. */
 int biodiff_launch_count(biodiff_session* session, int64_t* launches);
 
-/* Device-side cross_check (validation.hpp:288-292, validation.cpp:112-137)
+/* Device-side cross_check (validation.hpp:61-65, validation.cpp:112-137)
  * of the session field against a host field: max_abs, max_rel, worst value
  * index, pass (|a-b| <= abs_tol + rel_tol*max(|a|,|b|) everywhere). */
 int biodiff_cross_check(biodiff_session* session, const double* other, int64_t count, double abs_tol,

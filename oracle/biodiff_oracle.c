@@ -22,13 +22,13 @@
 #include <string.h>
 #include <math.h>
 
-/* solver.cpp:129-179 precompute_thomas_coefficients (one axis).
+/* solver.cpp:47-97 precompute_thomas_coefficients (one axis).
  * q[s] = dt*D/(h*h); decay = 1 + dt*lambda/dims;
- * diag(i): n==1 -> decay; ends -> decay+q; interior -> decay+2q  (solver.cpp:161-164)
- * denom_inv[0] = 1/diag(0); c_back[0] = n>1 ? q*denom_inv[0] : 0   (solver.cpp:166-169)
+ * diag(i): n==1 -> decay; ends -> decay+q; interior -> decay+2q  (solver.cpp:79-82)
+ * denom_inv[0] = 1/diag(0); c_back[0] = n>1 ? q*denom_inv[0] : 0   (solver.cpp:84-87)
  * i>=1: denom = diag(i) - q*c_back[i-1]; denom_inv[i] = 1/denom;
- *       c_back[i] = q*denom_inv[i] for i < n-1, else 0             (solver.cpp:170-176)
- * Returns 0, or 1 on invalid arguments (solver.cpp:133-138). */
+ *       c_back[i] = q*denom_inv[i] for i < n-1, else 0             (solver.cpp:88-94)
+ * Returns 0, or 1 on invalid arguments (solver.cpp:51-56). */
 int orc_precompute(int n, int S, const double* D, const double* lambda, double h, double dt, int dims,
                    double* off_diag, double* denom_inv, double* c_back)
 {
@@ -55,7 +55,7 @@ int orc_precompute(int n, int S, const double* D, const double* lambda, double h
 
 /* One strided line: element m lives at v[m*stride]. The per-element ops are
  * solver.cpp:17-19 (fwd_first, fwd, bwd); the loop shape is thomas_solve
- * solver.cpp:181-208 restated for one substrate. */
+ * solver.cpp:99-126 restated for one substrate. */
 static void line_solve(double* v, long stride, int n, int S, int s, double q, const double* dinv, const double* cb)
 {
     v[0] = v[0] * dinv[s];
@@ -65,7 +65,7 @@ static void line_solve(double* v, long stride, int n, int S, int s, double q, co
         v[(long)i * stride] = v[(long)i * stride] + cb[(size_t)i * S + s] * v[(long)(i + 1) * stride];
 }
 
-/* solver.cpp:212-326 sweep_x / sweep_y / sweep_z. Lines are disjoint so the
+/* solver.cpp:130-244 sweep_x / sweep_y / sweep_z. Lines are disjoint so the
  * per-line restatement is bitwise equal to the reference's chunked loops
  * (backend.hpp:28-33). axis: 0=x, 1=y, 2=z.
  * Layout (mesh.hpp:59-61): rho[(i + j*nx + k*nx*ny)*S + s]. */
@@ -91,7 +91,7 @@ void orc_sweep(double* rho, int nx, int ny, int nz, int S, int axis,
     }
 }
 
-/* solver.cpp:349-357 apply_dirichlet_conditions: masked overwrite per entry. */
+/* solver.cpp:267-275 apply_dirichlet_conditions: masked overwrite per entry. */
 void orc_dirichlet(double* rho, int S, int64_t count, const int64_t* voxel, const uint8_t* mask, const double* values)
 {
     for (int64_t e = 0; e < count; ++e)
@@ -99,8 +99,8 @@ void orc_dirichlet(double* rho, int S, int64_t count, const int64_t* voxel, cons
             if (mask[e * S + s]) rho[voxel[e] * S + s] = values[e * S + s];
 }
 
-/* mesh.cpp:234-250 nearest_voxel: floor((p-min)/h) clamped to [0, n-1].
- * Returns -1 when the position is outside [min, max] (mesh.cpp:228-232). */
+/* mesh.cpp:72-88 nearest_voxel: floor((p-min)/h) clamped to [0, n-1].
+ * Returns -1 when the position is outside [min, max] (mesh.cpp:66-70). */
 int64_t orc_nearest_voxel(const double* bounds /* xmin,xmax,ymin,ymax,zmin,zmax */, const double* h,
                           const int* n, const double* p)
 {
@@ -126,7 +126,7 @@ static int key_cmp(const void* a, const void* b)
     return 0;
 }
 
-/* agents.cpp:492-509 rebuild_voxel_grouping: sort agent indices by
+/* agents.cpp:56-73 rebuild_voxel_grouping: sort agent indices by
  * (voxel, id), then cut into groups of equal voxel.
  * Outputs: group_voxel[G], group_offsets[G+1], order[N] (agent indices in
  * group order). Returns G, or -1 when an agent lies outside the mesh. */
@@ -155,11 +155,11 @@ int64_t orc_group(int64_t n_agents, const int64_t* ids, const double* positions,
     return G;
 }
 
-/* agents.cpp:511-548 cell_sources_sinks_step. Agents are indexed through
+/* agents.cpp:75-112 cell_sources_sinks_step. Agents are indexed through
  * order[] (group order); per-agent arrays are in the caller's agent order.
- * inv_voxel_volume = 1/((dx*dy)*dz) (agents.cpp:518, mesh.hpp:34);
- * f = dt*volume*inv (agents.cpp:538);
- * rho = (rho + f*sec*target) / (1 + f*(sec+upt)) (agents.cpp:542-543). */
+ * inv_voxel_volume = 1/((dx*dy)*dz) (agents.cpp:82, mesh.hpp:34);
+ * f = dt*volume*inv (agents.cpp:102);
+ * rho = (rho + f*sec*target) / (1 + f*(sec+upt)) (agents.cpp:106-107). */
 void orc_sources(double* rho, int S, int64_t G, const int64_t* group_voxel, const int64_t* group_offsets,
                  const int64_t* order, const double* volume, const double* secretion, const double* uptake,
                  const double* saturation, double dt, double inv_voxel_volume)
@@ -178,7 +178,7 @@ void orc_sources(double* rho, int S, int64_t G, const int64_t* group_voxel, cons
     }
 }
 
-/* solver.cpp:371-381 diffuse_decay_step: x, y if ny>1, z if nz>1, then the
+/* solver.cpp:289-299 diffuse_decay_step: x, y if ny>1, z if nz>1, then the
  * Dirichlet clamp. ws_* point at the per-axis (q, dinv, cb) arrays. */
 void orc_diffuse_decay_step(double* rho, int nx, int ny, int nz, int S,
                             const double* qx, const double* dx_, const double* cx,

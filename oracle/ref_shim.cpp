@@ -6,12 +6,12 @@
 // (mirroring build_microenvironment config.cpp:494-527 and build_agents
 // config.cpp:529-566, since config.cpp needs the absent Boost) and drives the
 // reference's own entry points:
-//   SolverWorkspaces::build        solver.cpp:359-369
-//   diffusion_sweep                solver.cpp:330-347
-//   apply_dirichlet_conditions     solver.cpp:349-357
-//   diffuse_decay_step             solver.cpp:371-381
-//   cell_sources_sinks_step        agents.cpp:511-548
-//   AgentPopulation (grouping)     agents.cpp:448-509
+//   SolverWorkspaces::build        solver.cpp:277-287
+//   diffusion_sweep                solver.cpp:248-265
+//   apply_dirichlet_conditions     solver.cpp:267-275
+//   diffuse_decay_step             solver.cpp:289-299
+//   cell_sources_sinks_step        agents.cpp:75-112
+//   AgentPopulation (grouping)     agents.cpp:12-73
 //   run_convergence_test           validation.cpp:65-110
 //   run_dirichlet_mutant_check     validation.cpp:274-287
 // The step loop [diffuse_decay_step; cell_sources_sinks_step] is SPEC.md:297
@@ -75,7 +75,7 @@ extern "C" {
 const char* ref_last_error() { return g_err.c_str(); }
 
 // Builds a Microenvironment. When `staged` is nonzero the reference's own
-// Microenvironment::create (nested-vector staging, mesh.cpp:335-357) is used;
+// Microenvironment::create (nested-vector staging, mesh.cpp:173-195) is used;
 // otherwise the public fields are filled directly (SURVEY.md §7 hard part 8),
 // which yields the identical field without the 3x staging memory.
 int ref_create(const double* bounds, const double* spacing, int S, const double* D, const double* lambda,
@@ -134,7 +134,7 @@ int ref_get_field(void* h, double* v, int64_t count)
     });
 }
 
-// DirichletMap::add (mesh.cpp:300-321), one call per entry in caller order.
+// DirichletMap::add (mesh.cpp:138-159), one call per entry in caller order.
 int ref_add_dirichlet(void* h, int64_t count, const int64_t* voxel, const uint8_t* mask, const double* values)
 {
     return guarded([&] {
@@ -183,7 +183,7 @@ int ref_add_boundary_dirichlet(void* h, const uint8_t* mask, const double* value
     });
 }
 
-// AgentPopulation ctor (agents.cpp:448-454): validate + grouping.
+// AgentPopulation ctor (agents.cpp:12-18): validate + grouping.
 int ref_set_agents(void* h, int64_t n, const int64_t* ids, const double* pos, const double* volume,
                    const double* secretion, const double* uptake, const double* saturation)
 {

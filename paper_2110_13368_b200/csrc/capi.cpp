@@ -480,7 +480,7 @@ int biodiff_ensemble_create(const biodiff_mesh* mesh, int32_t substrates, int32_
     });
 }
 
-// Per-replica SolverWorkspaces::build (solver.cpp:359-369), uploaded as
+// Per-replica SolverWorkspaces::build (solver.cpp:277-287), uploaded as
 // replicas consecutive coefficient sets per axis.
 int biodiff_ensemble_set_substrates(biodiff_session* session, const double* diffusion, const double* decay, double dt)
 {
@@ -520,7 +520,7 @@ int biodiff_ensemble_set_substrates(biodiff_session* session, const double* diff
 
 // Agents of all replicas: replica[n] in [0, replicas); ids must be unique
 // within a replica. Each replica's population is validated and grouped as
-// AgentPopulation does (agents.cpp:448-509).
+// AgentPopulation does (agents.cpp:12-73).
 int biodiff_ensemble_set_agents(biodiff_session* session, int64_t n, const int32_t* replica, const int64_t* ids,
                                 const double* positions, const double* volume, const double* secretion,
                                 const double* uptake, const double* saturation)

@@ -366,7 +366,7 @@ void DeviceSession::set_workspaces(const SolverWorkspaces& ws)
 // Splits the map into the per-substrate boundary-shell rule (evaluated in
 // the last sweep's epilogue) and residual entries. Writes of distinct
 // (voxel, substrate) pairs commute, so the split is bitwise equivalent to
-// applying every entry after the sweeps (solver.cpp:380).
+// applying every entry after the sweeps (solver.cpp:298).
 void DeviceSession::set_dirichlet(const DirichletMap& map)
 {
     ck(cudaSetDevice(device_), "cudaSetDevice");
@@ -1023,7 +1023,7 @@ void DeviceSession::ensure_source_factors(double dt)
     std::uint64_t bits;
     std::memcpy(&bits, &dt, sizeof(bits));
     if (n_agents_ == 0 || (factors_valid_ && bits == factors_dt_bits_)) return;
-    const double inv_voxel_volume = 1.0 / mesh_.voxel_volume(); // agents.cpp:518
+    const double inv_voxel_volume = 1.0 / mesh_.voxel_volume(); // agents.cpp:82
     const long long total = n_agents_ * S_;
     const int block = 256;
     begin_kernel(kAux);
@@ -1062,7 +1062,7 @@ void DeviceSession::apply_dirichlet()
     launch_residual_dirichlet(true);
 }
 
-// solver.cpp:371-381 with the clamp fused into the last active sweep.
+// solver.cpp:289-299 with the clamp fused into the last active sweep.
 void DeviceSession::step_body(bool with_sources, double dt)
 {
     if (slab_ && nccl_comm_) { // one slab per rank: exchanges on this stream (slab.cu)

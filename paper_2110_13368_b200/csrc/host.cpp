@@ -17,7 +17,7 @@ std::string format_double(double v)
     return std::string(buf, r.ptr);
 }
 
-// mesh.cpp:174-206: counts rounded from the extent, upper bounds snapped.
+// mesh.cpp:12-44: counts rounded from the extent, upper bounds snapped.
 CartesianMesh CartesianMesh::from_bounds(double x_min, double x_max, double y_min, double y_max, double z_min,
                                          double z_max, double dx, double dy, double dz)
 {
@@ -66,7 +66,7 @@ bool CartesianMesh::contains(const std::array<double, 3>& p) const
     return p[0] >= x_min && p[0] <= x_max && p[1] >= y_min && p[1] <= y_max && p[2] >= z_min && p[2] <= z_max;
 }
 
-// mesh.cpp:234-250: containing voxel, upper boundary clamps to the last one.
+// mesh.cpp:72-88: containing voxel, upper boundary clamps to the last one.
 index_t CartesianMesh::nearest_voxel(const std::array<double, 3>& p) const
 {
     if (!contains(p))
@@ -84,7 +84,7 @@ index_t CartesianMesh::boundary_voxel_count() const
     return voxel_count() - inner;
 }
 
-// mesh.cpp:300-321: sorted unique entries; re-adding a voxel merges masks.
+// mesh.cpp:138-159: sorted unique entries; re-adding a voxel merges masks.
 void DirichletMap::add(index_t voxel, std::vector<std::uint8_t> mask, std::vector<double> values,
                        index_t voxel_count, int substrates)
 {
@@ -115,7 +115,7 @@ void DirichletMap::add_single(index_t voxel, int substrate, double value, index_
     add(voxel, std::move(mask), std::move(values), voxel_count, substrates);
 }
 
-// mesh.cpp:335-357 (without the nested-vector staging: same values).
+// mesh.cpp:173-195 (without the nested-vector staging: same values).
 Microenvironment Microenvironment::create(const CartesianMesh& mesh, std::vector<SubstrateParams> substrates)
 {
     if (substrates.empty()) throw config_error("a microenvironment needs at least one substrate");
@@ -134,7 +134,7 @@ Microenvironment Microenvironment::create(const CartesianMesh& mesh, std::vector
     return env;
 }
 
-// solver.cpp:129-179. The expressions are written in the reference's
+// solver.cpp:47-97. The expressions are written in the reference's
 // evaluation order so the host (compiled without FMA contraction, see
 // Makefile) produces identical bits.
 SolverWorkspace precompute_thomas_coefficients(const CartesianMesh& mesh, const std::vector<double>& diffusion,
@@ -180,7 +180,7 @@ SolverWorkspace precompute_thomas_coefficients(const CartesianMesh& mesh, const 
     return ws;
 }
 
-// solver.cpp:359-369: x always; y, z only when the mesh extends along them.
+// solver.cpp:277-287: x always; y, z only when the mesh extends along them.
 SolverWorkspaces SolverWorkspaces::build(const CartesianMesh& mesh, const std::vector<SubstrateParams>& substrates,
                                          double dt)
 {
@@ -198,7 +198,7 @@ SolverWorkspaces SolverWorkspaces::build(const CartesianMesh& mesh, const std::v
     return w;
 }
 
-// agents.cpp:448-454
+// agents.cpp:12-18
 AgentPopulation::AgentPopulation(std::vector<CellAgent> agents, const CartesianMesh& mesh, int substrates)
     : agents_(std::move(agents))
 {
@@ -206,7 +206,7 @@ AgentPopulation::AgentPopulation(std::vector<CellAgent> agents, const CartesianM
     rebuild_voxel_grouping(mesh);
 }
 
-// agents.cpp:456-479: same checks, same exception types, same order.
+// agents.cpp:20-43: same checks, same exception types, same order.
 void AgentPopulation::validate(const CartesianMesh& mesh, int substrates) const
 {
     std::unordered_set<std::int64_t> ids;
@@ -238,7 +238,7 @@ void AgentPopulation::set_position(std::int64_t id, const std::array<double, 3>&
     throw std::invalid_argument("no agent with id " + std::to_string(id));
 }
 
-// agents.cpp:492-509: cache voxels, stable order by (voxel, id), cut groups.
+// agents.cpp:56-73: cache voxels, stable order by (voxel, id), cut groups.
 void AgentPopulation::rebuild_voxel_grouping(const CartesianMesh& mesh)
 {
     for (auto& a : agents_) a.voxel = mesh.nearest_voxel(a.position);

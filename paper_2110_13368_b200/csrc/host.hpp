@@ -143,7 +143,7 @@ struct CellAgent {
     index_t voxel = 0;
 };
 
-// agents.hpp:389-424
+// agents.hpp:30-65
 class AgentPopulation {
 public:
     AgentPopulation() = default;
@@ -192,7 +192,7 @@ private:
     std::unique_ptr<DeviceSession> session_;
 };
 
-// solver.hpp:72-73 / agents.hpp:431-432 with the device backend. The field
+// solver.hpp:72-73 / agents.hpp:72-73 with the device backend. The field
 // argument stays device-resident; call backend.download(env.field) to read it.
 void diffuse_decay_step(Microenvironment& env, const SolverWorkspaces& workspaces, DeviceBackend& backend);
 void cell_sources_sinks_step(DensityField& field, const AgentPopulation& agents, const CartesianMesh& mesh,

@@ -6,7 +6,7 @@
 //   forward       : (v + q*prev)*dinv      (solver.cpp:18 fwd)
 //   backward      : v + cb*next            (solver.cpp:19 bwd)
 //   sources       : (r + (f*sec)*target) / (1 + f*(sec+upt)),  f = (dt*V)*inv_vox
-//                                          (agents.cpp:538-543)
+//                                          (agents.cpp:102-107)
 #pragma once
 
 #include "ptx.cuh"
@@ -109,7 +109,7 @@ __device__ __forceinline__ double fwd_seg(const Chain& c, double* p, int step, i
 // Back substitution over positions mtop down to m0; position m lives at
 // p[(m - m0) * step]. Stores the (optionally clamped) result while the
 // recurrence carries the unclamped one: the clamp is applied after all
-// sweeps (solver.cpp:380), so it must not feed back into this sweep.
+// sweeps (solver.cpp:298), so it must not feed back into this sweep.
 template <bool CONSTC, bool CLAMP>
 __device__ __forceinline__ double bwd_seg(const Chain& c, double* p, int step, int mtop, int m0, double next)
 {
@@ -834,7 +834,7 @@ static __global__ void __launch_bounds__(128) sweep_global(GlobalSweep a)
     }
 }
 
-// Masked overwrite of Dirichlet entries (solver.cpp:349-357); one thread per
+// Masked overwrite of Dirichlet entries (solver.cpp:267-275); one thread per
 // (entry, substrate). Entries are unique voxels, so order is irrelevant.
 static __global__ void dirichlet_entries(double* rho, int S, long long count, const int64_t* voxel,
                                   const unsigned char* mask, const double* values)
@@ -844,13 +844,13 @@ static __global__ void dirichlet_entries(double* rho, int S, long long count, co
     if (mask[t]) rho[voxel[t / S] * S + (t % S)] = values[t];
 }
 
-// cell_sources_sinks_step (agents.cpp:511-548): one thread per (voxel group,
+// cell_sources_sinks_step (agents.cpp:75-112): one thread per (voxel group,
 // substrate); the group's agents are applied in ascending-id order. The
 // substrates of one agent update independently, so (group, s) threads
 // reproduce the reference's agent-outer / substrate-inner loop bitwise.
 // Per-agent, per-substrate factors of the implicit update for one dt:
 // add = (f*sec)*target and den = 1 + f*(sec+upt), f = (dt*V)*inv_vox
-// (agents.cpp:538-543). They do not depend on the density, so computing them
+// (agents.cpp:102-107). They do not depend on the density, so computing them
 // once per dt and reusing them is bit-identical to the reference.
 static __global__ void sources_factors(int S, long long agents, const double* volume, const double* secretion,
                                 const double* uptake, const double* saturation, double dt, double inv_voxel_volume,

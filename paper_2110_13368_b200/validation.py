@@ -69,7 +69,7 @@ def analytic_solution_1d(x: float, t: float, diffusion: float, length: float, mo
 
 
 @dataclass
-class ConvergenceSetup:  # validation.hpp:261-270
+class ConvergenceSetup:  # validation.hpp:34-43
     length: float = 2000.0
     diffusion: float = 1000.0
     total_time: float = 10.0
@@ -81,7 +81,7 @@ class ConvergenceSetup:  # validation.hpp:261-270
 
 
 @dataclass
-class ConvergenceReport:  # validation.hpp:251-257
+class ConvergenceReport:  # validation.hpp:24-30
     kind: str
     steps: List[float] = field(default_factory=list)
     errors: List[float] = field(default_factory=list)

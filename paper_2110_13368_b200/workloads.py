@@ -118,11 +118,11 @@ class Workload:
             present[pos] = True
             for e, v in enumerate(iv):
                 p = np.searchsorted(allk, v)
-                if not present[p]:  # new entry: stored as given (mesh.cpp:320)
+                if not present[p]:  # new entry: stored as given (mesh.cpp:158)
                     M[p] = im[e]
                     X[p] = ival[e]
                     present[p] = True
-                else:  # merge: later adds win per masked substrate (mesh.cpp:311-318)
+                else:  # merge: later adds win per masked substrate (mesh.cpp:149-156)
                     sel = im[e].astype(bool)
                     M[p, sel] = 1
                     X[p, sel] = ival[e, sel]

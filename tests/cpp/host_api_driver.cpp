@@ -77,7 +77,7 @@ int main(int argc, char** argv)
         const int steps = 25;
         for (int s = 0; s < steps; ++s) {
             diffuse_decay_step(env, ws, gpu);                             // solver.hpp:72
-            cell_sources_sinks_step(env.field, agents, env.mesh, dt, gpu); // agents.hpp:431
+            cell_sources_sinks_step(env.field, agents, env.mesh, dt, gpu); // agents.hpp:72
         }
         gpu.download(env.field);
         put(env.field.values.data(), sizeof(double) * env.field.values.size());

@@ -57,7 +57,7 @@ SWEEP_SHAPES = [
                                   "smem_plain"])
 @pytest.mark.parametrize("shape,S", SWEEP_SHAPES)
 def test_single_sweep_bitwise(shape, S, path, monkeypatch):
-    """diffusion_sweep (solver.cpp:330-347) along every active axis, every kernel path."""
+    """diffusion_sweep (solver.cpp:248-265) along every active axis, every kernel path."""
     _paths(monkeypatch, path)
     w = W.make("t", shape, S, 0, 1, seed=2)
     rng = np.random.default_rng(hash((shape, S)) & 0xffff)
@@ -237,10 +237,10 @@ def test_errors_map_to_reference_categories():
         s.advance(3, w.dt * 2)  # dt must match the workspace (solver.hpp:57-68)
     one = np.ones(11)
     p = one.ctypes.data_as(B._P(B._d))
-    with pytest.raises(B.StateError):  # workspace line length != mesh axis (solver.cpp:333-335)
+    with pytest.raises(B.StateError):  # workspace line length != mesh axis (solver.cpp:251-253)
         B._check(B.lib().biodiff_set_workspace(s._h, 0, 11, 3, 0.01, p, p, p))
     with pytest.raises(B.StateError):
-        s.cell_sources_sinks_step(0.0)  # agents.cpp:514
+        s.cell_sources_sinks_step(0.0)  # agents.cpp:78
     with pytest.raises(B.StateError):
         s.set_agents([1, 1], np.zeros((2, 3)), [1, 1], np.zeros(2), np.zeros(2), np.zeros(2))  # duplicate id
     with pytest.raises(B.StateError):
