@@ -101,18 +101,63 @@ int biodiff_set_dirichlet(biodiff_session* session, int64_t count, const int64_t
                           const double* values);
 
 /* Replaces the AgentPopulation (agents.hpp:30-65): validates as the
- * reference ctor does (agents.cpp:20-43) and builds the (voxel, id)
- * grouping on the host (agents.cpp:56-73). positions[3n], volume[n],
- * secretion/uptake/saturation[n*S]. */
+ * reference ctor does (agents.cpp:20-43) on the host, then builds the
+ * (voxel, id) grouping ON THE DEVICE (agents.cpp:56-73 as a radix-sort
+ * pipeline, csrc/agents.cu). positions[3n], volume[n],
+ * secretion/uptake/saturation[n*S]. The device keeps the agents in this
+ * input order ("agent index" below). */
 int biodiff_set_agents(biodiff_session* session, int64_t n, const int64_t* ids, const double* positions,
                        const double* volume, const double* secretion, const double* uptake,
                        const double* saturation);
 
 /* Group count of the current agent grouping and a copy of it:
  * group_voxel[G], group_offsets[G+1], order[n] (agent indices in the
- * caller's order) — AgentPopulation::grouping() (agents.hpp:43-47). */
+ * caller's order) — AgentPopulation::grouping() (agents.hpp:43-47). With
+ * only `groups` non-null, returns the count alone. */
 int biodiff_agent_grouping(biodiff_session* session, int64_t* groups, int64_t* group_voxel,
                            int64_t* group_offsets, int64_t* order);
+
+/* Moving agents (agents.hpp:49-56). Positions change on the device; the
+ * grouping is stale until biodiff_rebuild_voxel_grouping (the reference's
+ * contract: "the caller is expected to rebuild the voxel grouping before
+ * the next reaction step").
+ *   set_agent_positions : all n positions, xyz[3n] host, agent-index order
+ *   set_agent_position  : AgentPopulation::set_position(id, p) (agents.cpp:45-54);
+ *                         status 2 "no agent with id" if absent
+ *   agent_positions_device: the device xyz[3n] buffer (stream-ordered with
+ *                         the session stream) for movers running on the GPU
+ *   rebuild_voxel_grouping: agents.cpp:56-73 on the device; status 2 with
+ *                         mesh.cpp:74-76's message if a position left the
+ *                         domain (the grouping is then empty). */
+int biodiff_agent_count(biodiff_session* session, int64_t* n);
+int biodiff_set_agent_positions(biodiff_session* session, const double* xyz, int64_t n);
+int biodiff_set_agent_position(biodiff_session* session, int64_t id, const double* xyz);
+int biodiff_agent_positions_device(biodiff_session* session, double** xyz);
+int biodiff_rebuild_voxel_grouping(biodiff_session* session);
+
+/* The device's agents in agent-index order (null outputs are skipped):
+ * ids[n], xyz[3n], volume[n], secretion/uptake/saturation[n*S]. */
+int biodiff_download_agents(biodiff_session* session, int64_t* ids, double* xyz, double* volume,
+                            double* secretion, double* uptake, double* saturation);
+
+/* Agent CSV files (config.cpp:416-491): load_agents + set_agents, and
+ * save_agents of the device's current agents. Header
+ * "id,x,y,z,volume" then ",S_<name>,U_<name>,target_<name>" per substrate;
+ * names[S] are the substrate names. Errors: status 1 (config_error
+ * "agent file <path> line <n>: ...") or 4 (io_error). */
+int biodiff_load_agents_csv(biodiff_session* session, const char* path, const char* const* names);
+
+/* Host-only agent file I/O (no device needed): parse + validate an agent
+ * file on `mesh` (call with null arrays to get *n, then with arrays of that
+ * size), and write agents in the reference's format (format_double = the
+ * shortest round-trip std::to_chars, text.cpp:9-14). */
+int biodiff_parse_agents_csv(const biodiff_mesh* mesh, const char* path, const char* const* names, int32_t substrates,
+                             int64_t* n, int64_t* ids, double* xyz, double* volume, double* secretion, double* uptake,
+                             double* saturation);
+int biodiff_write_agents_csv(const char* path, const char* const* names, int32_t substrates, int64_t n,
+                             const int64_t* ids, const double* xyz, const double* volume, const double* secretion,
+                             const double* uptake, const double* saturation);
+int biodiff_save_agents_csv(biodiff_session* session, const char* path, const char* const* names);
 
 /* Fills every voxel with the per-substrate values initial[S] on the device —
  * the initial condition of Microenvironment::create (mesh.cpp:173-195)

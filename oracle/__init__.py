@@ -121,6 +121,11 @@ def ref_lib():
         L.ref_convergence.argtypes = [ctypes.c_int, ctypes.c_int, _P(_d), _P(_d), _P(_d), _P(ctypes.c_int)]
         L.ref_mutant_check.argtypes = [_P(ctypes.c_int)]
         L.ref_format_double.argtypes = [_d, ctypes.c_char_p, ctypes.c_int]
+        L.ref_format_int.argtypes = [_i64, ctypes.c_char_p, ctypes.c_int]
+        L.ref_load_agents.argtypes = [_vp, ctypes.c_char_p, _P(ctypes.c_char_p), ctypes.c_int]
+        L.ref_agent_count.argtypes = [_vp]
+        L.ref_agent_count.restype = _i64
+        L.ref_get_agents.argtypes = [_vp, _P(_i64), _P(_d), _P(_d), _P(_d), _P(_d), _P(_d)]
         L.ref_snapshot.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_char_p, _i64]
         L.ref_snapshot.restype = _i64
         _ref = L
@@ -262,6 +267,18 @@ class Reference:
                                    _dp(_f(w.agent_vol)), _dp(_f(w.agent_sec)), _dp(_f(w.agent_upt)),
                                    _dp(_f(w.agent_sat))))
         _rchk(L.ref_build_workspaces(self.h, w.dt))
+
+    def load_agents(self, path, names):
+        """load_agents (config.cpp:416-477) over the reference's text.cpp + AgentPopulation."""
+        L = ref_lib()
+        nm = (ctypes.c_char_p * max(1, len(names)))(*[str(x).encode() for x in names])
+        _rchk(L.ref_load_agents(self.h, str(path).encode(), nm, len(names)))
+        n, S = int(L.ref_agent_count(self.h)), len(names)
+        ids = np.zeros(n, np.int64)
+        pos, vol = np.zeros((n, 3)), np.zeros(n)
+        sec, upt, sat = np.zeros((n, S)), np.zeros((n, S)), np.zeros((n, S))
+        _rchk(L.ref_get_agents(self.h, _ip(ids), _dp(pos), _dp(vol), _dp(sec), _dp(upt), _dp(sat)))
+        return ids, pos, vol, sec, upt, sat
 
     def close(self):
         if getattr(self, "h", None):

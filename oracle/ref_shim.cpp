@@ -26,6 +26,7 @@
 #include "core/text.hpp"
 #include "core/validation.hpp"
 
+#include <fstream>
 #include <sstream>
 
 #include <chrono>
@@ -73,6 +74,93 @@ struct RefCtx {
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
+
+// load_agents (config.cpp:416-477) restated over the reference's own pieces
+// (text.cpp trim / split_csv_line / parse_int / parse_double / format_int and
+// the AgentPopulation ctor, agents.cpp:12-43): config.cpp itself needs the
+// absent Boost. Stores the population in the context.
+int ref_load_agents(void* h, const char* path, const char* const* names, int S)
+{
+    return guarded([&] {
+        auto* c = static_cast<RefCtx*>(h);
+        auto fail = [](const std::string& m) -> void { throw config_error(m); };
+        auto agent_fail = [&](std::size_t line, const std::string& msg) {
+            fail(std::string("agent file ") + path + " line " + format_int(static_cast<std::int64_t>(line)) + ": " +
+                 msg);
+        };
+        std::ifstream in(path, std::ios::binary);
+        if (!in) fail(std::string("agent file not found: ") + path);
+        std::string expected = "id,x,y,z,volume";
+        for (int s = 0; s < S; ++s)
+            expected += std::string(",S_") + names[s] + ",U_" + names[s] + ",target_" + names[s];
+        std::string line;
+        std::size_t line_no = 0;
+        if (!std::getline(in, line)) fail(std::string("agent file ") + path + " is empty");
+        ++line_no;
+        if (trim(line) != expected) agent_fail(line_no, "header must be '" + expected + "'");
+        std::vector<CellAgent> agents;
+        while (std::getline(in, line)) {
+            ++line_no;
+            const std::string stripped = trim(line);
+            if (stripped.empty()) continue;
+            const auto fields = split_csv_line(stripped);
+            if (fields.size() != 5 + 3 * static_cast<std::size_t>(S))
+                agent_fail(line_no, "expected " + format_int(5 + 3 * S) + " fields, got " +
+                                        format_int(static_cast<std::int64_t>(fields.size())));
+            try {
+                CellAgent a;
+                a.id = parse_int(fields[0], "id");
+                a.position = {parse_double(fields[1], "x"), parse_double(fields[2], "y"), parse_double(fields[3], "z")};
+                a.volume = parse_double(fields[4], "volume");
+                a.secretion_rates.resize(S);
+                a.uptake_rates.resize(S);
+                a.saturation_densities.resize(S);
+                for (int s = 0; s < S; ++s) {
+                    a.secretion_rates[s] = parse_double(fields[5 + 3 * s], "secretion rate");
+                    a.uptake_rates[s] = parse_double(fields[6 + 3 * s], "uptake rate");
+                    a.saturation_densities[s] = parse_double(fields[7 + 3 * s], "target density");
+                }
+                agents.push_back(std::move(a));
+            } catch (const std::invalid_argument& e) {
+                agent_fail(line_no, e.what());
+            }
+        }
+        try {
+            c->agents = AgentPopulation(std::move(agents), c->env.mesh, S);
+        } catch (const std::exception& e) {
+            fail(std::string("agent file ") + path + ": " + e.what());
+        }
+    });
+}
+
+int64_t ref_agent_count(void* h) { return static_cast<int64_t>(static_cast<RefCtx*>(h)->agents.size()); }
+
+int ref_get_agents(void* h, int64_t* ids, double* pos, double* vol, double* sec, double* upt, double* sat)
+{
+    return guarded([&] {
+        const auto& all = static_cast<RefCtx*>(h)->agents.agents();
+        for (std::size_t a = 0; a < all.size(); ++a) {
+            const std::size_t S = all[a].secretion_rates.size();
+            ids[a] = all[a].id;
+            for (int k = 0; k < 3; ++k) pos[3 * a + k] = all[a].position[k];
+            vol[a] = all[a].volume;
+            for (std::size_t s = 0; s < S; ++s) {
+                sec[a * S + s] = all[a].secretion_rates[s];
+                upt[a * S + s] = all[a].uptake_rates[s];
+                sat[a * S + s] = all[a].saturation_densities[s];
+            }
+        }
+    });
+}
+
+// format_int (text.cpp:16-21).
+int ref_format_int(int64_t v, char* out, int cap)
+{
+    const std::string s = format_int(v);
+    if (static_cast<int>(s.size()) + 1 > cap) return 1;
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return 0;
+}
 
 // Builds a Microenvironment. When `staged` is nonzero the reference's own
 // Microenvironment::create (nested-vector staging, mesh.cpp:173-195) is used;

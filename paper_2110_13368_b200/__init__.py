@@ -8,10 +8,10 @@ is no CPU fallback.
 
 The names mirror the reference's C++ API (/root/reference/proj/src/core):
 ``diffuse_decay_step`` (solver.hpp:72), ``cell_sources_sinks_step``
-(agents.hpp:431), ``diffusion_sweep`` (solver.hpp:51),
+(agents.hpp:72), ``diffusion_sweep`` (solver.hpp:51),
 ``apply_dirichlet_conditions`` (solver.hpp:55),
 ``precompute_thomas_coefficients`` (solver.hpp:38), ``cross_check``
-(validation.hpp:291), with errors raised as the reference's exception
+(validation.hpp:64), with errors raised as the reference's exception
 categories (errors.hpp:9-24).
 """
 from __future__ import annotations
@@ -105,6 +105,18 @@ _SIGNATURES = {
     "biodiff_set_dirichlet": (ctypes.c_int, [_vp, _i64, _P(_i64), _P(ctypes.c_uint8), _P(_d)]),
     "biodiff_set_agents": (ctypes.c_int, [_vp, _i64, _P(_i64), _P(_d), _P(_d), _P(_d), _P(_d), _P(_d)]),
     "biodiff_agent_grouping": (ctypes.c_int, [_vp, _P(_i64), _P(_i64), _P(_i64), _P(_i64)]),
+    "biodiff_agent_count": (ctypes.c_int, [_vp, _P(_i64)]),
+    "biodiff_set_agent_positions": (ctypes.c_int, [_vp, _P(_d), _i64]),
+    "biodiff_set_agent_position": (ctypes.c_int, [_vp, _i64, _P(_d)]),
+    "biodiff_agent_positions_device": (ctypes.c_int, [_vp, _P(_vp)]),
+    "biodiff_rebuild_voxel_grouping": (ctypes.c_int, [_vp]),
+    "biodiff_download_agents": (ctypes.c_int, [_vp, _P(_i64), _P(_d), _P(_d), _P(_d), _P(_d), _P(_d)]),
+    "biodiff_load_agents_csv": (ctypes.c_int, [_vp, ctypes.c_char_p, _P(ctypes.c_char_p)]),
+    "biodiff_save_agents_csv": (ctypes.c_int, [_vp, ctypes.c_char_p, _P(ctypes.c_char_p)]),
+    "biodiff_parse_agents_csv": (ctypes.c_int, [_P(Mesh), ctypes.c_char_p, _P(ctypes.c_char_p), _i32, _P(_i64),
+                                                _P(_i64), _P(_d), _P(_d), _P(_d), _P(_d), _P(_d)]),
+    "biodiff_write_agents_csv": (ctypes.c_int, [ctypes.c_char_p, _P(ctypes.c_char_p), _i32, _i64, _P(_i64), _P(_d),
+                                                _P(_d), _P(_d), _P(_d), _P(_d)]),
     "biodiff_upload_field": (ctypes.c_int, [_vp, _P(_d), _i64]),
     "biodiff_fill_field": (ctypes.c_int, [_vp, _P(_d)]),
     "biodiff_download_field": (ctypes.c_int, [_vp, _P(_d), _i64]),
@@ -175,22 +187,52 @@ def _f64(a, n=None) -> np.ndarray:
 
 
 def mesh_from_bounds(x_min, x_max, y_min, y_max, z_min, z_max, dx, dy, dz) -> Mesh:
-    """CartesianMesh::from_bounds (mesh.cpp:174-206)."""
+    """CartesianMesh::from_bounds (mesh.cpp:12-44)."""
     m = Mesh()
     _check(lib().biodiff_mesh_from_bounds(x_min, x_max, y_min, y_max, z_min, z_max, dx, dy, dz, ctypes.byref(m)))
     return m
 
 
 def nearest_voxel(mesh: Mesh, position) -> int:
-    """CartesianMesh::nearest_voxel (mesh.cpp:234-250)."""
+    """CartesianMesh::nearest_voxel (mesh.cpp:72-88)."""
     p = _f64(position, 3)
     out = _i64()
     _check(lib().biodiff_nearest_voxel(ctypes.byref(mesh), _dptr(p), ctypes.byref(out)))
     return int(out.value)
 
 
+def parse_agents_csv(mesh: Mesh, path: str, names):
+    """load_agents (config.cpp:416-477) on the host: parse + validate an agent file.
+    Returns (ids, xyz[n,3], volume, secretion[n,S], uptake[n,S], saturation[n,S])."""
+    S = len(names)
+    nm = (ctypes.c_char_p * max(1, S))(*[str(x).encode() for x in names])
+    n = _i64()
+    p = str(path).encode()
+    _check(lib().biodiff_parse_agents_csv(ctypes.byref(mesh), p, nm, S, ctypes.byref(n), None, None, None, None,
+                                          None, None))
+    N = int(n.value)
+    ids = np.zeros(N, np.int64)
+    xyz, vol = np.zeros((N, 3)), np.zeros(N)
+    sec, upt, sat = np.zeros((N, S)), np.zeros((N, S)), np.zeros((N, S))
+    _check(lib().biodiff_parse_agents_csv(ctypes.byref(mesh), p, nm, S, ctypes.byref(n), ids.ctypes.data_as(_P(_i64)),
+                                          _dptr(xyz), _dptr(vol), _dptr(sec), _dptr(upt), _dptr(sat)))
+    return ids, xyz, vol, sec, upt, sat
+
+
+def write_agents_csv(path: str, names, ids, xyz, volume, secretion, uptake, saturation):
+    """save_agents (config.cpp:479-491): the reference's agent file format."""
+    S = len(names)
+    nm = (ctypes.c_char_p * max(1, S))(*[str(x).encode() for x in names])
+    ids = np.ascontiguousarray(np.asarray(ids, dtype=np.int64).ravel())
+    n = ids.size
+    _check(lib().biodiff_write_agents_csv(str(path).encode(), nm, S, n, ids.ctypes.data_as(_P(_i64)),
+                                          _dptr(_f64(xyz, 3 * n)), _dptr(_f64(volume, n)),
+                                          _dptr(_f64(secretion, n * S)), _dptr(_f64(uptake, n * S)),
+                                          _dptr(_f64(saturation, n * S))))
+
+
 def precompute_thomas_coefficients(mesh: Mesh, diffusion, decay, dt: float, axis: int, dims: int):
-    """precompute_thomas_coefficients (solver.cpp:129-179) -> (off_diag[S], denom_inv[n,S], c_back[n,S])."""
+    """precompute_thomas_coefficients (solver.cpp:47-97) -> (off_diag[S], denom_inv[n,S], c_back[n,S])."""
     D = _f64(diffusion)
     L = _f64(decay, D.size)
     S = D.size
@@ -211,7 +253,7 @@ def device_count() -> int:
 
 @dataclass
 class CrossCheckReport:
-    """validation.hpp:279-286."""
+    """validation.hpp:52-59."""
     max_abs: float
     max_rel: float
     worst_value_index: int
@@ -307,7 +349,7 @@ class Session:
 
     # -- set-up ---------------------------------------------------------
     def set_substrates(self, diffusion, decay, dt: float):
-        """SolverWorkspaces::build (solver.cpp:359-369) + upload."""
+        """SolverWorkspaces::build (solver.cpp:277-287) + upload."""
         _check(lib().biodiff_set_substrates(self._h, _dptr(_f64(diffusion, self.S)), _dptr(_f64(decay, self.S)), dt))
 
     def set_workspace(self, axis: int, dims: int, dt: float, off_diag, denom_inv, c_back):
@@ -324,10 +366,9 @@ class Session:
                                            m.ctypes.data_as(_P(ctypes.c_uint8)), _dptr(x)))
 
     def set_agents(self, ids, positions, volume, secretion, uptake, saturation):
-        """AgentPopulation (agents.cpp:448-509): validate + (voxel, id) grouping."""
+        """AgentPopulation (agents.cpp:12-73): host validation, device (voxel, id) grouping (csrc/agents.cu)."""
         ids = np.ascontiguousarray(np.asarray(ids, dtype=np.int64).ravel())
         n = ids.size
-        self._n_agents = n
         _check(lib().biodiff_set_agents(
             self._h, n, ids.ctypes.data_as(_P(_i64)), _dptr(_f64(positions, 3 * n)), _dptr(_f64(volume, n)),
             _dptr(_f64(secretion, n * self.S)), _dptr(_f64(uptake, n * self.S)), _dptr(_f64(saturation, n * self.S))))
@@ -345,7 +386,58 @@ class Session:
         return gv, go, order[: go[-1]]
 
     def _agent_capacity(self, G):
-        return getattr(self, "_n_agents", 0)
+        return self.agent_count()
+
+    # -- moving agents / agent files ------------------
+    def agent_count(self) -> int:
+        n = _i64()
+        _check(lib().biodiff_agent_count(self._h, ctypes.byref(n)))
+        return int(n.value)
+
+    def set_agent_positions(self, xyz):
+        """Every agent's position (agent-index order); the grouping is stale until rebuilt."""
+        n = self.agent_count()
+        _check(lib().biodiff_set_agent_positions(self._h, _dptr(_f64(xyz, 3 * n)), n))
+
+    def set_agent_position(self, agent_id: int, xyz):
+        """AgentPopulation::set_position (agents.cpp:45-54)."""
+        _check(lib().biodiff_set_agent_position(self._h, int(agent_id), _dptr(_f64(xyz, 3))))
+
+    def agent_positions_device(self) -> int:
+        """Device address of the xyz[3n] position buffer (for GPU-side movers)."""
+        p = _vp()
+        _check(lib().biodiff_agent_positions_device(self._h, ctypes.byref(p)))
+        return int(p.value or 0)
+
+    def rebuild_voxel_grouping(self):
+        """AgentPopulation::rebuild_voxel_grouping (agents.cpp:56-73), on the device."""
+        _check(lib().biodiff_rebuild_voxel_grouping(self._h))
+
+    def download_agents(self):
+        """(ids, xyz[n,3], volume, secretion[n,S], uptake[n,S], saturation[n,S]) in agent-index order."""
+        n, S = self.agent_count(), self.S
+        ids = np.zeros(n, np.int64)
+        xyz, vol = np.zeros((n, 3)), np.zeros(n)
+        sec, upt, sat = np.zeros((n, S)), np.zeros((n, S)), np.zeros((n, S))
+        _check(lib().biodiff_download_agents(self._h, ids.ctypes.data_as(_P(_i64)), _dptr(xyz), _dptr(vol),
+                                             _dptr(sec), _dptr(upt), _dptr(sat)))
+        return ids, xyz, vol, sec, upt, sat
+
+    @staticmethod
+    def _names(names):
+        return (ctypes.c_char_p * len(names))(*[str(x).encode() for x in names])
+
+    def load_agents_csv(self, path: str, names):
+        """load_agents (config.cpp:416-477) + set_agents."""
+        if len(names) != self.S:
+            raise ValueError("one name per substrate")
+        _check(lib().biodiff_load_agents_csv(self._h, str(path).encode(), self._names(names)))
+
+    def save_agents_csv(self, path: str, names):
+        """save_agents (config.cpp:479-491) of the device's current agents."""
+        if len(names) != self.S:
+            raise ValueError("one name per substrate")
+        _check(lib().biodiff_save_agents_csv(self._h, str(path).encode(), self._names(names)))
 
     # -- field ----------------------------------------------------------
     def upload_field(self, values):

@@ -1,0 +1,375 @@
+// On-device agent grouping: the reference's
+// AgentPopulation::rebuild_voxel_grouping (agents.cpp:56-73) — cache each
+// agent's voxel with CartesianMesh::nearest_voxel (mesh.cpp:72-88), order the
+// agents by (voxel, id), cut one group per voxel — as a device pipeline, so
+// agents that move between steps (set_position, agents.cpp:45-54) are
+// regrouped without a host round trip:
+//
+//   agent_keys     one thread per agent, in ascending-id rank order: domain
+//                  check (mesh.cpp:66-70) + voxel key (replica offset for
+//                  ensembles, slab-local / sentinel for z-slabs)
+//   radix sort     stable by key over the id-ranked sequence => (key, id)
+//                  order, exactly the reference's comparator
+//   group_flags    group starts; exclusive scan -> group index
+//   group_write    CSR: group voxel, offsets, group and agent counts
+//   agent_gather   per-agent parameters into group order
+//
+// The source kernel reads the group count from device memory and is
+// launched over the agent capacity, so CUDA graphs captured before a rebuild
+// stay valid after it. Every set_agents goes through this pipeline.
+#include "device.hpp"
+#include "kernels.cuh"
+
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstring>
+#include <numeric>
+
+namespace biodiff_b200 {
+
+namespace {
+
+void ck(cudaError_t e, const char* what)
+{
+    if (e != cudaSuccess) throw state_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+void dfree(T*& p)
+{
+    if (p) cudaFree(p);
+    p = nullptr;
+}
+
+template <class T>
+void dalloc(T*& p, std::size_t count)
+{
+    dfree(p);
+    if (count) ck(cudaMalloc(&p, sizeof(T) * count), "cudaMalloc agents");
+}
+
+struct AgentMesh {
+    double lo[3], hi[3], h[3];
+    int n[3];
+    long long nvox;     // voxels of one replica of the (global) mesh
+    long long vox_lo;   // slab filter: keep voxels in [vox_lo, vox_hi), key = voxel - vox_lo
+    long long vox_hi;
+    long long key_span; // keys per replica (vox_hi - vox_lo)
+    long long sentinel; // key of a filtered-out agent (sorts last)
+};
+
+// mesh.cpp:78-86: floor((v - lo) / h) clamped to [0, n - 1].
+__device__ __forceinline__ int cell_of(double v, double lo, double h, int n)
+{
+    const int i = static_cast<int>(floor(__ddiv_rn(__dsub_rn(v, lo), h)));
+    return min(max(i, 0), n - 1);
+}
+
+__global__ void agent_keys(const double* pos, const int* rep, long long N, AgentMesh m, const int64_t* id_order,
+                           int64_t* keys, unsigned long long* bad)
+{
+    const long long r = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (r >= N) return;
+    const long long a = id_order[r];
+    const double p0 = pos[3 * a], p1 = pos[3 * a + 1], p2 = pos[3 * a + 2];
+    // mesh.cpp:66-70 (NaN fails every comparison, as on the host).
+    const bool inside = p0 >= m.lo[0] && p0 <= m.hi[0] && p1 >= m.lo[1] && p1 <= m.hi[1] && p2 >= m.lo[2] &&
+                        p2 <= m.hi[2];
+    if (!inside) {
+        atomicMin(bad, static_cast<unsigned long long>(a));
+        keys[r] = m.sentinel;
+        return;
+    }
+    const int i = cell_of(p0, m.lo[0], m.h[0], m.n[0]);
+    const int j = cell_of(p1, m.lo[1], m.h[1], m.n[1]);
+    const int k = cell_of(p2, m.lo[2], m.h[2], m.n[2]);
+    const long long v = static_cast<long long>(i) + static_cast<long long>(m.n[0]) * (j + static_cast<long long>(m.n[1]) * k);
+    if (v < m.vox_lo || v >= m.vox_hi) {
+        keys[r] = m.sentinel;
+        return;
+    }
+    keys[r] = (v - m.vox_lo) + static_cast<long long>(rep ? rep[a] : 0) * m.key_span;
+}
+
+__global__ void group_flags(const int64_t* keys, long long N, long long sentinel, int* flags)
+{
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    flags[i] = keys[i] != sentinel && (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
+}
+
+// counts[0] = groups, counts[1] = grouped agents (keys before the first sentinel).
+__global__ void group_write(const int64_t* keys, const int* flags, const int64_t* gidx, long long N,
+                            long long sentinel, int64_t* group_voxel, int64_t* group_offsets, int64_t* counts)
+{
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    if (flags[i]) {
+        group_voxel[gidx[i]] = keys[i];
+        group_offsets[gidx[i]] = i;
+    }
+    const bool valid = keys[i] != sentinel;
+    const bool last_valid = valid && (i == N - 1 || keys[i + 1] == sentinel);
+    if (last_valid) {
+        const long long G = gidx[i] + flags[i];
+        counts[0] = G;
+        counts[1] = i + 1;
+        group_offsets[G] = i + 1;
+    }
+}
+
+__global__ void agent_gather(const int64_t* order, long long N, int S, const double* vol, const double* sec,
+                             const double* upt, const double* sat, double* vol_g, double* sec_g, double* upt_g,
+                             double* sat_g)
+{
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= N * S) return;
+    const long long i = t / S;
+    const int s = static_cast<int>(t % S);
+    const long long a = order[i];
+    if (s == 0) vol_g[i] = vol[a];
+    sec_g[t] = sec[a * S + s];
+    upt_g[t] = upt[a * S + s];
+    sat_g[t] = sat[a * S + s];
+}
+
+int bits_for(long long v)
+{
+    int b = 1;
+    while (b < 63 && (1LL << b) <= v) ++b;
+    return b;
+}
+
+unsigned blocks(long long n, int block) { return static_cast<unsigned>(std::max(1LL, (n + block - 1) / block)); }
+
+} // namespace
+
+void DeviceSession::release_agents()
+{
+    for (auto** p : {&in_ids_, &id_order_, &keys_a_, &keys_b_, &vals_b_, &scan_, &group_voxel_, &group_offsets_,
+                     &agent_counts_})
+        dfree(*p);
+    for (auto** p : {&in_pos_, &in_vol_, &in_sec_, &in_upt_, &in_sat_, &agent_volume_, &agent_secretion_,
+                     &agent_uptake_, &agent_saturation_, &agent_add_, &agent_den_})
+        dfree(*p);
+    dfree(in_rep_);
+    dfree(flags_);
+    dfree(agent_bad_);
+    if (cub_tmp_) cudaFree(cub_tmp_);
+    cub_tmp_ = nullptr;
+    cub_bytes_ = 0;
+    n_agents_ = 0;
+    groups_ = 0;
+    grouped_agents_ = 0;
+    id_index_.clear();
+}
+
+// Ensembles: population r lives in replica r (keys offset by r * voxels).
+// Input order = the populations' agents concatenated (replica-major).
+void DeviceSession::set_agents_multi(const std::vector<const AgentPopulation*>& pops)
+{
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    auto st = static_cast<cudaStream_t>(stream_);
+    ck(cudaStreamSynchronize(st), "sync");
+    if (static_cast<int>(pops.size()) > replicas_) throw state_error("more agent populations than replicas");
+    const int S = S_;
+    std::vector<std::int64_t> ids;
+    std::vector<double> pos, vol, sec, upt, sat;
+    std::vector<int> rep;
+    for (std::size_t r = 0; r < pops.size(); ++r)
+        for (const CellAgent& a : pops[r]->agents()) {
+            if (a.secretion_rates.size() != static_cast<std::size_t>(S) ||
+                a.uptake_rates.size() != static_cast<std::size_t>(S) ||
+                a.saturation_densities.size() != static_cast<std::size_t>(S))
+                throw state_error("agent rate vectors do not match the substrate count");
+            ids.push_back(a.id);
+            pos.insert(pos.end(), a.position.begin(), a.position.end());
+            vol.push_back(a.volume);
+            sec.insert(sec.end(), a.secretion_rates.begin(), a.secretion_rates.end());
+            upt.insert(upt.end(), a.uptake_rates.begin(), a.uptake_rates.end());
+            sat.insert(sat.end(), a.saturation_densities.begin(), a.saturation_densities.end());
+            rep.push_back(static_cast<int>(r));
+        }
+    const std::int64_t N = static_cast<std::int64_t>(ids.size());
+    // Ascending-id rank order (the tie-break of the (voxel, id) sort).
+    std::vector<std::int64_t> order(N);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](std::int64_t l, std::int64_t r) { return ids[l] < ids[r]; });
+
+    invalidate_graphs(); // buffers are reallocated below
+    release_agents();
+    factors_valid_ = false;
+    n_agents_ = N;
+    if (replicas_ == 1)
+        for (std::int64_t a = 0; a < N; ++a) id_index_[ids[a]] = a;
+    if (N == 0) return;
+    auto up = [&](auto*& d, const auto& h) {
+        dalloc(d, h.size());
+        ck(cudaMemcpyAsync(d, h.data(), sizeof(h[0]) * h.size(), cudaMemcpyHostToDevice, st), "upload agents");
+    };
+    up(in_ids_, ids);
+    up(in_pos_, pos);
+    up(in_vol_, vol);
+    up(in_sec_, sec);
+    up(in_upt_, upt);
+    up(in_sat_, sat);
+    if (replicas_ > 1) up(in_rep_, rep);
+    up(id_order_, order);
+    dalloc(keys_a_, N);
+    dalloc(keys_b_, N);
+    dalloc(vals_b_, N);
+    dalloc(flags_, N);
+    dalloc(scan_, N);
+    dalloc(group_voxel_, N);
+    dalloc(group_offsets_, N + 1);
+    dalloc(agent_counts_, 2);
+    dalloc(agent_bad_, 1);
+    dalloc(agent_volume_, N);
+    dalloc(agent_secretion_, N * S);
+    dalloc(agent_uptake_, N * S);
+    dalloc(agent_saturation_, N * S);
+    dalloc(agent_add_, N * S);
+    dalloc(agent_den_, N * S);
+    // CUB scratch for the sort and the scan (sized once per population).
+    std::size_t sort_bytes = 0, scan_bytes = 0;
+    ck(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, keys_a_, keys_b_, id_order_, vals_b_, N, 0, 63, st),
+       "cub sort size");
+    ck(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, flags_, scan_, N, st), "cub scan size");
+    cub_bytes_ = std::max(sort_bytes, scan_bytes);
+    ck(cudaMalloc(&cub_tmp_, cub_bytes_), "cudaMalloc cub");
+    rebuild_voxel_grouping();
+}
+
+void DeviceSession::rebuild_voxel_grouping()
+{
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    const std::int64_t N = n_agents_;
+    if (N == 0) return;
+    auto st = static_cast<cudaStream_t>(stream_);
+    const CartesianMesh& gm = agent_mesh_set_ ? agent_mesh_ : mesh_;
+    AgentMesh m{};
+    m.lo[0] = gm.x_min;
+    m.lo[1] = gm.y_min;
+    m.lo[2] = gm.z_min;
+    m.hi[0] = gm.x_max;
+    m.hi[1] = gm.y_max;
+    m.hi[2] = gm.z_max;
+    m.h[0] = gm.dx;
+    m.h[1] = gm.dy;
+    m.h[2] = gm.dz;
+    m.n[0] = gm.nx;
+    m.n[1] = gm.ny;
+    m.n[2] = gm.nz;
+    m.nvox = gm.voxel_count();
+    m.vox_lo = agent_filter_ ? filter_lo_ : 0;
+    m.vox_hi = agent_filter_ ? filter_hi_ : m.nvox;
+    m.key_span = m.vox_hi - m.vox_lo;
+    m.sentinel = m.key_span * replicas_;
+    const int end_bit = bits_for(m.sentinel);
+    const unsigned long long none = ~0ull;
+    ck(cudaMemcpyAsync(agent_bad_, &none, sizeof(none), cudaMemcpyHostToDevice, st), "reset");
+    ck(cudaMemsetAsync(agent_counts_, 0, 2 * sizeof(long long), st), "reset");
+    ck(cudaMemsetAsync(group_offsets_, 0, sizeof(long long), st), "reset");
+    const int block = 256;
+    begin_kernel(kAux);
+    agent_keys<<<blocks(N, block), block, 0, st>>>(in_pos_, in_rep_, N, m, id_order_, keys_a_, agent_bad_);
+    end_kernel(kAux);
+    std::size_t bytes = cub_bytes_;
+    ck(cub::DeviceRadixSort::SortPairs(cub_tmp_, bytes, keys_a_, keys_b_, id_order_, vals_b_, N, 0, end_bit, st),
+       "cub sort");
+    begin_kernel(kAux);
+    group_flags<<<blocks(N, block), block, 0, st>>>(keys_b_, N, m.sentinel, flags_);
+    end_kernel(kAux);
+    bytes = cub_bytes_;
+    ck(cub::DeviceScan::ExclusiveSum(cub_tmp_, bytes, flags_, scan_, N, st), "cub scan");
+    begin_kernel(kAux);
+    group_write<<<blocks(N, block), block, 0, st>>>(keys_b_, flags_, scan_, N, m.sentinel, group_voxel_,
+                                                    group_offsets_, agent_counts_);
+    end_kernel(kAux);
+    begin_kernel(kAux);
+    agent_gather<<<blocks(N * S_, block), block, 0, st>>>(vals_b_, N, S_, in_vol_, in_sec_, in_upt_, in_sat_,
+                                                          agent_volume_, agent_secretion_, agent_uptake_,
+                                                          agent_saturation_);
+    end_kernel(kAux);
+    unsigned long long bad = 0;
+    long long counts[2] = {0, 0};
+    ck(cudaMemcpyAsync(&bad, agent_bad_, sizeof(bad), cudaMemcpyDeviceToHost, st), "download");
+    ck(cudaMemcpyAsync(counts, agent_counts_, sizeof(counts), cudaMemcpyDeviceToHost, st), "download");
+    ck(cudaStreamSynchronize(st), "sync");
+    factors_valid_ = false;
+    groups_ = counts[0];
+    grouped_agents_ = counts[1];
+    if (bad != ~0ull) {
+        // mesh.cpp:74-76 (nearest_voxel's std::domain_error, same message).
+        double p[3];
+        ck(cudaMemcpy(p, in_pos_ + 3 * bad, sizeof(p), cudaMemcpyDeviceToHost), "download");
+        groups_ = 0;
+        grouped_agents_ = 0;
+        throw std::domain_error("position (" + format_double(p[0]) + "," + format_double(p[1]) + "," +
+                                format_double(p[2]) + ") outside the simulation domain");
+    }
+}
+
+void DeviceSession::set_agent_positions(const double* xyz, std::int64_t n)
+{
+    if (n != n_agents_) throw std::invalid_argument("position count does not match the agent count");
+    if (n == 0) return;
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    auto st = static_cast<cudaStream_t>(stream_);
+    ck(cudaMemcpyAsync(in_pos_, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st), "upload positions");
+    ck(cudaStreamSynchronize(st), "sync");
+}
+
+// AgentPopulation::set_position (agents.cpp:45-54): the id must exist.
+void DeviceSession::set_agent_position(std::int64_t id, const double* xyz)
+{
+    if (replicas_ > 1) throw state_error("set_position by id needs a single-replica session (ids repeat across replicas)");
+    auto it = id_index_.find(id);
+    if (it == id_index_.end()) throw std::invalid_argument("no agent with id " + std::to_string(id));
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    auto st = static_cast<cudaStream_t>(stream_);
+    ck(cudaMemcpyAsync(in_pos_ + 3 * it->second, xyz, 3 * sizeof(double), cudaMemcpyHostToDevice, st), "upload");
+    ck(cudaStreamSynchronize(st), "sync");
+}
+
+std::int64_t DeviceSession::download_grouping(std::int64_t* group_voxel, std::int64_t* group_offsets,
+                                              std::int64_t* order)
+{
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    synchronize();
+    if (groups_ == 0) {
+        if (group_offsets) group_offsets[0] = 0;
+        return 0;
+    }
+    if (group_voxel)
+        ck(cudaMemcpy(group_voxel, group_voxel_, sizeof(long long) * groups_, cudaMemcpyDeviceToHost), "download");
+    if (group_offsets)
+        ck(cudaMemcpy(group_offsets, group_offsets_, sizeof(long long) * (groups_ + 1), cudaMemcpyDeviceToHost),
+           "download");
+    if (order)
+        ck(cudaMemcpy(order, vals_b_, sizeof(long long) * grouped_agents_, cudaMemcpyDeviceToHost), "download");
+    return groups_;
+}
+
+void DeviceSession::download_agents(std::int64_t* ids, double* pos, double* vol, double* sec, double* upt,
+                                    double* sat)
+{
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    synchronize();
+    const std::size_t N = static_cast<std::size_t>(n_agents_), S = static_cast<std::size_t>(S_);
+    if (N == 0) return;
+    auto down = [&](void* h, const void* d, std::size_t bytes) {
+        if (h) ck(cudaMemcpy(h, d, bytes, cudaMemcpyDeviceToHost), "download agents");
+    };
+    down(ids, in_ids_, 8 * N);
+    down(pos, in_pos_, 24 * N);
+    down(vol, in_vol_, 8 * N);
+    down(sec, in_sec_, 8 * N * S);
+    down(upt, in_upt_, 8 * N * S);
+    down(sat, in_sat_, 8 * N * S);
+}
+
+} // namespace biodiff_b200

@@ -185,6 +185,73 @@ int biodiff_nearest_voxel(const biodiff_mesh* mesh, const double position[3], in
     });
 }
 
+int biodiff_parse_agents_csv(const biodiff_mesh* mesh, const char* path, const char* const* names, int32_t substrates,
+                             int64_t* n, int64_t* ids, double* xyz, double* volume, double* secretion, double* uptake,
+                             double* saturation)
+{
+    return guarded([&] {
+        need(path, "path");
+        need(names, "names");
+        need(n, "n");
+        std::vector<std::string> v;
+        for (int s = 0; s < substrates; ++s) {
+            need(names[s], "substrate name");
+            v.emplace_back(names[s]);
+        }
+        const AgentPopulation pop = load_agents(path, to_mesh(mesh), v);
+        const auto& all = pop.agents();
+        *n = static_cast<int64_t>(all.size());
+        if (!ids || !xyz || !volume || !secretion || !uptake || !saturation) return;
+        const int S = substrates;
+        for (std::size_t a = 0; a < all.size(); ++a) {
+            ids[a] = all[a].id;
+            for (int c = 0; c < 3; ++c) xyz[3 * a + c] = all[a].position[c];
+            volume[a] = all[a].volume;
+            for (int s = 0; s < S; ++s) {
+                secretion[a * S + s] = all[a].secretion_rates[s];
+                uptake[a * S + s] = all[a].uptake_rates[s];
+                saturation[a * S + s] = all[a].saturation_densities[s];
+            }
+        }
+    });
+}
+
+int biodiff_write_agents_csv(const char* path, const char* const* names, int32_t substrates, int64_t n,
+                             const int64_t* ids, const double* xyz, const double* volume, const double* secretion,
+                             const double* uptake, const double* saturation)
+{
+    return guarded([&] {
+        need(path, "path");
+        need(names, "names");
+        if (n < 0) throw std::invalid_argument("negative agent count");
+        if (n > 0) {
+            need(ids, "ids");
+            need(xyz, "xyz");
+            need(volume, "volume");
+            need(secretion, "secretion");
+            need(uptake, "uptake");
+            need(saturation, "saturation");
+        }
+        std::vector<std::string> v;
+        for (int s = 0; s < substrates; ++s) {
+            need(names[s], "substrate name");
+            v.emplace_back(names[s]);
+        }
+        const int S = substrates;
+        std::vector<CellAgent> agents(static_cast<std::size_t>(n));
+        for (int64_t a = 0; a < n; ++a) {
+            CellAgent& c = agents[a];
+            c.id = ids[a];
+            c.position = {xyz[3 * a], xyz[3 * a + 1], xyz[3 * a + 2]};
+            c.volume = volume[a];
+            c.secretion_rates.assign(secretion + a * S, secretion + (a + 1) * S);
+            c.uptake_rates.assign(uptake + a * S, uptake + (a + 1) * S);
+            c.saturation_densities.assign(saturation + a * S, saturation + (a + 1) * S);
+        }
+        save_agents(agents, v, path);
+    });
+}
+
 int biodiff_precompute_thomas(const biodiff_mesh* mesh, int32_t substrates, const double* diffusion,
                               const double* decay, double dt, int32_t axis, int32_t dims, double* off_diag,
                               double* denom_inv, double* c_back)
@@ -295,6 +362,33 @@ int biodiff_set_dirichlet(biodiff_session* session, int64_t count, const int64_t
     });
 }
 
+namespace {
+
+std::vector<std::string> substrate_names(const biodiff_session* session, const char* const* names)
+{
+    need(names, "names");
+    std::vector<std::string> v;
+    for (int s = 0; s < session->S; ++s) {
+        need(names[s], "substrate name");
+        v.emplace_back(names[s]);
+    }
+    return v;
+}
+
+void install_agents(biodiff_session* session, const AgentPopulation& pop)
+{
+    DeviceSession& d = dev(session);
+    if (session->replicas > 1) throw state_error("ensembles take agents through biodiff_ensemble_set_agents");
+    if (!session->slab) {
+        d.set_agents(pop);
+    } else {
+        const std::int64_t plane = static_cast<std::int64_t>(session->mesh.nx) * session->mesh.ny;
+        d.set_agents_range(pop, session->mesh, session->z0 * plane, session->z1 * plane);
+    }
+}
+
+} // namespace
+
 int biodiff_set_agents(biodiff_session* session, int64_t n, const int64_t* ids, const double* positions,
                        const double* volume, const double* secretion, const double* uptake,
                        const double* saturation)
@@ -321,13 +415,8 @@ int biodiff_set_agents(biodiff_session* session, int64_t n, const int64_t* ids, 
             c.uptake_rates.assign(uptake + a * S, uptake + (a + 1) * S);
             c.saturation_densities.assign(saturation + a * S, saturation + (a + 1) * S);
         }
-        AgentPopulation pop(std::move(agents), session->mesh, S); // global validation + grouping
-        if (!session->slab) {
-            d.set_agents(pop);
-        } else {
-            const std::int64_t plane = static_cast<std::int64_t>(session->mesh.nx) * session->mesh.ny;
-            d.set_agents_range(pop, session->z0 * plane, session->z1 * plane);
-        }
+        (void)d;
+        install_agents(session, AgentPopulation(std::move(agents), session->mesh, S)); // host validation
     });
 }
 
@@ -336,16 +425,90 @@ int biodiff_agent_grouping(biodiff_session* session, int64_t* groups, int64_t* g
 {
     return guarded([&] {
         need(groups, "groups");
-        const auto& g = dev(session).agents().grouping();
-        *groups = static_cast<int64_t>(g.size());
-        if (!group_voxel || !group_offsets || !order) return;
-        int64_t m = 0;
-        for (std::size_t k = 0; k < g.size(); ++k) {
-            group_voxel[k] = g[k].first;
-            group_offsets[k] = m;
-            for (std::size_t idx : g[k].second) order[m++] = static_cast<int64_t>(idx);
+        DeviceSession& d = dev(session);
+        if (!group_voxel || !group_offsets || !order) {
+            *groups = d.download_grouping(nullptr, nullptr, nullptr);
+            return;
         }
-        group_offsets[g.size()] = m;
+        *groups = d.download_grouping(group_voxel, group_offsets, order);
+    });
+}
+
+int biodiff_agent_count(biodiff_session* session, int64_t* n)
+{
+    return guarded([&] {
+        need(n, "n");
+        *n = dev(session).agent_count();
+    });
+}
+
+int biodiff_set_agent_positions(biodiff_session* session, const double* xyz, int64_t n)
+{
+    return guarded([&] {
+        if (n > 0) need(xyz, "xyz");
+        dev(session).set_agent_positions(xyz, n);
+    });
+}
+
+int biodiff_set_agent_position(biodiff_session* session, int64_t id, const double* xyz)
+{
+    return guarded([&] {
+        need(xyz, "xyz");
+        dev(session).set_agent_position(id, xyz);
+    });
+}
+
+int biodiff_agent_positions_device(biodiff_session* session, double** xyz)
+{
+    return guarded([&] {
+        need(xyz, "xyz");
+        *xyz = dev(session).agent_positions_device();
+    });
+}
+
+int biodiff_rebuild_voxel_grouping(biodiff_session* session)
+{
+    return guarded([&] { dev(session).rebuild_voxel_grouping(); });
+}
+
+int biodiff_download_agents(biodiff_session* session, int64_t* ids, double* xyz, double* volume, double* secretion,
+                            double* uptake, double* saturation)
+{
+    return guarded([&] { dev(session).download_agents(ids, xyz, volume, secretion, uptake, saturation); });
+}
+
+
+int biodiff_load_agents_csv(biodiff_session* session, const char* path, const char* const* names)
+{
+    return guarded([&] {
+        need(path, "path");
+        const auto v = substrate_names(session, names);
+        install_agents(session, load_agents(path, session->mesh, v));
+    });
+}
+
+int biodiff_save_agents_csv(biodiff_session* session, const char* path, const char* const* names)
+{
+    return guarded([&] {
+        need(path, "path");
+        const auto v = substrate_names(session, names);
+        DeviceSession& d = dev(session);
+        const std::int64_t n = d.agent_count();
+        const int S = session->S;
+        std::vector<std::int64_t> ids(n);
+        std::vector<double> xyz(3 * n), vol(n), sec(n * S), upt(n * S), sat(n * S);
+        d.download_agents(ids.data(), xyz.data(), vol.data(), sec.data(), upt.data(), sat.data());
+        std::vector<CellAgent> agents(n);
+        for (std::int64_t a = 0; a < n; ++a) {
+            CellAgent& c = agents[a];
+            c.id = ids[a];
+            c.position = {xyz[3 * a], xyz[3 * a + 1], xyz[3 * a + 2]};
+            c.volume = vol[a];
+            c.secretion_rates.assign(sec.begin() + a * S, sec.begin() + (a + 1) * S);
+            c.uptake_rates.assign(upt.begin() + a * S, upt.begin() + (a + 1) * S);
+            c.saturation_densities.assign(sat.begin() + a * S, sat.begin() + (a + 1) * S);
+        }
+        save_agents(agents, v, path);
     });
 }
 

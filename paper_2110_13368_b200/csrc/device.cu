@@ -188,14 +188,7 @@ DeviceSession::~DeviceSession()
     dfree(dir_res_values_);
     dfree(shell_values_);
     dfree(xy_ctr_);
-    dfree(group_voxel_);
-    dfree(group_offsets_);
-    dfree(agent_volume_);
-    dfree(agent_secretion_);
-    dfree(agent_uptake_);
-    dfree(agent_saturation_);
-    dfree(agent_add_);
-    dfree(agent_den_);
+    release_agents();
     release_slab();
     for (auto& pe : pending_events_) {
         cudaEventDestroy(static_cast<cudaEvent_t>(pe.second.first));
@@ -459,83 +452,6 @@ void DeviceSession::set_agents(const AgentPopulation& agents)
 {
     set_agents_multi({&agents});
     agents_ = agents;
-}
-
-// Ensembles: population r lives in replica r (voxel offset r * voxel_count).
-void DeviceSession::set_agents_multi(const std::vector<const AgentPopulation*>& pops)
-{
-    ck(cudaSetDevice(device_), "cudaSetDevice");
-    auto st = static_cast<cudaStream_t>(stream_);
-    ck(cudaStreamSynchronize(st), "sync");
-    if (static_cast<int>(pops.size()) > replicas_) throw state_error("more agent populations than replicas");
-    const int S = S_;
-    std::vector<std::int64_t> gv, go;
-    std::vector<double> vol, sec, upt, sat;
-    std::int64_t m = 0;
-    // Longest groups first (dense tumour cores): distinct voxels commute, so
-    // the group order is free; it only shortens the kernel's tail.
-    struct G {
-        const AgentPopulation* pop;
-        std::size_t g;
-        std::int64_t offset;
-    };
-    std::vector<G> gorder;
-    for (std::size_t r = 0; r < pops.size(); ++r)
-        for (std::size_t g = 0; g < pops[r]->grouping().size(); ++g)
-            gorder.push_back({pops[r], g, static_cast<std::int64_t>(r) * mesh_.voxel_count()});
-    std::stable_sort(gorder.begin(), gorder.end(), [](const G& a, const G& b) {
-        return a.pop->grouping()[a.g].second.size() > b.pop->grouping()[b.g].second.size();
-    });
-    gv.reserve(gorder.size());
-    go.reserve(gorder.size() + 1);
-    for (const G& gr : gorder) {
-        const auto& all = gr.pop->agents();
-        const auto& [gvoxel, idxs] = gr.pop->grouping()[gr.g];
-        if (set_agents_filtered_ && (gvoxel < filter_lo_ || gvoxel >= filter_hi_)) continue;
-        if (gvoxel < 0 || (!set_agents_filtered_ && gvoxel >= mesh_.voxel_count()))
-            throw state_error("agent voxel " + std::to_string(gvoxel) + " outside the mesh; rebuild the voxel grouping");
-        const index_t voxel = (set_agents_filtered_ ? gvoxel - filter_lo_ : gvoxel) + gr.offset;
-        if (voxel < 0 || voxel >= mesh_.voxel_count() * replicas_)
-            throw state_error("agent voxel " + std::to_string(voxel) + " outside the mesh; rebuild the voxel grouping");
-        gv.push_back(voxel);
-        go.push_back(m);
-        for (std::size_t idx : idxs) {
-            const CellAgent& a = all[idx];
-            if (a.secretion_rates.size() != static_cast<std::size_t>(S))
-                throw state_error("agent rate vectors do not match the substrate count");
-            vol.push_back(a.volume);
-            for (int s = 0; s < S; ++s) {
-                sec.push_back(a.secretion_rates[s]);
-                upt.push_back(a.uptake_rates[s]);
-                sat.push_back(a.saturation_densities[s]);
-            }
-            ++m;
-        }
-    }
-    go.push_back(m);
-    dfree(group_voxel_);
-    dfree(group_offsets_);
-    dfree(agent_volume_);
-    dfree(agent_secretion_);
-    dfree(agent_uptake_);
-    dfree(agent_saturation_);
-    dfree(agent_add_);
-    dfree(agent_den_);
-    factors_valid_ = false;
-    groups_ = static_cast<std::int64_t>(gv.size());
-    n_agents_ = m;
-    group_voxel_ = dalloc_copy(gv.data(), gv.size(), st);
-    group_offsets_ = dalloc_copy(go.data(), go.size(), st);
-    agent_volume_ = dalloc_copy(vol.data(), vol.size(), st);
-    agent_secretion_ = dalloc_copy(sec.data(), sec.size(), st);
-    agent_uptake_ = dalloc_copy(upt.data(), upt.size(), st);
-    agent_saturation_ = dalloc_copy(sat.data(), sat.size(), st);
-    if (m > 0) {
-        ck(cudaMalloc(&agent_add_, sizeof(double) * m * S), "cudaMalloc");
-        ck(cudaMalloc(&agent_den_, sizeof(double) * m * S), "cudaMalloc");
-    }
-    ck(cudaStreamSynchronize(st), "sync");
-    invalidate_graphs();
 }
 
 void DeviceSession::upload(const double* values, std::int64_t count)
@@ -1036,16 +952,18 @@ void DeviceSession::ensure_source_factors(double dt)
     factors_valid_ = true;
 }
 
+// Launched over the agent capacity; the kernel reads the group count of the
+// last (device) rebuild, so graphs stay valid across rebuilds.
 void DeviceSession::launch_sources(double dt)
 {
-    if (groups_ == 0) return;
+    if (n_agents_ == 0) return;
     ensure_source_factors(dt);
-    const long long total = groups_ * S_;
+    const long long total = n_agents_ * S_;
     const int block = 128;
     begin_kernel(kSources);
     kernels::sources_groups<<<static_cast<unsigned>((total + block - 1) / block), block, 0,
-                              static_cast<cudaStream_t>(stream_)>>>(rho_, S_, groups_, group_voxel_, group_offsets_,
-                                                                    agent_add_, agent_den_);
+                              static_cast<cudaStream_t>(stream_)>>>(rho_, S_, agent_counts_, group_voxel_,
+                                                                    group_offsets_, agent_add_, agent_den_);
     end_kernel(kSources);
 }
 

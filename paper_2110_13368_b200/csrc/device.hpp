@@ -7,6 +7,7 @@
 
 #include <cstdint>
 #include <map>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -87,6 +88,18 @@ public:
     void set_agents(const AgentPopulation& agents);
     const AgentPopulation& agents() const { return agents_; }
 
+    // ---- on-device agent grouping (agents.cu) ------------
+    // Agents live on the device in input order (set_agents order; ensembles:
+    // replica-major). Moving them and regrouping needs no host round trip.
+    std::int64_t agent_count() const { return n_agents_; }
+    void set_agent_positions(const double* xyz, std::int64_t n);   // host xyz[3n], input order
+    void set_agent_position(std::int64_t id, const double* xyz);   // AgentPopulation::set_position
+    double* agent_positions_device() const { return in_pos_; }     // device xyz[3n] (caller-side movers)
+    void rebuild_voxel_grouping();                                  // agents.cpp:56-73 on the device
+    // Group CSR in (voxel, id) order: returns G; voxel[G], offsets[G+1], order[grouped agents].
+    std::int64_t download_grouping(std::int64_t* group_voxel, std::int64_t* group_offsets, std::int64_t* order);
+    void download_agents(std::int64_t* ids, double* pos, double* vol, double* sec, double* upt, double* sat);
+
     void upload(const double* values, std::int64_t count);
     void fill(const double* initial); // [S] per-substrate initial condition
     void download(double* values, std::int64_t count);
@@ -127,7 +140,8 @@ public:
     static void link_local(const std::vector<DeviceSession*>& slabs);
     static void group_advance(const std::vector<DeviceSession*>& slabs, std::int64_t steps, double dt,
                               bool with_sources);
-    void set_agents_range(const AgentPopulation& agents, std::int64_t vox_lo, std::int64_t vox_hi);
+    void set_agents_range(const AgentPopulation& agents, const CartesianMesh& global_mesh, std::int64_t vox_lo,
+                          std::int64_t vox_hi);
 
 private:
     bool slab_ = false;
@@ -155,8 +169,10 @@ private:
     void slab_step_nccl(bool with_sources, double dt);
     void nccl_exchange(double* send, int send_peer, double* recv, int recv_peer);
     std::int64_t plane_count() const { return static_cast<std::int64_t>(mesh_.nx) * mesh_.ny * S_; }
-    bool set_agents_filtered_ = false; // set_agents keeps groups with voxel in [filter_lo_, filter_hi_)
+    bool agent_filter_ = false; // z-slab: groups keep global voxels in [filter_lo_, filter_hi_), made local
     std::int64_t filter_lo_ = 0, filter_hi_ = 0;
+    bool agent_mesh_set_ = false; // z-slab: agents are located on the global mesh
+    CartesianMesh agent_mesh_;
     void release_slab();
 
     void check_ready(Axis axis) const;
@@ -210,10 +226,31 @@ private:
     std::uint64_t shell_mask_ = 0;
     double* shell_values_ = nullptr; // [S]
 
-    // Agents in group order (CSR): group voxel, offsets, per-agent params.
+    // Agents: input-order arrays (in_*), the id-rank order, sort scratch,
+    // and the group CSR + per-agent parameters in group order.
     AgentPopulation agents_;
-    std::int64_t groups_ = 0;
-    std::int64_t n_agents_ = 0;
+    std::int64_t groups_ = 0;          // host copy of the last rebuild's group count
+    std::int64_t grouped_agents_ = 0;  // agents inside the mesh (slab) after the last rebuild
+    std::int64_t n_agents_ = 0;        // agent capacity (all agents handed to set_agents)
+    std::int64_t* in_ids_ = nullptr;
+    double* in_pos_ = nullptr;
+    int* in_rep_ = nullptr;
+    double* in_vol_ = nullptr;
+    double* in_sec_ = nullptr;
+    double* in_upt_ = nullptr;
+    double* in_sat_ = nullptr;
+    std::int64_t* id_order_ = nullptr;
+    std::int64_t* keys_a_ = nullptr;
+    std::int64_t* keys_b_ = nullptr;
+    std::int64_t* vals_b_ = nullptr;   // agent indices in (voxel, id) order
+    int* flags_ = nullptr;
+    std::int64_t* scan_ = nullptr;
+    std::int64_t* agent_counts_ = nullptr; // [0] groups, [1] grouped agents (device)
+    unsigned long long* agent_bad_ = nullptr;
+    void* cub_tmp_ = nullptr;
+    std::size_t cub_bytes_ = 0;
+    std::unordered_map<std::int64_t, std::int64_t> id_index_;
+    void release_agents();
     std::int64_t* group_voxel_ = nullptr;
     std::int64_t* group_offsets_ = nullptr;
     double* agent_volume_ = nullptr;

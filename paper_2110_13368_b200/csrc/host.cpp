@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <charconv>
 #include <cmath>
+#include <fstream>
 #include <unordered_set>
 
 namespace biodiff_b200 {
@@ -253,6 +254,149 @@ void AgentPopulation::rebuild_voxel_grouping(const CartesianMesh& mesh)
         if (groups_.empty() || groups_.back().first != agents_[i].voxel) groups_.push_back({agents_[i].voxel, {}});
         groups_.back().second.push_back(i);
     }
+}
+
+// ---- text.cpp:16-76 --------------------------------------------------------
+
+std::string format_int(std::int64_t v)
+{
+    char buf[32];
+    auto r = std::to_chars(buf, buf + sizeof(buf), v);
+    return std::string(buf, r.ptr);
+}
+
+std::string trim(const std::string& s)
+{
+    const char* ws = " \t\r\n";
+    const auto b = s.find_first_not_of(ws);
+    if (b == std::string::npos) return {};
+    const auto e = s.find_last_not_of(ws);
+    return s.substr(b, e - b + 1);
+}
+
+std::vector<std::string> split_csv_line(const std::string& line)
+{
+    std::vector<std::string> fields;
+    std::size_t start = 0;
+    while (true) {
+        const std::size_t comma = line.find(',', start);
+        if (comma == std::string::npos) {
+            fields.emplace_back(line.substr(start));
+            break;
+        }
+        fields.emplace_back(line.substr(start, comma - start));
+        start = comma + 1;
+    }
+    return fields;
+}
+
+namespace {
+
+[[noreturn]] void bad_token(const std::string& token, const std::string& what)
+{
+    throw std::invalid_argument("invalid number '" + token + "' for " + what);
+}
+
+} // namespace
+
+double parse_double(const std::string& token, const std::string& what)
+{
+    const std::string t = trim(token);
+    double value = 0.0;
+    const auto r = std::from_chars(t.data(), t.data() + t.size(), value);
+    if (r.ec != std::errc{} || r.ptr != t.data() + t.size() || t.empty()) bad_token(token, what);
+    return value;
+}
+
+std::int64_t parse_int(const std::string& token, const std::string& what)
+{
+    const std::string t = trim(token);
+    std::int64_t value = 0;
+    const auto r = std::from_chars(t.data(), t.data() + t.size(), value);
+    if (r.ec != std::errc{} || r.ptr != t.data() + t.size() || t.empty()) bad_token(token, what);
+    return value;
+}
+
+// ---- config.cpp:407-491: agent CSV -----------------------------------------
+
+namespace {
+
+[[noreturn]] void agent_fail(const std::string& path, std::size_t line, const std::string& msg)
+{
+    throw config_error("agent file " + path + " line " + format_int(static_cast<std::int64_t>(line)) + ": " + msg);
+}
+
+std::string agent_header(const std::vector<std::string>& names)
+{
+    std::string h = "id,x,y,z,volume";
+    for (const auto& n : names) h += ",S_" + n + ",U_" + n + ",target_" + n;
+    return h;
+}
+
+} // namespace
+
+AgentPopulation load_agents(const std::string& path, const CartesianMesh& mesh,
+                            const std::vector<std::string>& substrate_names)
+{
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw config_error("agent file not found: " + path);
+    const std::string expected = agent_header(substrate_names);
+    std::string line;
+    std::size_t line_no = 0;
+    if (!std::getline(in, line)) throw config_error("agent file " + path + " is empty");
+    ++line_no;
+    if (trim(line) != expected) agent_fail(path, line_no, "header must be '" + expected + "'");
+    const std::size_t S = substrate_names.size();
+    std::vector<CellAgent> agents;
+    while (std::getline(in, line)) {
+        ++line_no;
+        const std::string stripped = trim(line);
+        if (stripped.empty()) continue;
+        const auto f = split_csv_line(stripped);
+        if (f.size() != 5 + 3 * S)
+            agent_fail(path, line_no,
+                       "expected " + format_int(static_cast<std::int64_t>(5 + 3 * S)) + " fields, got " +
+                           format_int(static_cast<std::int64_t>(f.size())));
+        try {
+            CellAgent a;
+            a.id = parse_int(f[0], "id");
+            a.position = {parse_double(f[1], "x"), parse_double(f[2], "y"), parse_double(f[3], "z")};
+            a.volume = parse_double(f[4], "volume");
+            a.secretion_rates.resize(S);
+            a.uptake_rates.resize(S);
+            a.saturation_densities.resize(S);
+            for (std::size_t s = 0; s < S; ++s) {
+                a.secretion_rates[s] = parse_double(f[5 + 3 * s], "secretion rate");
+                a.uptake_rates[s] = parse_double(f[6 + 3 * s], "uptake rate");
+                a.saturation_densities[s] = parse_double(f[7 + 3 * s], "target density");
+            }
+            agents.push_back(std::move(a));
+        } catch (const std::invalid_argument& e) {
+            agent_fail(path, line_no, e.what());
+        }
+    }
+    try {
+        return AgentPopulation(std::move(agents), mesh, static_cast<int>(S));
+    } catch (const std::exception& e) {
+        throw config_error("agent file " + path + ": " + e.what());
+    }
+}
+
+void save_agents(const std::vector<CellAgent>& agents, const std::vector<std::string>& substrate_names,
+                 const std::string& path)
+{
+    std::ofstream out(path, std::ios::binary);
+    if (!out) throw io_error("cannot open " + path + " for writing");
+    out << agent_header(substrate_names) << "\n";
+    for (const auto& a : agents) {
+        out << format_int(a.id) << ',' << format_double(a.position[0]) << ',' << format_double(a.position[1]) << ','
+            << format_double(a.position[2]) << ',' << format_double(a.volume);
+        for (std::size_t s = 0; s < substrate_names.size(); ++s)
+            out << ',' << format_double(a.secretion_rates[s]) << ',' << format_double(a.uptake_rates[s]) << ','
+                << format_double(a.saturation_densities[s]);
+        out << "\n";
+    }
+    if (!out) throw io_error("failed writing " + path);
 }
 
 } // namespace biodiff_b200

@@ -200,4 +200,21 @@ void cell_sources_sinks_step(DensityField& field, const AgentPopulation& agents,
 
 std::string format_double(double v);
 
+// text.cpp:16-76 (the reference's token rules: std::from_chars over the
+// trimmed token, the whole token must parse; std::invalid_argument
+// "invalid number '<token>' for <what>").
+std::string format_int(std::int64_t v);
+std::string trim(const std::string& s);
+std::vector<std::string> split_csv_line(const std::string& line);
+double parse_double(const std::string& token, const std::string& what);
+std::int64_t parse_int(const std::string& token, const std::string& what);
+
+// config.cpp:416-477 / 479-491: agent CSV ingest and export. Header
+// "id,x,y,z,volume" + ",S_<name>,U_<name>,target_<name>" per substrate;
+// errors are config_error("agent file <path> line <n>: ...") / io_error.
+AgentPopulation load_agents(const std::string& path, const CartesianMesh& mesh,
+                            const std::vector<std::string>& substrate_names);
+void save_agents(const std::vector<CellAgent>& agents, const std::vector<std::string>& substrate_names,
+                 const std::string& path);
+
 } // namespace biodiff_b200

@@ -868,13 +868,14 @@ static __global__ void sources_factors(int S, long long agents, const double* vo
 // One thread per (voxel group, substrate); the group's agents are applied in
 // ascending-id order: x <- (x + add) / den. Agents of distinct voxels commute
 // and substrates are independent, so (group, s) threads reproduce the
-// reference's agent-outer / substrate-inner loop bitwise. Groups are stored
-// longest-first so the dense-core voxels start early.
-static __global__ void sources_groups(double* rho, int S, long long groups, const int64_t* group_voxel,
+// reference's agent-outer / substrate-inner loop bitwise. Groups are in
+// (voxel) order, built on the device (agents.cu); counts[0] is the group
+// count of the last rebuild (the grid covers the agent capacity).
+static __global__ void sources_groups(double* rho, int S, const int64_t* counts, const int64_t* group_voxel,
                                const int64_t* group_offsets, const double* add, const double* den)
 {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= groups * S) return;
+    if (t >= counts[0] * S) return;
     const long long g = t / S;
     const int s = static_cast<int>(t % S);
     double* r = rho + group_voxel[g] * S + s;

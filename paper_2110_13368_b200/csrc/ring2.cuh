@@ -306,9 +306,9 @@ __device__ __forceinline__ Ring2Smem ring2_carve(unsigned char* smem)
 template <int NS, bool CLAMP>
 __global__ void __launch_bounds__(kLanes) sweep_yz_ring2(const __grid_constant__ CUtensorMap tmap, StridedSweep a)
 {
-    extern __shared__ __align__(1024) unsigned char smem[];
+    extern __shared__ __align__(1024) unsigned char smem_r2[];
     constexpr int kSlot = kChunk * kLanes;
-    const Ring2Smem sm = ring2_carve<NS>(smem);
+    const Ring2Smem sm = ring2_carve<NS>(smem_r2);
     const int lane = threadIdx.x;
     const int G = gridDim.x;
     int t = blockIdx.x;
@@ -377,10 +377,10 @@ struct XSweep2 {
 template <int NS, int S, bool CLAMP>
 __global__ void __launch_bounds__(kLanes) sweep_x_ring2(const __grid_constant__ CUtensorMap tmap, XSweep2 a)
 {
-    extern __shared__ __align__(1024) unsigned char smem[];
+    extern __shared__ __align__(1024) unsigned char smem_r2[];
     constexpr int kSlot = kChunk * kLanes;
     constexpr int L = kLanes / S;
-    const Ring2Smem sm = ring2_carve<NS>(smem);
+    const Ring2Smem sm = ring2_carve<NS>(smem_r2);
     const int lane = threadIdx.x;
     const long long G = gridDim.x;
     long long t = blockIdx.x;

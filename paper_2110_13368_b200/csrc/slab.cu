@@ -333,16 +333,18 @@ void DeviceSession::release_slab()
     nccl_comm_ = nullptr;
 }
 
-void DeviceSession::set_agents_range(const AgentPopulation& agents, std::int64_t vox_lo, std::int64_t vox_hi)
+void DeviceSession::set_agents_range(const AgentPopulation& agents, const CartesianMesh& global_mesh,
+                                     std::int64_t vox_lo, std::int64_t vox_hi)
 {
-    // Keep the groups whose (global) voxel lies in [vox_lo, vox_hi) and make
-    // their voxel indices local; the (voxel, id) order is preserved.
-    AgentPopulation local = agents;
-    set_agents_filtered_ = true;
+    // Every agent is kept on the device (they may move between slabs); each
+    // rebuild groups those whose GLOBAL voxel lies in [vox_lo, vox_hi), with
+    // slab-local voxel indices, in (voxel, id) order.
+    agent_filter_ = true;
     filter_lo_ = vox_lo;
     filter_hi_ = vox_hi;
-    set_agents(local);
-    set_agents_filtered_ = false;
+    agent_mesh_ = global_mesh;
+    agent_mesh_set_ = true;
+    set_agents(agents);
 }
 
 } // namespace biodiff_b200

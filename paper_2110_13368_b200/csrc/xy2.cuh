@@ -80,10 +80,10 @@ template <int NS, int S>
 __global__ void __launch_bounds__(kLanes) sweep_xy2(const __grid_constant__ CUtensorMap tmap_x,
                                                     const __grid_constant__ CUtensorMap tmap_y, XYFused2 a)
 {
-    extern __shared__ __align__(1024) unsigned char smem[];
+    extern __shared__ __align__(1024) unsigned char smem_r2[];
     constexpr int kSlot = kChunk * kLanes;
     constexpr int L = kLanes / S;
-    const Ring2Smem sm = ring2_carve<NS>(smem);
+    const Ring2Smem sm = ring2_carve<NS>(smem_r2);
     const int lane = threadIdx.x;
     const int nchx = (a.nx + kChunk - 1) / kChunk;
     const int nchy = (a.ny + kChunk - 1) / kChunk;
