@@ -242,6 +242,10 @@ int DeviceSession::ring_slots(int axis) const
     // (4 slots cost occupancy: 8 -> 6 CTAs per SM, slower).
     const char* e = std::getenv("BIODIFF_RING_SLOTS");
     const int want = e ? std::max(2, std::atoi(e)) : (axis == 0 ? 4 : 3);
+    // Short y / z lines (<= 2 chunks): two slot sets, alternate tiles (ring2
+    // solve_short2) so the next tile loads while this one computes (C5
+    // 64-point lines: y 1253 -> 1197 us, z 1294 -> 1246; x measured slower).
+    if (!e && axis != 0 && nch <= 2 && std::getenv("BIODIFF_NO_SHORT") == nullptr) return 2 * nch;
     return std::min(nch, want);
 }
 
@@ -772,9 +776,14 @@ const void* x_ring2_fn()
     return reinterpret_cast<const void*>(kernels::sweep_x_ring2<NS, S, CLAMP>);
 }
 
+// short: two slot sets for lines of <= ns/2 chunks (solve_short2); only
+// ns = 2 (one-chunk lines) and ns = 4 (two-chunk lines) occur.
 template <bool CLAMP>
-const void* yz_ring2_pick(int ns)
+const void* yz_ring2_pick(int ns, bool short_lines)
 {
+    if (short_lines)
+        return ns == 2 ? reinterpret_cast<const void*>(kernels::sweep_yz_ring2<2, CLAMP, true>)
+                       : reinterpret_cast<const void*>(kernels::sweep_yz_ring2<4, CLAMP, true>);
     switch (ns) {
     case 1: return yz_ring2_fn<1, CLAMP>();
     case 2: return yz_ring2_fn<2, CLAMP>();
@@ -784,8 +793,11 @@ const void* yz_ring2_pick(int ns)
 }
 
 template <int S, bool CLAMP>
-const void* x_ring2_pick_ns(int ns)
+const void* x_ring2_pick_ns(int ns, bool short_lines)
 {
+    if (short_lines)
+        return ns == 2 ? reinterpret_cast<const void*>(kernels::sweep_x_ring2<2, S, CLAMP, true>)
+                       : reinterpret_cast<const void*>(kernels::sweep_x_ring2<4, S, CLAMP, true>);
     switch (ns) {
     case 1: return x_ring2_fn<1, S, CLAMP>();
     case 2: return x_ring2_fn<2, S, CLAMP>();
@@ -795,11 +807,11 @@ const void* x_ring2_pick_ns(int ns)
 }
 
 template <bool CLAMP>
-const void* x_ring2_pick(int ns, int S)
+const void* x_ring2_pick(int ns, int S, bool short_lines)
 {
-    if (S == 1) return x_ring2_pick_ns<1, CLAMP>(ns);
-    if (S == 2) return x_ring2_pick_ns<2, CLAMP>(ns);
-    return x_ring2_pick_ns<4, CLAMP>(ns);
+    if (S == 1) return x_ring2_pick_ns<1, CLAMP>(ns, short_lines);
+    if (S == 2) return x_ring2_pick_ns<2, CLAMP>(ns, short_lines);
+    return x_ring2_pick_ns<4, CLAMP>(ns, short_lines);
 }
 
 } // namespace
@@ -833,7 +845,9 @@ void DeviceSession::launch_ring2(int ax, bool do_clamp, const kernels::Clamp& cl
         x.xi = (mesh_.ny + L - 1) / L;
         x.tiles = static_cast<long long>(x.xi) * x.planes;
         x.clamp = cl;
-        const void* fn = do_clamp ? x_ring2_pick<true>(ns, S_) : x_ring2_pick<false>(ns, S_);
+        const int nchx = (mesh_.nx + kernels::kChunk - 1) / kernels::kChunk;
+        const bool short_lines = 2 * nchx <= ns && (ns == 2 || ns == 4);
+        const void* fn = do_clamp ? x_ring2_pick<true>(ns, S_, short_lines) : x_ring2_pick<false>(ns, S_, short_lines);
         const unsigned grid = ring_persist_x_ ? occupancy_grid(fn, x.tiles) : static_cast<unsigned>(x.tiles);
         if (!ring_persist_x_) ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
         void* args[] = {const_cast<CUtensorMap*>(&tm), &x};
@@ -855,9 +869,11 @@ void DeviceSession::launch_ring2(int ax, bool do_clamp, const kernels::Clamp& cl
     y.clamp = cl;
     y.exp_bottom = (slab_ && ax == 2) ? plane_bottom_ : nullptr;
     y.exp_top = (slab_ && ax == 2) ? plane_top_ : nullptr;
-    const void* fn = do_clamp ? yz_ring2_pick<true>(ns) : yz_ring2_pick<false>(ns);
+    const int nch = (y.n + kernels::kChunk - 1) / kernels::kChunk;
+    const bool short_lines = 2 * nch <= ns && (ns == 2 || ns == 4);
+    const void* fn = do_clamp ? yz_ring2_pick<true>(ns, short_lines) : yz_ring2_pick<false>(ns, short_lines);
     unsigned grid;
-    if (ring_persist_yz_) {
+    if (ring_persist_yz_ || short_lines) { // short lines: persistent, next tile prefetched (solve_short2)
         grid = occupancy_grid(fn, y.tiles);
     } else {
         ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");

@@ -275,6 +275,67 @@ __device__ __forceinline__ void solve_ring2(const Chain& c, bool active, uint64_
     __syncwarp();
 }
 
+// Short lines (2 * nch <= NS, e.g. the C5 ensemble's 64-point lines): every
+// chunk of a tile stays resident (no reloads) and the slots form two sets
+// used by alternate tiles, so the NEXT tile's chunks are issued when this
+// tile starts — its load latency hides behind a whole tile of work instead of
+// the last chunk's back substitution. `base` = first slot of this tile's set.
+template <int NS, bool CLAMP, class Lay, class Next, class Load, class Store>
+__device__ __forceinline__ void solve_short2(const Chain& c, bool active, uint64_t* bars, double* slots,
+                                             int slot_doubles, int lane, uint32_t& parity, int base, Next has_next,
+                                             const Lay& lay, Load load, Store store, const SlabExport* exp)
+{
+    const int n = c.n;
+    const int nch = (n + kChunk - 1) / kChunk;
+    const int other = nch - base;
+    auto wait_slot = [&](int s) {
+        ptx::mbar_wait(&bars[s], (parity >> s) & 1u);
+        parity ^= (1u << s);
+    };
+    if (lane == 0 && has_next()) {
+        ptx::bulk_wait_read<0>(); // the previous tile's stores out of the other set
+        for (int k = 0; k < nch; ++k) load(1, k, other + k);
+    }
+    __syncwarp();
+    double prev = 0.0;
+    for (int k = 0; k < nch; ++k) {
+        wait_slot(base + k);
+        const int m0 = k * kChunk;
+        const int cnt = min(kChunk, n - m0);
+        if (active) {
+            double* sl = slots + (base + k) * slot_doubles;
+            const bool constc = k > 0 && m0 >= c.settle && m0 + cnt <= n - 1;
+            if (cnt == kChunk)
+                prev = fwd_chunk<true>(c, sl, lay, m0, cnt, k == 0, constc, true, prev);
+            else
+                prev = fwd_chunk<false>(c, sl, lay, m0, cnt, k == 0, constc, true, prev);
+        }
+    }
+    if (exp && active && exp->bottom) exp->bottom[exp->idx] = prev;
+    double next = prev;
+    for (int k = nch - 1; k >= 0; --k) {
+        const int m0 = k * kChunk;
+        const int cnt = min(kChunk, n - m0);
+        if (active) {
+            double* sl = slots + (base + k) * slot_doubles;
+            const bool top = k == nch - 1;
+            const bool constb = m0 >= c.settle;
+            if (cnt == kChunk)
+                next = bwd_chunk<true, CLAMP>(c, sl, lay, m0, cnt, top, constb, next);
+            else
+                next = bwd_chunk<false, CLAMP>(c, sl, lay, m0, cnt, top, constb, next);
+        }
+        ptx::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            store(k, base + k);
+            ptx::bulk_commit();
+        }
+    }
+    if (exp && active && exp->top) exp->top[exp->idx] = next;
+    __syncwarp();
+}
+
 // Dynamic smem of the ring2 kernels: 1024-byte aligned slots (the x box
 // uses the 128-byte swizzle), then mbarriers, then checkpoints.
 __host__ __device__ constexpr int ring2_smem_bytes(int ns, int nch)
@@ -303,7 +364,7 @@ __device__ __forceinline__ Ring2Smem ring2_carve(unsigned char* smem)
 // y / z sweep: tile t = (32-double column block e0 of a row, outer index,
 // replica); persistent over t, t + G, ... (G = grid; one tile per CTA when
 // the grid covers every tile).
-template <int NS, bool CLAMP>
+template <int NS, bool CLAMP, bool SHORT = false>
 __global__ void __launch_bounds__(kLanes) sweep_yz_ring2(const __grid_constant__ CUtensorMap tmap, StridedSweep a)
 {
     extern __shared__ __align__(1024) unsigned char smem_r2[];
@@ -340,6 +401,7 @@ __global__ void __launch_bounds__(kLanes) sweep_yz_ring2(const __grid_constant__
     }
     __syncwarp();
     uint32_t parity = 0;
+    int it = 0;
     const LayoutYZ lay{lane};
     for (; t < a.tiles; t += G) {
         const int tn = t + G;
@@ -351,15 +413,20 @@ __global__ void __launch_bounds__(kLanes) sweep_yz_ring2(const __grid_constant__
         const int s = e % a.S, i = e / a.S;
         const Chain c = make_chain_yz(a, s, i, outer, r);
         const SlabExport ex{a.exp_bottom, a.exp_top, static_cast<long long>(outer) * a.rowlen + e};
-        solve_ring2<NS, CLAMP>(
-            c, active, sm.bars, sm.slots, kSlot, sm.ckpt, lane, parity, [&] { return tn < a.tiles; }, lay,
-            [&](int rel, int k, int slot) { issue(rel ? dn : dc, k, slot); },
-            [&](int k, int slot) {
-                const int c1 = a.axis == 2 ? outer : k * kChunk;
-                const int c2 = a.axis == 2 ? k * kChunk : outer;
-                ptx::tma_store_4d(&tmap, e0, c1, c2, r, sm.slots + slot * kSlot);
-            },
-            &ex);
+        auto has_next = [&] { return tn < a.tiles; };
+        auto load = [&](int rel, int k, int slot) { issue(rel ? dn : dc, k, slot); };
+        auto store = [&](int k, int slot) {
+            const int c1 = a.axis == 2 ? outer : k * kChunk;
+            const int c2 = a.axis == 2 ? k * kChunk : outer;
+            ptx::tma_store_4d(&tmap, e0, c1, c2, r, sm.slots + slot * kSlot);
+        };
+        if constexpr (SHORT) // host guarantees 2 * nch <= NS
+            solve_short2<NS, CLAMP>(c, active, sm.bars, sm.slots, kSlot, lane, parity, (it & 1) ? nch : 0, has_next,
+                                    lay, load, store, &ex);
+        else
+            solve_ring2<NS, CLAMP>(c, active, sm.bars, sm.slots, kSlot, sm.ckpt, lane, parity, has_next, lay, load,
+                                   store, &ex);
+        ++it;
     }
 }
 
@@ -374,7 +441,7 @@ struct XSweep2 {
     Clamp clamp;
 };
 
-template <int NS, int S, bool CLAMP>
+template <int NS, int S, bool CLAMP, bool SHORT = false>
 __global__ void __launch_bounds__(kLanes) sweep_x_ring2(const __grid_constant__ CUtensorMap tmap, XSweep2 a)
 {
     extern __shared__ __align__(1024) unsigned char smem_r2[];
@@ -399,6 +466,7 @@ __global__ void __launch_bounds__(kLanes) sweep_x_ring2(const __grid_constant__ 
     }
     __syncwarp();
     uint32_t parity = 0;
+    int it = 0;
     const int l = lane / S, sub = lane % S;
     const LayoutX<S> lay(l, sub);
     for (; t < a.tiles; t += G) {
@@ -409,16 +477,21 @@ __global__ void __launch_bounds__(kLanes) sweep_x_ring2(const __grid_constant__ 
         const int j = j0 + l;
         const bool active = j < a.ny;
         const Chain c = make_chain(a.coef, S, sub, a.nx, a.clamp, j == 0 || j == a.ny - 1 || kface(kk, a.clamp), rep);
-        solve_ring2<NS, CLAMP>(
-            c, active, sm.bars, sm.slots, kSlot, sm.ckpt, lane, parity, [&] { return tn < a.tiles; }, lay,
-            [&](int rel, int k, int slot) {
-                if (rel)
-                    issue(Pn, j0n, k, slot);
-                else
-                    issue(P, j0, k, slot);
-            },
-            [&](int k, int slot) { ptx::tma_store_4d(&tmap, 0, j0, P, k * 2 * S, sm.slots + slot * kSlot); },
-            nullptr);
+        auto has_next = [&] { return tn < a.tiles; };
+        auto load = [&](int rel, int k, int slot) {
+            if (rel)
+                issue(Pn, j0n, k, slot);
+            else
+                issue(P, j0, k, slot);
+        };
+        auto store = [&](int k, int slot) { ptx::tma_store_4d(&tmap, 0, j0, P, k * 2 * S, sm.slots + slot * kSlot); };
+        if constexpr (SHORT) // host guarantees 2 * nch <= NS
+            solve_short2<NS, CLAMP>(c, active, sm.bars, sm.slots, kSlot, lane, parity, (it & 1) ? nch : 0, has_next,
+                                    lay, load, store, nullptr);
+        else
+            solve_ring2<NS, CLAMP>(c, active, sm.bars, sm.slots, kSlot, sm.ckpt, lane, parity, has_next, lay, load,
+                                   store, nullptr);
+        ++it;
     }
 }
 
