@@ -238,10 +238,12 @@ int DeviceSession::ring_slots(int axis) const
 {
     const int n = axis == 0 ? mesh_.nx : axis == 1 ? mesh_.ny : mesh_.nz;
     const int nch = (n + kernels::kChunk - 1) / kernels::kChunk;
-    // x: 4 slots (deeper prefetch measured faster: C3 226 -> 217 us); y / z: 3
-    // (4 slots cost occupancy: 8 -> 6 CTAs per SM, slower).
+    // x: 2 slots (C3, after the bank-conflict-free lane map: 2 slots 208 us,
+    // 3 slots 218, 4 slots 218 — occupancy is register-bound at 8 CTAs/SM
+    // either way); y / z: 3 (2 and 4 measured slower).
     const char* e = std::getenv("BIODIFF_RING_SLOTS");
-    const int want = e ? std::max(2, std::atoi(e)) : (axis == 0 ? 4 : 3);
+    if (axis == 0 && std::getenv("BIODIFF_X_SLOTS")) e = std::getenv("BIODIFF_X_SLOTS");
+    const int want = e ? std::max(2, std::atoi(e)) : (axis == 0 ? 2 : 3);
     // Short y / z lines (<= 2 chunks): two slot sets, alternate tiles (ring2
     // solve_short2) so the next tile loads while this one computes (C5
     // 64-point lines: y 1253 -> 1197 us, z 1294 -> 1246; x measured slower).

@@ -55,6 +55,20 @@ struct LayoutX {
     __device__ __forceinline__ int off(int u) const { return row + t[u % P] + (u / P) * (L * 16); }
 };
 
+// Lane -> (line, substrate) of an x tile. With the swizzle above, lines l
+// and l^1 share a 32-byte granule pair at every position, so they must not
+// sit in the same half-warp (64-bit shared accesses are served per 16 lanes):
+// at S = 4 the half-warps take the even and the odd lines (ncu: the plain
+// lane/S mapping measured 4 bank-conflict wavefronts per load). S <= 2
+// needs no remap (at S = 2 a half-warp's 8 lines hit 8 distinct granules).
+template <int S>
+__device__ __forceinline__ void x_lane(int lane, int& l, int& s)
+{
+    s = lane % S;
+    const int q = lane / S;
+    l = S == 4 ? (((q & 3) << 1) | (q >> 2)) : q;
+}
+
 // Forward elimination over positions u < cnt of one chunk (line positions
 // m0 + u). `first`: position 0 of the line (fwd_first). `constc`: every row
 // of the chunk is in the settled region. `keep`: store the forward values
@@ -467,7 +481,8 @@ __global__ void __launch_bounds__(kLanes) sweep_x_ring2(const __grid_constant__ 
     __syncwarp();
     uint32_t parity = 0;
     int it = 0;
-    const int l = lane / S, sub = lane % S;
+    int l, sub;
+    x_lane<S>(lane, l, sub);
     const LayoutX<S> lay(l, sub);
     for (; t < a.tiles; t += G) {
         const long long tn = t + G;

@@ -161,7 +161,8 @@ __global__ void __launch_bounds__(kLanes) sweep_xy2(const __grid_constant__ CUte
         };
         if (cur.kind == 0) {
             const int j0 = cur.it * L;
-            const int l = lane / S, sub = lane % S;
+            int l, sub;
+            x_lane<S>(lane, l, sub);
             const int rep = cur.P / a.nz, kk = cur.P % a.nz;
             const int j = j0 + l;
             const LayoutX<S> lay(l, sub);
