@@ -159,6 +159,21 @@ int biodiff_write_agents_csv(const char* path, const char* const* names, int32_t
                              const double* uptake, const double* saturation);
 int biodiff_save_agents_csv(biodiff_session* session, const char* path, const char* const* names);
 
+/* PhysiCell's vector-of-vectors density (mesh.hpp:93-100, mesh.cpp:101-136):
+ *   translate_vector_to_array : host only; voxels[v] points at counts[v]
+ *       values; writes the flat voxel-major array to out (if non-null) and
+ *       the substrate count; status 2 "ragged nested density: voxel ..." as
+ *       the reference when counts differ.
+ *   upload_field_nested / download_field_nested: the session field from /
+ *       to per-voxel host buffers (one pack + one copy each way).
+ *   field_all_finite : DensityField::all_finite (mesh.cpp:95-99) on the device. */
+int biodiff_translate_vector_to_array(const double* const* voxels, const int64_t* counts, int64_t nvox, double* out,
+                                      int32_t* substrates);
+int biodiff_upload_field_nested(biodiff_session* session, const double* const* voxels, const int64_t* counts,
+                                int64_t nvox);
+int biodiff_download_field_nested(biodiff_session* session, double* const* voxels, int64_t nvox);
+int biodiff_field_all_finite(biodiff_session* session, int32_t* finite);
+
 /* Fills every voxel with the per-substrate values initial[S] on the device —
  * the initial condition of Microenvironment::create (mesh.cpp:173-195)
  * without staging a host copy of the field. */

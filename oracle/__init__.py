@@ -122,6 +122,8 @@ def ref_lib():
         L.ref_mutant_check.argtypes = [_P(ctypes.c_int)]
         L.ref_format_double.argtypes = [_d, ctypes.c_char_p, ctypes.c_int]
         L.ref_format_int.argtypes = [_i64, ctypes.c_char_p, ctypes.c_int]
+        L.ref_translate_vector_to_array.argtypes = [_P(_P(_d)), _P(_i64), _i64, _P(_d), _P(ctypes.c_int)]
+        L.ref_translate_round_trip.argtypes = [_P(_d), _i64, ctypes.c_int, _P(_d)]
         L.ref_load_agents.argtypes = [_vp, ctypes.c_char_p, _P(ctypes.c_char_p), ctypes.c_int]
         L.ref_agent_count.argtypes = [_vp]
         L.ref_agent_count.restype = _i64

@@ -153,6 +153,34 @@ int ref_get_agents(void* h, int64_t* ids, double* pos, double* vol, double* sec,
     });
 }
 
+// translate_vector_to_array (mesh.cpp:101-119) of the reference on a nested
+// density given as per-voxel pointers; out may be null (count only).
+int ref_translate_vector_to_array(const double* const* voxels, const int64_t* counts, int64_t nvox, double* out,
+                                  int* substrates)
+{
+    return guarded([&] {
+        NestedDensity nested(static_cast<std::size_t>(nvox));
+        for (int64_t v = 0; v < nvox; ++v) nested[v].assign(voxels[v], voxels[v] + counts[v]);
+        const DensityField f = translate_vector_to_array(nested);
+        *substrates = f.substrates;
+        if (out) std::copy(f.values.begin(), f.values.end(), out);
+    });
+}
+
+// translate_array_to_vector (mesh.cpp:121-136) round trip: flat -> nested -> flat.
+int ref_translate_round_trip(const double* flat, int64_t count, int S, double* out)
+{
+    return guarded([&] {
+        DensityField f;
+        f.substrates = S;
+        f.values.assign(flat, flat + count);
+        const NestedDensity nested = translate_array_to_vector(f);
+        int64_t k = 0;
+        for (const auto& v : nested)
+            for (double x : v) out[k++] = x;
+    });
+}
+
 // format_int (text.cpp:16-21).
 int ref_format_int(int64_t v, char* out, int cap)
 {

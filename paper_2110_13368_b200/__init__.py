@@ -118,6 +118,10 @@ _SIGNATURES = {
     "biodiff_write_agents_csv": (ctypes.c_int, [ctypes.c_char_p, _P(ctypes.c_char_p), _i32, _i64, _P(_i64), _P(_d),
                                                 _P(_d), _P(_d), _P(_d), _P(_d)]),
     "biodiff_upload_field": (ctypes.c_int, [_vp, _P(_d), _i64]),
+    "biodiff_translate_vector_to_array": (ctypes.c_int, [_P(_P(_d)), _P(_i64), _i64, _P(_d), _P(_i32)]),
+    "biodiff_upload_field_nested": (ctypes.c_int, [_vp, _P(_P(_d)), _P(_i64), _i64]),
+    "biodiff_download_field_nested": (ctypes.c_int, [_vp, _P(_P(_d)), _i64]),
+    "biodiff_field_all_finite": (ctypes.c_int, [_vp, _P(_i32)]),
     "biodiff_fill_field": (ctypes.c_int, [_vp, _P(_d)]),
     "biodiff_download_field": (ctypes.c_int, [_vp, _P(_d), _i64]),
     "biodiff_diffusion_sweep": (ctypes.c_int, [_vp, _i32]),
@@ -199,6 +203,20 @@ def nearest_voxel(mesh: Mesh, position) -> int:
     out = _i64()
     _check(lib().biodiff_nearest_voxel(ctypes.byref(mesh), _dptr(p), ctypes.byref(out)))
     return int(out.value)
+
+
+def translate_vector_to_array(nested):
+    """translate_vector_to_array (mesh.cpp:101-119) on the host: (flat values, substrate count)."""
+    arrs = [np.ascontiguousarray(np.asarray(v, dtype=np.float64)) for v in nested]
+    ptrs = (_P(_d) * max(1, len(arrs)))(*[_dptr(a) for a in arrs])
+    counts = np.array([a.size for a in arrs] or [0], dtype=np.int64)
+    S = _i32()
+    _check(lib().biodiff_translate_vector_to_array(ptrs, counts.ctypes.data_as(_P(_i64)), len(arrs), None,
+                                                   ctypes.byref(S)))
+    out = np.empty(len(arrs) * S.value)
+    _check(lib().biodiff_translate_vector_to_array(ptrs, counts.ctypes.data_as(_P(_i64)), len(arrs), _dptr(out),
+                                                   ctypes.byref(S)))
+    return out, int(S.value)
 
 
 def parse_agents_csv(mesh: Mesh, path: str, names):
@@ -443,6 +461,27 @@ class Session:
     def upload_field(self, values):
         a = _f64(values, self.value_count)
         _check(lib().biodiff_upload_field(self._h, _dptr(a), a.size))
+
+    def upload_field_nested(self, nested):
+        """PhysiCell's vector-of-vectors density (one array per voxel) -> HBM (mesh.cpp:101-119 checks)."""
+        arrs = [np.ascontiguousarray(np.asarray(v, dtype=np.float64)) for v in nested]
+        ptrs = (_P(_d) * max(1, len(arrs)))(*[_dptr(a) for a in arrs])
+        counts = np.array([a.size for a in arrs], dtype=np.int64)
+        _check(lib().biodiff_upload_field_nested(self._h, ptrs, counts.ctypes.data_as(_P(_i64)), len(arrs)))
+
+    def download_field_nested(self):
+        """HBM -> a list of per-voxel arrays (translate_array_to_vector, mesh.cpp:121-136)."""
+        nvox = self.value_count // self.S
+        arrs = [np.empty(self.S) for _ in range(nvox)]
+        ptrs = (_P(_d) * max(1, nvox))(*[_dptr(a) for a in arrs])
+        _check(lib().biodiff_download_field_nested(self._h, ptrs, nvox))
+        return arrs
+
+    def all_finite(self) -> bool:
+        """DensityField::all_finite (mesh.cpp:95-99) on the device field."""
+        f = _i32()
+        _check(lib().biodiff_field_all_finite(self._h, ctypes.byref(f)))
+        return bool(f.value)
 
     def fill_field(self, initial):
         """Every voxel := initial[S] (Microenvironment::create's initial condition)."""

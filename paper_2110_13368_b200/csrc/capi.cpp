@@ -512,6 +512,74 @@ int biodiff_save_agents_csv(biodiff_session* session, const char* path, const ch
     });
 }
 
+int biodiff_translate_vector_to_array(const double* const* voxels, const int64_t* counts, int64_t nvox, double* out,
+                                      int32_t* substrates)
+{
+    return guarded([&] {
+        need(substrates, "substrates");
+        if (nvox < 0) throw std::invalid_argument("negative voxel count");
+        if (nvox > 0) {
+            need(voxels, "voxels");
+            need(counts, "counts");
+        }
+        NestedDensity nested(static_cast<std::size_t>(nvox));
+        for (int64_t v = 0; v < nvox; ++v) {
+            if (counts[v] < 0) throw std::invalid_argument("negative substrate count");
+            if (counts[v] > 0) need(voxels[v], "voxel values");
+            nested[v].assign(voxels[v], voxels[v] + counts[v]);
+        }
+        const DensityField f = translate_vector_to_array(nested);
+        *substrates = f.substrates;
+        if (out) std::copy(f.values.begin(), f.values.end(), out);
+    });
+}
+
+int biodiff_upload_field_nested(biodiff_session* session, const double* const* voxels, const int64_t* counts,
+                                int64_t nvox)
+{
+    return guarded([&] {
+        DeviceSession& d = dev(session);
+        if (nvox != d.value_count() / d.substrates()) throw state_error("density field size does not match the mesh");
+        need(voxels, "voxels");
+        need(counts, "counts");
+        const int S = d.substrates();
+        std::vector<double> flat(static_cast<std::size_t>(d.value_count()));
+        for (int64_t v = 0; v < nvox; ++v) {
+            if (counts[v] != S)  // translate_vector_to_array's ragged check (mesh.cpp:110-114)
+                throw std::invalid_argument("ragged nested density: voxel " + format_int(v) + " holds " +
+                                            format_int(counts[v]) + " substrates, expected " + format_int(S));
+            need(voxels[v], "voxel values");
+            std::copy(voxels[v], voxels[v] + S, flat.begin() + v * S);
+        }
+        d.upload(flat.data(), static_cast<std::int64_t>(flat.size()));
+        d.synchronize();
+    });
+}
+
+int biodiff_download_field_nested(biodiff_session* session, double* const* voxels, int64_t nvox)
+{
+    return guarded([&] {
+        DeviceSession& d = dev(session);
+        if (nvox != d.value_count() / d.substrates()) throw state_error("density field size does not match the mesh");
+        need(voxels, "voxels");
+        const int S = d.substrates();
+        std::vector<double> flat(static_cast<std::size_t>(d.value_count()));
+        d.download(flat.data(), static_cast<std::int64_t>(flat.size()));
+        for (int64_t v = 0; v < nvox; ++v) {
+            need(voxels[v], "voxel values");
+            std::copy(flat.begin() + v * S, flat.begin() + (v + 1) * S, voxels[v]);
+        }
+    });
+}
+
+int biodiff_field_all_finite(biodiff_session* session, int32_t* finite)
+{
+    return guarded([&] {
+        need(finite, "finite");
+        *finite = dev(session).all_finite() ? 1 : 0;
+    });
+}
+
 int biodiff_upload_field(biodiff_session* session, const double* values, int64_t count)
 {
     return guarded([&] {

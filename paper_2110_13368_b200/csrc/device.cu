@@ -1076,6 +1076,23 @@ void DeviceSession::advance(std::int64_t steps, double dt, bool with_sources)
     if (steps % kGraphSteps) run_chunk(steps % kGraphSteps);
 }
 
+bool DeviceSession::all_finite()
+{
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    auto st = static_cast<cudaStream_t>(stream_);
+    int* flag = nullptr;
+    ck(cudaMalloc(&flag, sizeof(int)), "cudaMalloc");
+    ck(cudaMemsetAsync(flag, 0, sizeof(int), st), "memset");
+    begin_kernel(kAux);
+    kernels::any_nonfinite<<<sm_count_ * 4, 256, 0, st>>>(rho_, value_count(), flag);
+    end_kernel(kAux);
+    int h = 0;
+    ck(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, st), "D2H");
+    ck(cudaStreamSynchronize(st), "sync");
+    cudaFree(flag);
+    return h == 0;
+}
+
 void DeviceSession::cross_check(const double* other, std::int64_t count, double abs_tol, double rel_tol,
                                 double* max_abs, double* max_rel, std::int64_t* worst, bool* pass)
 {
@@ -1141,6 +1158,22 @@ void DeviceBackend::download(DensityField& field)
     field.values.resize(static_cast<std::size_t>(session_->value_count()));
     field.substrates = session_->substrates();
     session_->download(field.values.data(), static_cast<std::int64_t>(field.values.size()));
+}
+
+void DeviceBackend::upload(const NestedDensity& nested)
+{
+    if (!session_) throw state_error("device backend not attached");
+    const DensityField flat = translate_vector_to_array(nested);
+    if (flat.substrates != session_->substrates() && !nested.empty())
+        throw state_error("nested density substrate count does not match the session");
+    session_->upload(flat.values.data(), static_cast<std::int64_t>(flat.values.size()));
+}
+
+void DeviceBackend::download(NestedDensity& nested)
+{
+    DensityField flat;
+    download(flat);
+    nested = translate_array_to_vector(flat);
 }
 
 void diffuse_decay_step(Microenvironment& env, const SolverWorkspaces& workspaces, DeviceBackend& backend)

@@ -119,6 +119,7 @@ public:
     std::int64_t launch_count() const { return launches_; }
     SweepPath path(Axis axis) const { return path_[static_cast<int>(axis)]; }
 
+    bool all_finite(); // DensityField::all_finite on the device field
     void cross_check(const double* other, std::int64_t count, double abs_tol, double rel_tol, double* max_abs,
                      double* max_rel, std::int64_t* worst, bool* pass);
 

@@ -256,6 +256,47 @@ void AgentPopulation::rebuild_voxel_grouping(const CartesianMesh& mesh)
     }
 }
 
+// ---- mesh.cpp:95-136: nested <-> flat --------------------------------------
+
+bool DensityField::all_finite() const
+{
+    return std::all_of(values.begin(), values.end(), [](double v) { return std::isfinite(v); });
+}
+
+DensityField translate_vector_to_array(const NestedDensity& nested)
+{
+    DensityField field;
+    if (nested.empty()) return field;
+    const std::size_t substrates = nested.front().size();
+    field.substrates = static_cast<int>(substrates);
+    field.values.reserve(nested.size() * substrates);
+    for (std::size_t v = 0; v < nested.size(); ++v) {
+        if (nested[v].size() != substrates)
+            throw std::invalid_argument("ragged nested density: voxel " + format_int(static_cast<std::int64_t>(v)) +
+                                        " holds " + format_int(static_cast<std::int64_t>(nested[v].size())) +
+                                        " substrates, expected " + format_int(static_cast<std::int64_t>(substrates)));
+        field.values.insert(field.values.end(), nested[v].begin(), nested[v].end());
+    }
+    return field;
+}
+
+NestedDensity translate_array_to_vector(const DensityField& field)
+{
+    if (field.substrates <= 0) {
+        if (!field.values.empty()) throw std::invalid_argument("density field with values but no substrate count");
+        return {};
+    }
+    if (field.values.size() % field.substrates != 0)
+        throw std::invalid_argument("density array length is not a multiple of the substrate count");
+    const index_t voxels = field.voxel_count();
+    NestedDensity nested(static_cast<std::size_t>(voxels));
+    for (index_t v = 0; v < voxels; ++v) {
+        auto begin = field.values.begin() + v * field.substrates;
+        nested[v].assign(begin, begin + field.substrates);
+    }
+    return nested;
+}
+
 // ---- text.cpp:16-76 --------------------------------------------------------
 
 std::string format_int(std::int64_t v)

@@ -66,7 +66,15 @@ struct DensityField {
     index_t voxel_count() const { return substrates == 0 ? 0 : static_cast<index_t>(values.size()) / substrates; }
     double& at(index_t v, int s) { return values[static_cast<std::size_t>(v) * substrates + s]; }
     double at(index_t v, int s) const { return values[static_cast<std::size_t>(v) * substrates + s]; }
+    bool all_finite() const; // mesh.cpp:95-99
 };
+
+// mesh.hpp:93-100 / mesh.cpp:101-136: PhysiCell's vector-of-vectors density
+// (one std::vector per voxel) <-> the flat voxel-major layout the kernels
+// use. Same checks and messages as the reference.
+using NestedDensity = std::vector<std::vector<double>>;
+DensityField translate_vector_to_array(const NestedDensity& nested);
+NestedDensity translate_array_to_vector(const DensityField& field);
 
 // mesh.hpp:103-110
 struct SubstrateParams {
@@ -178,6 +186,10 @@ public:
     void attach(const Microenvironment& env, const SolverWorkspaces& ws, const AgentPopulation* agents = nullptr);
     void upload(const DensityField& field);
     void download(DensityField& field);
+    // The nested (vector-of-vectors) layout straight to / from HBM: packed on
+    // the host with translate_vector_to_array's checks, one copy each way.
+    void upload(const NestedDensity& nested);
+    void download(NestedDensity& nested);
     void attach_agents(const AgentPopulation& agents);
     const AgentPopulation* attached_agents() const { return agents_from_; }
     DeviceSession& session()

@@ -951,6 +951,17 @@ static __global__ void zslab_correct(double* rho, const double* d_in, const doub
     }
 }
 
+// DensityField::all_finite (mesh.cpp:95-99): flag = 1 if any value is NaN/inf.
+static __global__ void any_nonfinite(const double* a, long long n, int* flag)
+{
+    int bad = 0;
+    for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < n;
+         t += static_cast<long long>(gridDim.x) * blockDim.x)
+        bad |= !isfinite(a[t]);
+    bad = __any_sync(0xffffffffu, bad);
+    if (bad && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
 // values[v*S + s] = initial[s] for every voxel (grid-stride).
 static __global__ void fill_field(double* rho, long long total, const double* initial, int S)
 {

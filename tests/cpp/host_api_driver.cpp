@@ -74,12 +74,18 @@ int main(int argc, char** argv)
         }
         DeviceBackend gpu(0);
         gpu.attach(env, ws, &agents);
+        // The field once more through PhysiCell's vector-of-vectors layout
+        // (mesh.cpp:101-136) — same values, so the run must not change.
+        gpu.upload(translate_array_to_vector(env.field));
         const int steps = 25;
         for (int s = 0; s < steps; ++s) {
             diffuse_decay_step(env, ws, gpu);                             // solver.hpp:72
             cell_sources_sinks_step(env.field, agents, env.mesh, dt, gpu); // agents.hpp:72
         }
-        gpu.download(env.field);
+        NestedDensity nested;
+        gpu.download(nested);
+        env.field = translate_vector_to_array(nested);
+        if (!env.field.all_finite()) throw state_error("non-finite density after the run");
         put(env.field.values.data(), sizeof(double) * env.field.values.size());
         std::printf("ok gpu %zu values\n", env.field.values.size());
         return 0;
