@@ -159,6 +159,36 @@ int biodiff_write_agents_csv(const char* path, const char* const* names, int32_t
                              const double* uptake, const double* saturation);
 int biodiff_save_agents_csv(biodiff_session* session, const char* path, const char* const* names);
 
+/* ---- engine loop (the reference's engine.cpp is absent) ----
+ * Three-tier clock dt_diff <= dt_mech <= dt_cell with integral ratios
+ * (config.cpp:237-244), integer step counting (t_now = steps * dt_diff),
+ * one CUDA-graph advance per mechanics interval, hooks on the calling thread
+ * between device calls. A hook returning non-zero aborts the run (status 2). */
+typedef struct biodiff_clock {
+    double dt_diff, dt_mech, dt_cell, t_max;
+    int64_t per_mech, per_cell, total_steps;           /* derived by biodiff_clock_make */
+    int64_t diffusion_steps, mechanics_steps, cell_steps; /* counters (in/out of a run) */
+    double t_now;                                      /* diffusion_steps * dt_diff */
+} biodiff_clock;
+
+typedef struct biodiff_run_metrics {
+    double wall_seconds, diffusion_seconds, hook_seconds, snapshot_seconds;
+    int64_t diffusion_steps, mechanics_steps, cell_steps, snapshots;
+} biodiff_run_metrics;
+
+typedef int (*biodiff_hook)(void* user, const biodiff_clock* clock);
+
+/* Validated clock with zero counters; status 1 (config_error) on
+ * non-integral ratios or negative t_max. */
+int biodiff_clock_make(double dt_diff, double dt_mech, double dt_cell, double t_max, biodiff_clock* clock);
+
+/* run_simulation (SPEC.md run_simulation): continues from clock's counters
+ * to total_steps; snapshot hook every snapshot_interval simulated minutes
+ * (0 = none); null hooks are no-ops. */
+int biodiff_run_simulation(biodiff_session* session, biodiff_clock* clock, int32_t with_sources,
+                           double snapshot_interval, biodiff_hook mechanics, biodiff_hook cell, biodiff_hook snapshot,
+                           void* user, biodiff_run_metrics* metrics);
+
 /* PhysiCell's vector-of-vectors density (mesh.hpp:93-100, mesh.cpp:101-136):
  *   translate_vector_to_array : host only; voxels[v] points at counts[v]
  *       values; writes the flat voxel-major array to out (if non-null) and

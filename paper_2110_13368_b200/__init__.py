@@ -118,6 +118,9 @@ _SIGNATURES = {
     "biodiff_write_agents_csv": (ctypes.c_int, [ctypes.c_char_p, _P(ctypes.c_char_p), _i32, _i64, _P(_i64), _P(_d),
                                                 _P(_d), _P(_d), _P(_d), _P(_d)]),
     "biodiff_upload_field": (ctypes.c_int, [_vp, _P(_d), _i64]),
+    # engine (typed bindings with the clock / metrics structs: engine.py)
+    "biodiff_clock_make": (ctypes.c_int, [_d, _d, _d, _d, _vp]),
+    "biodiff_run_simulation": (ctypes.c_int, [_vp, _vp, _i32, _d, _vp, _vp, _vp, _vp, _vp]),
     "biodiff_translate_vector_to_array": (ctypes.c_int, [_P(_P(_d)), _P(_i64), _i64, _P(_d), _P(_i32)]),
     "biodiff_upload_field_nested": (ctypes.c_int, [_vp, _P(_P(_d)), _P(_i64), _i64]),
     "biodiff_download_field_nested": (ctypes.c_int, [_vp, _P(_P(_d)), _i64]),

@@ -5,6 +5,7 @@
 #include "../../include/biodiff_b200.h"
 
 #include "device.hpp"
+#include "engine.hpp"
 #include "host.hpp"
 
 #include <cuda_runtime.h>
@@ -509,6 +510,79 @@ int biodiff_save_agents_csv(biodiff_session* session, const char* path, const ch
             c.saturation_densities.assign(sat.begin() + a * S, sat.begin() + (a + 1) * S);
         }
         save_agents(agents, v, path);
+    });
+}
+
+namespace {
+
+void to_c_clock(const SimulationClock& c, biodiff_clock* o)
+{
+    o->dt_diff = c.dt_diff;
+    o->dt_mech = c.dt_mech;
+    o->dt_cell = c.dt_cell;
+    o->t_max = c.t_max;
+    o->per_mech = c.per_mech;
+    o->per_cell = c.per_cell;
+    o->total_steps = c.total_steps;
+    o->diffusion_steps = c.diffusion_steps;
+    o->mechanics_steps = c.mechanics_steps;
+    o->cell_steps = c.cell_steps;
+    o->t_now = c.t_now();
+}
+
+} // namespace
+
+int biodiff_clock_make(double dt_diff, double dt_mech, double dt_cell, double t_max, biodiff_clock* clock)
+{
+    return guarded([&] {
+        need(clock, "clock");
+        to_c_clock(SimulationClock::make(dt_diff, dt_mech, dt_cell, t_max), clock);
+    });
+}
+
+int biodiff_run_simulation(biodiff_session* session, biodiff_clock* clock, int32_t with_sources,
+                           double snapshot_interval, biodiff_hook mechanics, biodiff_hook cell, biodiff_hook snapshot,
+                           void* user, biodiff_run_metrics* metrics)
+{
+    return guarded([&] {
+        need(clock, "clock");
+        SimulationClock c = SimulationClock::make(clock->dt_diff, clock->dt_mech, clock->dt_cell, clock->t_max);
+        if (clock->diffusion_steps < 0 || clock->mechanics_steps < 0 || clock->cell_steps < 0)
+            throw std::invalid_argument("negative clock counters");
+        c.diffusion_steps = clock->diffusion_steps;
+        c.mechanics_steps = clock->mechanics_steps;
+        c.cell_steps = clock->cell_steps;
+        auto wrap = [&](biodiff_hook h, const char* which) -> std::function<void(const SimulationClock&)> {
+            if (!h) return {};
+            return [h, user, which](const SimulationClock& k) {
+                biodiff_clock v;
+                to_c_clock(k, &v);
+                if (h(user, &v) != 0) throw state_error(std::string(which) + " hook aborted the run");
+            };
+        };
+        EngineHooks hooks;
+        hooks.mechanics = wrap(mechanics, "mechanics");
+        hooks.cell = wrap(cell, "cell");
+        hooks.snapshot = wrap(snapshot, "snapshot");
+        hooks.snapshot_interval = snapshot_interval;
+        RunMetrics m;
+        try {
+            m = run_simulation(dev(session), c, with_sources != 0, hooks);
+        } catch (...) {
+            to_c_clock(c, clock); // counters as far as the run got
+            throw;
+        }
+        to_c_clock(c, clock);
+        if (metrics) {
+            metrics->wall_seconds = m.wall_seconds;
+            metrics->diffusion_seconds = m.diffusion_seconds;
+            metrics->hook_seconds = m.hook_seconds;
+            metrics->snapshot_seconds = m.snapshot_seconds;
+            metrics->diffusion_steps = m.diffusion_steps;
+            metrics->mechanics_steps = m.mechanics_steps;
+            metrics->cell_steps = m.cell_steps;
+            metrics->snapshots = m.snapshots;
+        }
     });
 }
 

@@ -1,37 +1,56 @@
 """The engine loop around the hot path (the reference's
 core/engine.cpp is absent from the snapshot, CMakeLists.txt:11).
 
-Three-tier clock: dt_diff < dt_mech < dt_cell with integral ratios
-(config.cpp:237-244; default 10 diffusion steps per mechanics step and 60
-mechanics steps per cell step). Time is counted in integer diffusion steps
-(t_now = steps * dt_diff). Each mechanics interval is ONE
-device call — ``Session.advance(per_mech, dt)``, CUDA-graph replayed — so
-the field stays in HBM for the whole run and the host only wakes up for the
-hooks (no-ops by default) and for snapshots.
+Python view of the native engine (csrc/engine.cpp, C ABI
+``biodiff_clock_make`` / ``biodiff_run_simulation``). Three-tier clock:
+dt_diff < dt_mech < dt_cell with integral ratios (config.cpp:237-244; default
+10 diffusion steps per mechanics step and 60 mechanics steps per cell step).
+Time is counted in integer diffusion steps (t_now = steps * dt_diff,
+SPEC.md:320). Each mechanics interval is ONE device call — a CUDA-graph
+replay — so the field stays in HBM for the whole run and the host only wakes
+up for the hooks (no-ops by default) and for snapshots.
 """
 from __future__ import annotations
 
-import math
-import time
-from dataclasses import dataclass
+import ctypes
+from dataclasses import dataclass, fields
 from typing import Callable, Optional
 
 import paper_2110_13368_b200 as B
 
+_i64, _d = ctypes.c_int64, ctypes.c_double
 
-def _ratio(a: float, b: float, what: str) -> int:
-    """Positive integral a/b (config.cpp:237-244) or ConfigError."""
-    if not (a > 0 and b > 0):
-        raise B.ConfigError(f"{what}: step sizes must be positive")
-    r = a / b
-    n = int(round(r))
-    if n < 1 or abs(r - n) > 1e-9 * max(1.0, r):
-        raise B.ConfigError(f"{what}: ratio {r} is not a positive integer")
-    return n
+
+class CClock(ctypes.Structure):  # include/biodiff_b200.h biodiff_clock
+    _fields_ = [("dt_diff", _d), ("dt_mech", _d), ("dt_cell", _d), ("t_max", _d), ("per_mech", _i64),
+                ("per_cell", _i64), ("total_steps", _i64), ("diffusion_steps", _i64), ("mechanics_steps", _i64),
+                ("cell_steps", _i64), ("t_now", _d)]
+
+
+class CMetrics(ctypes.Structure):  # biodiff_run_metrics
+    _fields_ = [("wall_seconds", _d), ("diffusion_seconds", _d), ("hook_seconds", _d), ("snapshot_seconds", _d),
+                ("diffusion_steps", _i64), ("mechanics_steps", _i64), ("cell_steps", _i64), ("snapshots", _i64)]
+
+
+HOOK = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(CClock))
+_bound = False
+
+
+def _lib():
+    global _bound
+    L = B.lib()
+    if not _bound:
+        L.biodiff_clock_make.restype = ctypes.c_int
+        L.biodiff_clock_make.argtypes = [_d, _d, _d, _d, ctypes.POINTER(CClock)]
+        L.biodiff_run_simulation.restype = ctypes.c_int
+        L.biodiff_run_simulation.argtypes = [ctypes.c_void_p, ctypes.POINTER(CClock), ctypes.c_int32, _d, HOOK, HOOK,
+                                             HOOK, ctypes.c_void_p, ctypes.POINTER(CMetrics)]
+        _bound = True
+    return L
 
 
 @dataclass
-class SimulationClock:
+class SimulationClock:  # SPEC.md:275-281 (validated by the native SimulationClock::make)
     dt_diff: float = 0.01
     dt_mech: float = 0.1
     dt_cell: float = 6.0
@@ -41,22 +60,29 @@ class SimulationClock:
     cell_steps: int = 0
 
     def __post_init__(self):
-        self.per_mech = _ratio(self.dt_mech, self.dt_diff, "dt_mech / dt_diff")
-        self.per_cell = _ratio(self.dt_cell, self.dt_mech, "dt_cell / dt_mech")
-        if self.t_max < 0:
-            raise B.ConfigError("max_time must be non-negative")
-        x = self.t_max / self.dt_diff
-        self.total_steps = int(round(x)) if abs(x - round(x)) <= 1e-9 * max(1.0, x) else int(math.ceil(x))
+        c = CClock()
+        B._check(_lib().biodiff_clock_make(self.dt_diff, self.dt_mech, self.dt_cell, self.t_max, ctypes.byref(c)))
+        self.per_mech, self.per_cell, self.total_steps = int(c.per_mech), int(c.per_cell), int(c.total_steps)
 
     @property
     def t_now(self) -> float:
         return self.diffusion_steps * self.dt_diff  # integer step counting
 
+    def _c(self) -> CClock:
+        c = CClock()
+        for f in ("dt_diff", "dt_mech", "dt_cell", "t_max", "diffusion_steps", "mechanics_steps", "cell_steps"):
+            setattr(c, f, getattr(self, f))
+        return c
+
+    def _sync(self, c: CClock):
+        self.diffusion_steps, self.mechanics_steps, self.cell_steps = (int(c.diffusion_steps),
+                                                                       int(c.mechanics_steps), int(c.cell_steps))
+
 
 @dataclass
 class RunMetrics:
     wall_seconds: float = 0.0
-    diffusion_seconds: float = 0.0  # device time of [diffuse_decay_step; cell_sources_sinks_step] steps
+    diffusion_seconds: float = 0.0  # device time of the [diffuse_decay_step; cell_sources_sinks_step] replays
     hook_seconds: float = 0.0
     snapshot_seconds: float = 0.0
     diffusion_steps: int = 0
@@ -66,45 +92,43 @@ class RunMetrics:
 
     def as_lines(self):
         """key=value metric lines."""
-        return [f"{k}={v}" for k, v in self.__dict__.items()]
+        return [f"{f.name}={getattr(self, f.name)}" for f in fields(self)]
 
 
 def run_simulation(session: B.Session, clock: SimulationClock, with_sources: bool = True,
                    mech_hook: Optional[Callable] = None, cell_hook: Optional[Callable] = None,
                    snapshot_interval: float = 0.0, snapshot_hook: Optional[Callable] = None) -> RunMetrics:
     """for each mechanics step: per_mech x [diffuse_decay_step; cell_sources_sinks_step];
-    every per_cell mechanics steps: cell hook; stop at t_max."""
-    m = RunMetrics()
-    t0 = time.perf_counter()
-    snap_every = int(round(snapshot_interval / clock.dt_diff)) if snapshot_interval and snapshot_interval > 0 else 0
-    next_snap = snap_every if snap_every else None
-    while clock.diffusion_steps < clock.total_steps:
-        n = min(clock.per_mech, clock.total_steps - clock.diffusion_steps)
-        if next_snap is not None:
-            n = min(n, next_snap - clock.diffusion_steps)
-        session.event_record(14)
-        session.advance(n, clock.dt_diff, with_sources)
-        session.event_record(15)
-        m.diffusion_seconds += session.event_elapsed(14, 15) / 1e3
-        clock.diffusion_steps += n
-        if next_snap is not None and clock.diffusion_steps == next_snap:
-            ts = time.perf_counter()
-            if snapshot_hook:
-                snapshot_hook(clock.t_now, session.download_field())
-            m.snapshots += 1
-            m.snapshot_seconds += time.perf_counter() - ts
-            next_snap += snap_every
-        if clock.diffusion_steps % clock.per_mech == 0:
-            clock.mechanics_steps += 1
-            th = time.perf_counter()
-            if mech_hook:
-                mech_hook(clock)
-            if clock.mechanics_steps % clock.per_cell == 0:
-                clock.cell_steps += 1
-                if cell_hook:
-                    cell_hook(clock)
-            m.hook_seconds += time.perf_counter() - th
-    session.synchronize()
-    m.wall_seconds = time.perf_counter() - t0
-    m.diffusion_steps, m.mechanics_steps, m.cell_steps = clock.diffusion_steps, clock.mechanics_steps, clock.cell_steps
-    return m
+    every per_cell mechanics steps: cell hook; snapshots every `snapshot_interval`
+    simulated minutes (``snapshot_hook(t_now, field)``); stop at t_max.
+    Runs in the native engine; Python hooks are called back between device calls."""
+    errors = []
+
+    def wrap(fn, snap=False):
+        if fn is None:
+            return HOOK()  # null: no-op in the engine
+
+        def cb(_user, cp):
+            try:
+                clock._sync(cp.contents)
+                if snap:
+                    fn(clock.t_now, session.download_field())
+                else:
+                    fn(clock)
+                return 0
+            except BaseException as e:  # surfaced after the native call returns
+                errors.append(e)
+                return 1
+        return HOOK(cb)
+
+    hooks = (wrap(mech_hook), wrap(cell_hook), wrap(snapshot_hook, snap=True))
+    c = clock._c()
+    m = CMetrics()
+    rc = _lib().biodiff_run_simulation(session._h, ctypes.byref(c), 1 if with_sources else 0,
+                                       float(snapshot_interval or 0.0), hooks[0], hooks[1], hooks[2], None,
+                                       ctypes.byref(m))
+    clock._sync(c)
+    if errors:
+        raise errors[0]
+    B._check(rc)
+    return RunMetrics(**{f.name: getattr(m, f.name) for f in fields(RunMetrics)})

@@ -50,3 +50,45 @@ def test_engine_zero_time_keeps_initial_condition():
     m = run_simulation(s, SimulationClock(t_max=0.0))
     assert m.diffusion_steps == 0
     assert np.array_equal(s.download_field(), w.initial_field())
+
+
+@pytest.mark.gpu
+def test_engine_snapshots_off_the_mechanics_grid_keep_the_cadence():
+    """A snapshot interval that is not a multiple of dt_mech splits device
+    calls but never shifts the 10:60 cadence (hooks at every 10th step)."""
+    if B.device_count() == 0:
+        pytest.fail("no sm_100 device visible")
+    w = W.make("engine2", (12, 12, 12), 1, 50, 1, seed=7)
+    s = make_session(w)
+    mech, snaps = [], []
+    c = SimulationClock(t_max=1.2, dt_cell=0.6)
+    m = run_simulation(s, c, mech_hook=lambda k: mech.append(k.diffusion_steps), snapshot_interval=0.15,
+                       snapshot_hook=lambda t, f: snaps.append((round(t, 9), f.size)))
+    assert mech == list(range(10, 121, 10)) and m.cell_steps == 2
+    assert [t for t, _ in snaps] == [0.15, 0.3, 0.45, 0.6, 0.75, 0.9, 1.05, 1.2]
+    assert all(n == w.voxels * w.S for _, n in snaps)
+    ref = make_session(w)
+    ref.advance(120, w.dt)
+    assert bits_equal(s.download_field(), ref.download_field())
+
+
+@pytest.mark.gpu
+def test_engine_hook_error_stops_the_run_and_resumes():
+    if B.device_count() == 0:
+        pytest.fail("no sm_100 device visible")
+    w = W.make("engine3", (10, 10, 10), 1, 0, 1)
+    s = make_session(w)
+    c = SimulationClock(t_max=1.0)
+
+    def boom(k):
+        if k.mechanics_steps == 4:
+            raise RuntimeError("stop here")
+
+    with pytest.raises(RuntimeError, match="stop here"):
+        run_simulation(s, c, mech_hook=boom)
+    assert (c.diffusion_steps, c.mechanics_steps) == (40, 4)
+    m = run_simulation(s, c)  # continues from the clock's counters
+    assert c.diffusion_steps == 100 and m.diffusion_steps == 100
+    ref = make_session(w)
+    ref.advance(100, w.dt)
+    assert bits_equal(s.download_field(), ref.download_field())
