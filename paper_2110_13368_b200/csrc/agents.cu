@@ -136,6 +136,26 @@ __global__ void agent_gather(const int64_t* order, long long N, int S, const dou
     sat_g[t] = sat[a * S + s];
 }
 
+// rep_groups[r] = first group of replica r (groups are sorted by key, keys of
+// replica r start at r * key_span); rep_groups[R] = G.
+__global__ void rep_group_bounds(const int64_t* group_voxel, const int64_t* counts, long long key_span, int R,
+                                 int64_t* rep_groups)
+{
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r > R) return;
+    const long long G = counts[0];
+    const long long key = static_cast<long long>(r) * key_span;
+    long long lo = 0, hi = G;
+    while (lo < hi) {
+        const long long mid = (lo + hi) / 2;
+        if (group_voxel[mid] < key)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    rep_groups[r] = r == R ? G : lo;
+}
+
 int bits_for(long long v)
 {
     int b = 1;
@@ -150,7 +170,7 @@ unsigned blocks(long long n, int block) { return static_cast<unsigned>(std::max(
 void DeviceSession::release_agents()
 {
     for (auto** p : {&in_ids_, &id_order_, &keys_a_, &keys_b_, &vals_b_, &scan_, &group_voxel_, &group_offsets_,
-                     &agent_counts_})
+                     &agent_counts_, &rep_groups_})
         dfree(*p);
     for (auto** p : {&in_pos_, &in_vol_, &in_sec_, &in_upt_, &in_sat_, &agent_volume_, &agent_secretion_,
                      &agent_uptake_, &agent_saturation_, &agent_add_, &agent_den_})
@@ -165,6 +185,7 @@ void DeviceSession::release_agents()
     groups_ = 0;
     grouped_agents_ = 0;
     id_index_.clear();
+    rep_agents_.clear();
 }
 
 // Ensembles: population r lives in replica r (keys offset by r * voxels).
@@ -194,6 +215,8 @@ void DeviceSession::set_agents_multi(const std::vector<const AgentPopulation*>& 
             rep.push_back(static_cast<int>(r));
         }
     const std::int64_t N = static_cast<std::int64_t>(ids.size());
+    std::vector<std::int64_t> per_rep(replicas_, 0);
+    for (int r : rep) ++per_rep[r];
     // Ascending-id rank order (the tie-break of the (voxel, id) sort).
     std::vector<std::int64_t> order(N);
     std::iota(order.begin(), order.end(), 0);
@@ -203,6 +226,7 @@ void DeviceSession::set_agents_multi(const std::vector<const AgentPopulation*>& 
     release_agents();
     factors_valid_ = false;
     n_agents_ = N;
+    rep_agents_ = per_rep;
     if (replicas_ == 1)
         for (std::int64_t a = 0; a < N; ++a) id_index_[ids[a]] = a;
     if (N == 0) return;
@@ -226,6 +250,7 @@ void DeviceSession::set_agents_multi(const std::vector<const AgentPopulation*>& 
     dalloc(group_voxel_, N);
     dalloc(group_offsets_, N + 1);
     dalloc(agent_counts_, 2);
+    dalloc(rep_groups_, replicas_ + 1);
     dalloc(agent_bad_, 1);
     dalloc(agent_volume_, N);
     dalloc(agent_secretion_, N * S);
@@ -293,6 +318,10 @@ void DeviceSession::rebuild_voxel_grouping()
     agent_gather<<<blocks(N * S_, block), block, 0, st>>>(vals_b_, N, S_, in_vol_, in_sec_, in_upt_, in_sat_,
                                                           agent_volume_, agent_secretion_, agent_uptake_,
                                                           agent_saturation_);
+    end_kernel(kAux);
+    begin_kernel(kAux);
+    rep_group_bounds<<<blocks(replicas_ + 1, block), block, 0, st>>>(group_voxel_, agent_counts_, m.key_span,
+                                                                      replicas_, rep_groups_);
     end_kernel(kAux);
     unsigned long long bad = 0;
     long long counts[2] = {0, 0};

@@ -142,6 +142,13 @@ DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int devi
     ring_persist_x_ = persist != "0" && persist != "none";
     ring_persist_yz_ = persist == "1" || persist == "all";
     xy_fused_ = std::atoi(env_or("BIODIFF_XY_FUSED", "0")) != 0;
+    if (replicas_ > 1) { // L2 replica batches (step_body_batches)
+        const double replica_mb = static_cast<double>(mesh.voxel_count()) * substrates * 8.0 / 1e6;
+        const double budget = std::atof(env_or("BIODIFF_L2_BATCH_MB", "0")); // opt-in: measured slower (C5 latency-bound)
+        const int nb = budget > 0.0 ? std::max(1, static_cast<int>(budget / replica_mb)) : 0;
+        batch_replicas_ = (nb > 0 && nb < replicas_) ? nb : 0;
+        batch_steps_ = std::max(1, std::atoi(env_or("BIODIFF_BATCH_STEPS", "10")));
+    }
     nzg_ = mesh.nz;
     cudaStream_t st;
     ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -321,6 +328,8 @@ void DeviceSession::set_workspace(Axis axis, int n, int dims, double dt, const d
     dfree(w.cb);
     dfree(w.dconst);
     dfree(w.cconst);
+    dfree(w.dinvT);
+    dfree(w.cbT);
     // Ensembles: replicas_ consecutive coefficient sets (q[R*S], dinv/cb[R*n*S]);
     // the settle row is the max over replicas (warp-uniform in the kernels).
     const std::size_t set = static_cast<std::size_t>(n) * S_;
@@ -338,6 +347,20 @@ void DeviceSession::set_workspace(Axis axis, int n, int dims, double dt, const d
     if (std::getenv("BIODIFF_NO_SETTLE")) w.settle = n;
     w.dconst = dalloc_copy(dc.data(), dc.size(), st);
     w.cconst = dalloc_copy(cc.data(), cc.size(), st);
+    {   // Substrate-major copies (same bits) for ring2's unsettled rows.
+        std::vector<double> dT(set * replicas_), cT(set * replicas_);
+        for (int r = 0; r < replicas_; ++r)
+            for (int m = 0; m < n; ++m)
+                for (int sb = 0; sb < S_; ++sb) {
+                    const std::size_t from = r * set + static_cast<std::size_t>(m) * S_ + sb;
+                    const std::size_t to = (static_cast<std::size_t>(r) * S_ + sb) * n + m;
+                    dT[to] = dinv[from];
+                    cT[to] = cb[from];
+                }
+        w.dinvT = dalloc_copy(dT.data(), dT.size(), st);
+        w.cbT = dalloc_copy(cT.data(), cT.size(), st);
+        ck(cudaStreamSynchronize(st), "sync");
+    }
     ck(cudaStreamSynchronize(st), "sync"); // host staging vectors go out of scope
     w.n = n;
     w.dims = dims;
@@ -448,6 +471,12 @@ void DeviceSession::set_dirichlet(const DirichletMap& map)
     dir_res_voxel_ = dalloc_copy(rvox.data(), rvox.size(), st);
     dir_res_mask_ = dalloc_copy(rmask.data(), rmask.size(), st);
     dir_res_values_ = dalloc_copy(rvals.data(), rvals.size(), st);
+    // Residual entries are in voxel order, hence replica-major: per-replica
+    // offsets for the L2 replica batches.
+    dir_res_rep_off_.assign(static_cast<std::size_t>(replicas_) + 1, 0);
+    for (int r = 0; r <= replicas_; ++r)
+        dir_res_rep_off_[r] = std::lower_bound(rvox.begin(), rvox.end(), static_cast<std::int64_t>(r) * mesh_.voxel_count()) -
+                              rvox.begin();
     shell_mask_ = shell;
     ck(cudaMemcpyAsync(shell_values_, shell_vals.data(), sizeof(double) * S, cudaMemcpyHostToDevice, st), "shell");
     ck(cudaStreamSynchronize(st), "sync");
@@ -596,7 +625,8 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
     const int rowlen = mesh_.nx * S;
     kernels::Clamp cl{shell_values_, clamp ? shell_mask_ : 0ull, z0_, nzg_};
     const bool do_clamp = clamp && shell_mask_ != 0;
-    const kernels::Coef coef{w.q, w.dinv, w.cb, w.dconst, w.cconst, w.settle, static_cast<long long>(w.n) * S};
+    const kernels::Coef coef{w.q,        w.dinv, w.cb, w.dconst, w.cconst, w.settle, static_cast<long long>(w.n) * S,
+                             w.dinvT, w.cbT, w.n};
     const SweepPath p = path_[ax];
     const bool bulk = p == SweepPath::smem_bulk;
     begin_kernel(ax);
@@ -842,7 +872,8 @@ void DeviceSession::launch_ring2(int ax, bool do_clamp, const kernels::Clamp& cl
         x.ny = mesh_.ny;
         x.nz = mesh_.nz;
         x.S = S_;
-        x.planes = mesh_.nz * replicas_;
+        x.planes = mesh_.nz * batch_nr();
+        x.P0 = (rbn_ ? rb0_ : 0) * mesh_.nz;
         const int L = kernels::kLanes / S_;
         x.xi = (mesh_.ny + L - 1) / L;
         x.tiles = static_cast<long long>(x.xi) * x.planes;
@@ -865,7 +896,8 @@ void DeviceSession::launch_ring2(int ax, bool do_clamp, const kernels::Clamp& cl
     y.rowlen = rowlen;
     y.tiles_per_row = (rowlen + kernels::kLanes - 1) / kernels::kLanes;
     y.reps = replicas_;
-    y.tiles = y.tiles_per_row * y.n_outer * replicas_;
+    y.r0 = rbn_ ? rb0_ : 0;
+    y.tiles = y.tiles_per_row * y.n_outer * batch_nr();
     y.S = S_;
     y.nx = mesh_.nx;
     y.clamp = cl;
@@ -893,8 +925,10 @@ void DeviceSession::launch_xy2()
     const DeviceWorkspace& wx = ws_[0];
     const DeviceWorkspace& wy = ws_[1];
     kernels::XYFused2 a{};
-    a.xcoef = kernels::Coef{wx.q, wx.dinv, wx.cb, wx.dconst, wx.cconst, wx.settle, static_cast<long long>(wx.n) * S};
-    a.ycoef = kernels::Coef{wy.q, wy.dinv, wy.cb, wy.dconst, wy.cconst, wy.settle, static_cast<long long>(wy.n) * S};
+    a.xcoef = kernels::Coef{wx.q,     wx.dinv, wx.cb, wx.dconst, wx.cconst, wx.settle, static_cast<long long>(wx.n) * S,
+                            wx.dinvT, wx.cbT, wx.n};
+    a.ycoef = kernels::Coef{wy.q,     wy.dinv, wy.cb, wy.dconst, wy.cconst, wy.settle, static_cast<long long>(wy.n) * S,
+                            wy.dinvT, wy.cbT, wy.n};
     a.nx = mesh_.nx;
     a.ny = mesh_.ny;
     a.nz = mesh_.nz;
@@ -938,15 +972,21 @@ void DeviceSession::launch_xy2()
 
 void DeviceSession::launch_residual_dirichlet(bool all_entries)
 {
-    const std::int64_t count = all_entries ? dir_all_count_ : dir_res_count_;
+    std::int64_t count = all_entries ? dir_all_count_ : dir_res_count_;
+    std::int64_t first = 0;
+    if (!all_entries && rbn_ && !dir_res_rep_off_.empty()) { // this replica batch's entries only
+        first = dir_res_rep_off_[rb0_];
+        count = dir_res_rep_off_[rb0_ + rbn_] - first;
+    }
     if (count == 0) return;
     const long long total = count * S_;
     const int block = 256;
     begin_kernel(kDirichlet);
     kernels::dirichlet_entries<<<static_cast<unsigned>((total + block - 1) / block), block, 0,
                                  static_cast<cudaStream_t>(stream_)>>>(
-        rho_, S_, count, all_entries ? dir_all_voxel_ : dir_res_voxel_,
-        all_entries ? dir_all_mask_ : dir_res_mask_, all_entries ? dir_all_values_ : dir_res_values_);
+        rho_, S_, count, (all_entries ? dir_all_voxel_ : dir_res_voxel_) + first,
+        (all_entries ? dir_all_mask_ : dir_res_mask_) + first * S_,
+        (all_entries ? dir_all_values_ : dir_res_values_) + first * S_);
     end_kernel(kDirichlet);
 }
 
@@ -976,13 +1016,42 @@ void DeviceSession::launch_sources(double dt)
 {
     if (n_agents_ == 0) return;
     ensure_source_factors(dt);
-    const long long total = n_agents_ * S_;
+    // Groups of this replica batch (all replicas outside a batch); the grid
+    // covers the batch's agent count, an upper bound of its groups.
+    const int r0 = rbn_ ? rb0_ : 0, nr = batch_nr();
+    std::int64_t cap = n_agents_;
+    if (rbn_ && static_cast<int>(rep_agents_.size()) == replicas_) {
+        cap = 0;
+        for (int r = r0; r < r0 + nr; ++r) cap += rep_agents_[r];
+        if (cap == 0) return;
+    }
+    const long long total = cap * S_;
     const int block = 128;
     begin_kernel(kSources);
     kernels::sources_groups<<<static_cast<unsigned>((total + block - 1) / block), block, 0,
-                              static_cast<cudaStream_t>(stream_)>>>(rho_, S_, agent_counts_, group_voxel_,
-                                                                    group_offsets_, agent_add_, agent_den_);
+                              static_cast<cudaStream_t>(stream_)>>>(rho_, S_, rep_groups_ + r0, rep_groups_ + r0 + nr,
+                                                                    group_voxel_, group_offsets_, agent_add_,
+                                                                    agent_den_);
     end_kernel(kSources);
+}
+
+// Ensembles: `steps` steps as batch visits — each batch of batch_replicas_
+// replicas (sized to stay in L2) advances batch_steps_ steps before the next
+// batch starts. Replicas are independent, so this is exactly `steps`
+// whole-ensemble steps, bit for bit.
+void DeviceSession::step_body_batches(bool with_sources, double dt, std::int64_t steps)
+{
+    const int nb = batch_replicas_;
+    for (std::int64_t s0 = 0; s0 < steps; s0 += batch_steps_) {
+        const std::int64_t s1 = std::min<std::int64_t>(steps, s0 + batch_steps_);
+        for (int b = 0; b < replicas_; b += nb) {
+            rb0_ = b;
+            rbn_ = std::min(nb, replicas_ - b);
+            for (std::int64_t s = s0; s < s1; ++s) step_body(with_sources, dt);
+        }
+    }
+    rb0_ = 0;
+    rbn_ = 0;
 }
 
 void DeviceSession::sweep(Axis axis)
@@ -1044,8 +1113,17 @@ void DeviceSession::advance(std::int64_t steps, double dt, bool with_sources)
         throw state_error("advance dt does not match the solver workspace dt");
     auto st = static_cast<cudaStream_t>(stream_);
     if (with_sources) ensure_source_factors(dt); // not inside the graph capture
+    const bool batched = batch_replicas_ > 0 && !slab_ && path_[0] == SweepPath::smem_ring2 &&
+                         (!ws_[1].active || path_[1] == SweepPath::smem_ring2) &&
+                         (!ws_[2].active || path_[2] == SweepPath::smem_ring2) && !xy_fusable();
+    auto body = [&](std::int64_t n) {
+        if (batched)
+            step_body_batches(with_sources, dt, n);
+        else
+            for (std::int64_t s = 0; s < n; ++s) step_body(with_sources, dt);
+    };
     if (timing_ || slab_ || std::getenv("BIODIFF_NO_GRAPH")) {
-        for (std::int64_t s = 0; s < steps; ++s) step_body(with_sources, dt);
+        body(steps);
         return;
     }
     // Launch-bound small grids: replay a captured graph of up to kGraphSteps steps.
@@ -1059,7 +1137,7 @@ void DeviceSession::advance(std::int64_t steps, double dt, bool with_sources)
             const std::int64_t before = launches_;
             cudaGraph_t graph;
             ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
-            for (std::int64_t s = 0; s < n; ++s) step_body(with_sources, dt);
+            body(n);
             ck(cudaStreamEndCapture(st, &graph), "end capture");
             cudaGraphExec_t exec;
             ck(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");

@@ -42,6 +42,8 @@ struct DeviceWorkspace {
     double* cb = nullptr;     // [n*S]
     double* dconst = nullptr; // [S] settled denom_inv (rows settle..n-2)
     double* cconst = nullptr; // [S] settled c_back
+    double* dinvT = nullptr;  // [R][S][n] denom_inv, substrate-major (ring2 unsettled rows)
+    double* cbT = nullptr;    // [R][S][n] c_back
     int settle = 0;           // first row of the bit-constant region (n = none)
 };
 
@@ -204,6 +206,14 @@ private:
     bool ring_persist_x_ = true;   // persistent ring kernels per axis (BIODIFF_RING_PERSIST)
     bool ring_persist_yz_ = false;
     bool xy_fused_ = false;          // BIODIFF_XY_FUSED=1 (opt-in)
+    // Ensembles: replica batches that stay resident in L2 across several
+    // steps (advance). rbn_ = 0: kernels cover every replica.
+    int rb0_ = 0, rbn_ = 0;
+    int batch_replicas_ = 0;          // replicas per L2 batch (0 = no batching)
+    int batch_steps_ = 10;            // steps per batch visit
+    std::vector<std::int64_t> dir_res_rep_off_; // residual Dirichlet entries per replica (host, R+1)
+    int batch_nr() const { return rbn_ ? rbn_ : replicas_; }
+    void step_body_batches(bool with_sources, double dt, std::int64_t steps);
     unsigned* xy_ctr_ = nullptr;     // ticket + per-plane x-done counters of the fused kernel
     int xy_lag_ = 0;                 // chosen lag (planes) of the last fused launch
     int sweep_smem_bytes(int axis, bool bulk) const;
@@ -247,6 +257,8 @@ private:
     int* flags_ = nullptr;
     std::int64_t* scan_ = nullptr;
     std::int64_t* agent_counts_ = nullptr; // [0] groups, [1] grouped agents (device)
+    std::int64_t* rep_groups_ = nullptr;   // [R+1] first group of each replica (device)
+    std::vector<std::int64_t> rep_agents_; // agents per replica (host)
     unsigned long long* agent_bad_ = nullptr;
     void* cub_tmp_ = nullptr;
     std::size_t cub_bytes_ = 0;

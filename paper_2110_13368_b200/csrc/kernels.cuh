@@ -49,6 +49,9 @@ struct Coef {
     const double* cconst; // [S]
     int settle;
     long long rstride;    // ensembles: doubles between replicas' dinv/cb sets (n*S); q/dconst/cconst step S
+    const double* dinvT = nullptr; // [R][S][n]: the same bits per substrate row-contiguous (ring2:
+    const double* cbT = nullptr;   // row m0 + u of a chunk is an immediate offset from one base)
+    int n = 0;
 };
 
 __device__ __forceinline__ double fwd_first(double v, double d) { return __dmul_rn(v, d); }
@@ -73,6 +76,8 @@ struct Chain {
     int S;
     const double* dinv; // coefficient column of this lane's substrate (stride S)
     const double* cb;
+    const double* dT;   // the same column, contiguous (Coef::dinvT / cbT), or nullptr
+    const double* cT;
     double q, dc, cc;
     int settle, n;
     bool clamp_s, face;     // clamped substrate; lane's line lies on a mesh face
@@ -210,6 +215,7 @@ struct StridedSweep {
     int tiles_per_row;
     int tiles;   // tiles_per_row * n_outer * reps
     int reps;    // ensemble replicas stacked along the 4th tensor dimension (ring kernel)
+    int r0;      // first replica of this launch (ring2 replica batches), else 0
     int S;
     int nx;
     long long stride;       // (plain kernel) doubles between positions along the axis
@@ -225,6 +231,8 @@ __device__ __forceinline__ Chain make_chain(const Coef& coef, int S, int s, int 
     c.S = S;
     c.dinv = coef.dinv + r * coef.rstride + s;
     c.cb = coef.cb + r * coef.rstride + s;
+    c.dT = coef.dinvT ? coef.dinvT + (static_cast<long long>(r) * S + s) * coef.n : nullptr;
+    c.cT = coef.cbT ? coef.cbT + (static_cast<long long>(r) * S + s) * coef.n : nullptr;
     c.q = coef.q[r * S + s];
     c.dc = coef.dconst[r * S + s];
     c.cc = coef.cconst[r * S + s];
@@ -869,14 +877,17 @@ static __global__ void sources_factors(int S, long long agents, const double* vo
 // ascending-id order: x <- (x + add) / den. Agents of distinct voxels commute
 // and substrates are independent, so (group, s) threads reproduce the
 // reference's agent-outer / substrate-inner loop bitwise. Groups are in
-// (voxel) order, built on the device (agents.cu); counts[0] is the group
-// count of the last rebuild (the grid covers the agent capacity).
-static __global__ void sources_groups(double* rho, int S, const int64_t* counts, const int64_t* group_voxel,
-                               const int64_t* group_offsets, const double* add, const double* den)
+// (voxel) order, built on the device (agents.cu); [*g_lo, *g_hi) is the group
+// range to apply — all groups of the last rebuild, or one replica batch's —
+// read from device memory (the grid covers the agent capacity of the range).
+static __global__ void sources_groups(double* rho, int S, const int64_t* g_lo, const int64_t* g_hi,
+                               const int64_t* group_voxel, const int64_t* group_offsets, const double* add,
+                               const double* den)
 {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= counts[0] * S) return;
-    const long long g = t / S;
+    const long long g0 = *g_lo;
+    if (t >= (*g_hi - g0) * S) return;
+    const long long g = g0 + t / S;
     const int s = static_cast<int>(t % S);
     double* r = rho + group_voxel[g] * S + s;
     double x = *r;

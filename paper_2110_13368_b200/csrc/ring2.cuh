@@ -92,7 +92,7 @@ __device__ __forceinline__ double fwd_chunk(const Chain& c, double* sl, const La
 #pragma unroll
         for (int u = 0; u < kChunk; ++u)
             if (FULL || u < cnt) {
-                const double d = __ldg(c.dinv + (m0 + u) * c.S);
+                const double d = __ldg(c.dT + m0 + u);
                 prev = (u == 0 && first) ? fwd_first(v[u], d) : fwd(v[u], prev, c.q, d);
                 v[u] = prev;
             }
@@ -123,7 +123,7 @@ __device__ __forceinline__ double bwd_regs(const Chain& c, double (&v)[kChunk], 
     for (int u = kChunk - 1; u >= 0; --u) {
         if (!FULL && u > hi) continue;
         if (FULL && skip_top && u == kChunk - 1) continue;
-        const double b = CONSTB ? c.cc : __ldg(c.cb + (m0 + u) * c.S);
+        const double b = CONSTB ? c.cc : __ldg(c.cT + m0 + u);
         next = bwd(v[u], next, b);
         v[u] = cl_all ? c.clamp_v : next;
     }
@@ -177,7 +177,7 @@ __device__ __forceinline__ double rbwd_chunk(const Chain& c, double* sl, const L
     } else {
 #pragma unroll
         for (int u = 0; u < kChunk; ++u) {
-            const double d = __ldg(c.dinv + (m0 + u) * c.S);
+            const double d = __ldg(c.dT + m0 + u);
             fprev = (u == 0 && first) ? fwd_first(v[u], d) : fwd(v[u], fprev, c.q, d);
             v[u] = fprev;
         }
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kLanes) sweep_yz_ring2(const __grid_constant__
         TileAt d;
         d.e0 = (tile % a.tiles_per_row) * kLanes;
         const int outer_all = tile / a.tiles_per_row;
-        d.r = outer_all / a.n_outer;
+        d.r = a.r0 + outer_all / a.n_outer;
         d.outer = outer_all % a.n_outer;
         return d;
     };
@@ -449,7 +449,8 @@ __global__ void __launch_bounds__(kLanes) sweep_yz_ring2(const __grid_constant__
 struct XSweep2 {
     Coef coef;
     int nx, ny, nz, S;
-    int planes; // nz * replicas
+    int planes; // nz * replicas (of this launch's replica batch)
+    int P0;     // first plane (replica batch r0: r0 * nz)
     int xi;     // tiles per plane
     long long tiles;
     Clamp clamp;
@@ -476,7 +477,7 @@ __global__ void __launch_bounds__(kLanes) sweep_x_ring2(const __grid_constant__ 
         for (int s = 0; s < NS; ++s) ptx::mbar_init(&sm.bars[s], 1);
         ptx::fence_mbar_init();
         for (int k = 0; k < min(NS, nch); ++k)
-            issue(static_cast<int>(t / a.xi), static_cast<int>(t % a.xi) * L, k, k);
+            issue(a.P0 + static_cast<int>(t / a.xi), static_cast<int>(t % a.xi) * L, k, k);
     }
     __syncwarp();
     uint32_t parity = 0;
@@ -486,8 +487,8 @@ __global__ void __launch_bounds__(kLanes) sweep_x_ring2(const __grid_constant__ 
     const LayoutX<S> lay(l, sub);
     for (; t < a.tiles; t += G) {
         const long long tn = t + G;
-        const int P = static_cast<int>(t / a.xi), j0 = static_cast<int>(t % a.xi) * L;
-        const int Pn = static_cast<int>(tn / a.xi), j0n = static_cast<int>(tn % a.xi) * L;
+        const int P = a.P0 + static_cast<int>(t / a.xi), j0 = static_cast<int>(t % a.xi) * L;
+        const int Pn = a.P0 + static_cast<int>(tn / a.xi), j0n = static_cast<int>(tn % a.xi) * L;
         const int rep = P / a.nz, kk = P % a.nz;
         const int j = j0 + l;
         const bool active = j < a.ny;

@@ -29,13 +29,22 @@ def replicas(n, shape, S, agents, steps, clamps=0):
     return out
 
 
+# L2 replica batches (DeviceSession::step_body_batches): "0" = off; small
+# budgets force 1-2 replicas per batch and batch visits shorter than the run.
+BATCHING = [{"BIODIFF_L2_BATCH_MB": "0"}, {"BIODIFF_L2_BATCH_MB": "0.2", "BIODIFF_BATCH_STEPS": "3"},
+            {"BIODIFF_L2_BATCH_MB": "2.5", "BIODIFF_BATCH_STEPS": "4"}]
+
+
+@pytest.mark.parametrize("batching", BATCHING, ids=["off", "tiny", "small"])
 @pytest.mark.parametrize("n,shape,S,agents,steps,clamps", [
     (4, (24, 20, 18), 2, 200, 10, 3),
     (7, (32, 32, 32), 2, 300, 6, 0),
     (3, (64, 64, 64), 2, 1000, 4, 5),
     (5, (16, 12, 40), 3, 80, 8, 2),
 ])
-def test_ensemble_replicas_bitwise_equal_single_runs(n, shape, S, agents, steps, clamps):
+def test_ensemble_replicas_bitwise_equal_single_runs(n, shape, S, agents, steps, clamps, batching, monkeypatch):
+    for k, v in batching.items():
+        monkeypatch.setenv(k, v)
     ws = replicas(n, shape, S, agents, steps, clamps)
     e = ensemble_session(ws)
     e.advance(steps, ws[0].dt)
@@ -51,6 +60,32 @@ def test_ensemble_replicas_bitwise_equal_single_runs(n, shape, S, agents, steps,
         assert bits_equal(part, want), f"replica {r}: {first_diff(part, want)}"
     want0 = Oracle.run(ws[0], steps)
     assert bits_equal(got[:per], want0)
+
+
+def test_ensemble_batches_with_moving_agents(monkeypatch):
+    """Batched advance after an on-device regroup: per-replica group ranges follow the rebuild."""
+    monkeypatch.setenv("BIODIFF_L2_BATCH_MB", "0.2")
+    monkeypatch.setenv("BIODIFF_BATCH_STEPS", "2")
+    ws = replicas(6, (20, 16, 12), 2, 150, 1)
+    e = ensemble_session(ws)
+    e.advance(5, ws[0].dt)
+    rng = np.random.default_rng(3)
+    lo, hi = np.array(ws[0].bounds()[0::2]), np.array(ws[0].bounds()[1::2])
+    for w in ws:
+        w.agent_pos = np.clip(w.agent_pos + rng.normal(0, 40.0, w.agent_pos.shape), lo, hi)
+    e.set_agent_positions(np.concatenate([w.agent_pos for w in ws]))
+    e.rebuild_voxel_grouping()
+    e.advance(7, ws[0].dt)
+    got = e.download_field()
+    per = ws[0].voxels * ws[0].S
+    for r, w in enumerate(ws):
+        # replay: 5 steps at the old positions, then 7 at the new ones
+        old = w.agent_pos
+        w.agent_pos = replicas(6, (20, 16, 12), 2, 150, 1)[r].agent_pos
+        first = Oracle.run(w, 5)
+        w.agent_pos = old
+        want = Oracle.run(w, 7, field=first)
+        assert bits_equal(got[r * per:(r + 1) * per], want), f"replica {r}"
 
 
 def test_ensemble_c5_replicas_and_sharding():
