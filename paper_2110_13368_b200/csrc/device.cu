@@ -142,6 +142,7 @@ DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int devi
     ring_persist_x_ = persist != "0" && persist != "none";
     ring_persist_yz_ = persist == "1" || persist == "all";
     xy_fused_ = std::atoi(env_or("BIODIFF_XY_FUSED", "0")) != 0;
+    l2_hints_ = std::atoi(env_or("BIODIFF_L2_HINTS", "2")); // stores evict_first: C3 0.635 -> 0.629 ms; load hints slower
     if (replicas_ > 1) { // L2 replica batches (step_body_batches)
         const double replica_mb = static_cast<double>(mesh.voxel_count()) * substrates * 8.0 / 1e6;
         const double budget = std::atof(env_or("BIODIFF_L2_BATCH_MB", "0")); // opt-in: measured slower (C5 latency-bound)
@@ -874,6 +875,7 @@ void DeviceSession::launch_ring2(int ax, bool do_clamp, const kernels::Clamp& cl
         x.S = S_;
         x.planes = mesh_.nz * batch_nr();
         x.P0 = (rbn_ ? rb0_ : 0) * mesh_.nz;
+        x.hints = l2_hints_;
         const int L = kernels::kLanes / S_;
         x.xi = (mesh_.ny + L - 1) / L;
         x.tiles = static_cast<long long>(x.xi) * x.planes;
@@ -897,6 +899,7 @@ void DeviceSession::launch_ring2(int ax, bool do_clamp, const kernels::Clamp& cl
     y.tiles_per_row = (rowlen + kernels::kLanes - 1) / kernels::kLanes;
     y.reps = replicas_;
     y.r0 = rbn_ ? rb0_ : 0;
+    y.hints = l2_hints_;
     y.tiles = y.tiles_per_row * y.n_outer * batch_nr();
     y.S = S_;
     y.nx = mesh_.nx;

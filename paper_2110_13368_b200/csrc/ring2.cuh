@@ -236,7 +236,7 @@ __device__ __forceinline__ void solve_ring2(const Chain& c, bool active, uint64_
         if (k + NS < nch) { // recycle the slot for chunk k+NS (chunk k will be reloaded)
             ptx::fence_proxy_async_smem();
             __syncwarp();
-            if (lane == 0) load(0, k + NS, s);
+            if (lane == 0) load(0, k + NS, s, false);
         }
     }
     if (exp && active && exp->bottom) exp->bottom[exp->idx] = prev;
@@ -273,10 +273,10 @@ __device__ __forceinline__ void solve_ring2(const Chain& c, bool active, uint64_
             if (j < nch) {
                 if (j - NS >= 0 && j - NS <= first_reloaded) {
                     ptx::bulk_wait_read<1>();
-                    load(0, j - NS, (j - NS) % NS);
+                    load(0, j - NS, (j - NS) % NS, true);
                 } else if (j < NS && has_next()) {
                     ptx::bulk_wait_read<1>();
-                    load(1, j, j);
+                    load(1, j, j, false);
                 }
             }
         }
@@ -284,7 +284,7 @@ __device__ __forceinline__ void solve_ring2(const Chain& c, bool active, uint64_
     if (exp && active && exp->top) exp->top[exp->idx] = next;
     if (lane == 0) {
         ptx::bulk_wait_read<0>();
-        if (has_next()) load(1, 0, 0);
+        if (has_next()) load(1, 0, 0, false);
     }
     __syncwarp();
 }
@@ -308,7 +308,7 @@ __device__ __forceinline__ void solve_short2(const Chain& c, bool active, uint64
     };
     if (lane == 0 && has_next()) {
         ptx::bulk_wait_read<0>(); // the previous tile's stores out of the other set
-        for (int k = 0; k < nch; ++k) load(1, k, other + k);
+        for (int k = 0; k < nch; ++k) load(1, k, other + k, false);
     }
     __syncwarp();
     double prev = 0.0;
@@ -399,13 +399,20 @@ __global__ void __launch_bounds__(kLanes) sweep_yz_ring2(const __grid_constant__
         d.outer = outer_all % a.n_outer;
         return d;
     };
-    auto issue = [&](const TileAt& d, int k, int slot) {
+    const int nch = (a.n + kChunk - 1) / kChunk;
+    // L2 hints (a.hints bit 0): first loads of chunks the back substitution
+    // will reload stay (evict_last); reloads and the other loads stream.
+    const uint64_t keep_pol = ptx::policy_evict_last(), stream_pol = ptx::policy_evict_first();
+    auto issue = [&](const TileAt& d, int k, int slot, bool reload = false) {
         const int c1 = a.axis == 2 ? d.outer : k * kChunk;
         const int c2 = a.axis == 2 ? k * kChunk : d.outer;
         ptx::mbar_arrive_expect_tx(&sm.bars[slot], kSlot * 8);
-        ptx::tma_load_4d(sm.slots + slot * kSlot, &tmap, d.e0, c1, c2, d.r, &sm.bars[slot]);
+        if (a.hints & 1)
+            ptx::tma_load_4d_hint(sm.slots + slot * kSlot, &tmap, d.e0, c1, c2, d.r, &sm.bars[slot],
+                                  (!reload && k < nch - NS) ? keep_pol : stream_pol);
+        else
+            ptx::tma_load_4d(sm.slots + slot * kSlot, &tmap, d.e0, c1, c2, d.r, &sm.bars[slot]);
     };
-    const int nch = (a.n + kChunk - 1) / kChunk;
     if (lane == 0) {
         ptx::tma_prefetch_desc(&tmap);
         for (int s = 0; s < NS; ++s) ptx::mbar_init(&sm.bars[s], 1);
@@ -428,11 +435,14 @@ __global__ void __launch_bounds__(kLanes) sweep_yz_ring2(const __grid_constant__
         const Chain c = make_chain_yz(a, s, i, outer, r);
         const SlabExport ex{a.exp_bottom, a.exp_top, static_cast<long long>(outer) * a.rowlen + e};
         auto has_next = [&] { return tn < a.tiles; };
-        auto load = [&](int rel, int k, int slot) { issue(rel ? dn : dc, k, slot); };
+        auto load = [&](int rel, int k, int slot, bool reload) { issue(rel ? dn : dc, k, slot, reload); };
         auto store = [&](int k, int slot) {
             const int c1 = a.axis == 2 ? outer : k * kChunk;
             const int c2 = a.axis == 2 ? k * kChunk : outer;
-            ptx::tma_store_4d(&tmap, e0, c1, c2, r, sm.slots + slot * kSlot);
+            if (a.hints & 2)
+                ptx::tma_store_4d_hint(&tmap, e0, c1, c2, r, sm.slots + slot * kSlot, stream_pol);
+            else
+                ptx::tma_store_4d(&tmap, e0, c1, c2, r, sm.slots + slot * kSlot);
         };
         if constexpr (SHORT) // host guarantees 2 * nch <= NS
             solve_short2<NS, CLAMP>(c, active, sm.bars, sm.slots, kSlot, lane, parity, (it & 1) ? nch : 0, has_next,
@@ -451,6 +461,7 @@ struct XSweep2 {
     int nx, ny, nz, S;
     int planes; // nz * replicas (of this launch's replica batch)
     int P0;     // first plane (replica batch r0: r0 * nz)
+    int hints;  // L2 cache hints: bit 0 loads, bit 1 stores (BIODIFF_L2_HINTS)
     int xi;     // tiles per plane
     long long tiles;
     Clamp clamp;
@@ -467,11 +478,16 @@ __global__ void __launch_bounds__(kLanes) sweep_x_ring2(const __grid_constant__ 
     const long long G = gridDim.x;
     long long t = blockIdx.x;
     if (t >= a.tiles) return;
-    auto issue = [&](int P, int j0, int k, int slot) {
-        ptx::mbar_arrive_expect_tx(&sm.bars[slot], kSlot * 8);
-        ptx::tma_load_4d(sm.slots + slot * kSlot, &tmap, 0, j0, P, k * 2 * S, &sm.bars[slot]);
-    };
     const int nch = (a.nx + kChunk - 1) / kChunk;
+    const uint64_t keep_pol = ptx::policy_evict_last(), stream_pol = ptx::policy_evict_first();
+    auto issue = [&](int P, int j0, int k, int slot, bool reload = false) {
+        ptx::mbar_arrive_expect_tx(&sm.bars[slot], kSlot * 8);
+        if (a.hints & 1)
+            ptx::tma_load_4d_hint(sm.slots + slot * kSlot, &tmap, 0, j0, P, k * 2 * S, &sm.bars[slot],
+                                  (!reload && k < nch - NS) ? keep_pol : stream_pol);
+        else
+            ptx::tma_load_4d(sm.slots + slot * kSlot, &tmap, 0, j0, P, k * 2 * S, &sm.bars[slot]);
+    };
     if (lane == 0) {
         ptx::tma_prefetch_desc(&tmap);
         for (int s = 0; s < NS; ++s) ptx::mbar_init(&sm.bars[s], 1);
@@ -494,13 +510,18 @@ __global__ void __launch_bounds__(kLanes) sweep_x_ring2(const __grid_constant__ 
         const bool active = j < a.ny;
         const Chain c = make_chain(a.coef, S, sub, a.nx, a.clamp, j == 0 || j == a.ny - 1 || kface(kk, a.clamp), rep);
         auto has_next = [&] { return tn < a.tiles; };
-        auto load = [&](int rel, int k, int slot) {
+        auto load = [&](int rel, int k, int slot, bool reload) {
             if (rel)
                 issue(Pn, j0n, k, slot);
             else
-                issue(P, j0, k, slot);
+                issue(P, j0, k, slot, reload);
         };
-        auto store = [&](int k, int slot) { ptx::tma_store_4d(&tmap, 0, j0, P, k * 2 * S, sm.slots + slot * kSlot); };
+        auto store = [&](int k, int slot) {
+            if (a.hints & 2)
+                ptx::tma_store_4d_hint(&tmap, 0, j0, P, k * 2 * S, sm.slots + slot * kSlot, stream_pol);
+            else
+                ptx::tma_store_4d(&tmap, 0, j0, P, k * 2 * S, sm.slots + slot * kSlot);
+        };
         if constexpr (SHORT) // host guarantees 2 * nch <= NS
             solve_short2<NS, CLAMP>(c, active, sm.bars, sm.slots, kSlot, lane, parity, (it & 1) ? nch : 0, has_next,
                                     lay, load, store, nullptr);

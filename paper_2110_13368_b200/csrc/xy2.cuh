@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kLanes) sweep_xy2(const __grid_constant__ CUte
             }
             return pf;
         };
-        auto load = [&](int rel, int k, int slot) {
+        auto load = [&](int rel, int k, int slot, bool) {
             if (!rel)
                 issue(cur, k, slot);
             else if (k < min(NS, nch_of(nxt)))
