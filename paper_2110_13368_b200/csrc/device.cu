@@ -904,8 +904,10 @@ void DeviceSession::launch_ring2(int ax, bool do_clamp, const kernels::Clamp& cl
     y.S = S_;
     y.nx = mesh_.nx;
     y.clamp = cl;
-    y.exp_bottom = (slab_ && ax == 2) ? plane_bottom_ : nullptr;
-    y.exp_top = (slab_ && ax == 2) ? plane_top_ : nullptr;
+    y.exp_bottom = nullptr; // z-slabs: interface values come from zslab_interface
+    y.exp_top = nullptr;
+    y.in_lo = ax == 2 ? z_in_lo_ : nullptr;
+    y.in_hi = ax == 2 ? z_in_hi_ : nullptr;
     const int nch = (y.n + kernels::kChunk - 1) / kernels::kChunk;
     const bool short_lines = 2 * nch <= ns && (ns == 2 || ns == 4);
     const void* fn = do_clamp ? yz_ring2_pick<true>(ns, short_lines) : yz_ring2_pick<false>(ns, short_lines);

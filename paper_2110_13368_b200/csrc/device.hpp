@@ -165,12 +165,16 @@ private:
     DeviceSession* next_slab_ = nullptr;
     bool has_prev() const { return nccl_comm_ ? nccl_rank_ > 0 : prev_slab_ != nullptr; }
     bool has_next() const { return nccl_comm_ ? nccl_rank_ < nccl_ranks_ - 1 : next_slab_ != nullptr; }
-    void slab_phase_sweeps();
-    void slab_phase_fwdfix();
-    void slab_phase_topfix();
+    void slab_phase_xy();   // x, y sweeps + the interface pre-pass (dhat, xhat0)
+    void slab_phase_fwdfix(std::int64_t off, std::int64_t count);
+    void slab_phase_topfix(std::int64_t off, std::int64_t count);
+    void slab_phase_z();    // z sweep with the D_{p-1} / X_{p+1} inflows (+ shell clamp)
     void slab_phase_finish(bool with_sources, double dt);
     void slab_step_nccl(bool with_sources, double dt);
-    void nccl_exchange(double* send, int send_peer, double* recv, int recv_peer);
+    void nccl_exchange(double* send, int send_peer, double* recv, int recv_peer, std::int64_t count);
+    std::vector<std::pair<std::int64_t, std::int64_t>> plane_pieces() const; // chain pipelining
+    const double* z_in_lo_ = nullptr; // inflow planes for the next z launch (slab_phase_z)
+    const double* z_in_hi_ = nullptr;
     std::int64_t plane_count() const { return static_cast<std::int64_t>(mesh_.nx) * mesh_.ny * S_; }
     bool agent_filter_ = false; // z-slab: groups keep global voxels in [filter_lo_, filter_hi_), made local
     std::int64_t filter_lo_ = 0, filter_hi_ = 0;

@@ -83,6 +83,8 @@ struct Chain {
     bool clamp_s, face;     // clamped substrate; lane's line lies on a mesh face
     bool face_lo, face_hi;  // line positions 0 / n-1 lie on a mesh face (false at interior z-slab cuts)
     double clamp_v;
+    bool has_lo = false, has_hi = false; // z-slab inflows (ring2): row 0 continues the previous slab's
+    double lo_val = 0.0, hi_val = 0.0;   // forward recurrence, row n-1 the next slab's back substitution
 };
 
 // Forward elimination over positions [m0, m1) (m0 >= 1); position m lives
@@ -224,6 +226,8 @@ struct StridedSweep {
     Clamp clamp;
     double* exp_bottom;     // z-slab plane exports (ring kernel, z axis), or nullptr
     double* exp_top;
+    const double* in_lo = nullptr; // z-slab inflows (ring2, z axis): D_{p-1} into row 0,
+    const double* in_hi = nullptr; // X_{p+1} into the last row; nullptr at a global face
 };
 
 __device__ __forceinline__ Chain make_chain(const Coef& coef, int S, int s, int n, const Clamp& cl, bool face, int r = 0)
@@ -909,14 +913,19 @@ static __global__ void sources_groups(double* rho, int S, const int64_t* g_lo, c
 }
 
 // ---------------------------------------------------------------------------
-// z-slab partitioned solve. Slab p solved its z-lines with
-// zero inflow (x_hat). The true solution is
-//   x_m = x_hat_m + d_in * Phi_m + x_in * Psi_m
-// with d_in the forward value of the previous slab's last row, x_in the final
-// (unclamped) value of the next slab's first row, and Phi / Psi the
-// RHS-independent responses of this slab to a unit inflow at its top / bottom
-// (host-computed, per row and substrate). d_in / x_in come from the exact
-// interface recurrences below (no truncation of cross-slab couplings).
+// z-slab partitioned solve. With zero inflow at its ends a
+// slab's z-lines have forward value dhat at the last row and back-substituted
+// value xhat0 at row 0 (zslab_interface, one read of the slab). By linearity,
+// with d_in = D_{p-1} (the true forward value of the previous slab's last row)
+// and x_in = X_{p+1} (the true final value of the next slab's first row):
+//   forward value at the last row = dhat + phi_last * d_in,
+//   final value at row 0          = xhat0 + Phi_0 * d_in + Psi_0 * x_in,
+// with phi / Phi / Psi the slab's RHS-independent responses to unit inflows
+// (host-computed). The two plane chains below give every D and X exactly (no
+// truncation of cross-slab couplings); the z sweep then runs the global
+// recurrence itself on the slab with D_{p-1} / X_{p+1} as boundary values
+// (StridedSweep::in_lo / in_hi), so no correction pass over the slab is
+// needed: per step a slab moves 8 B/vsu more than a single domain, not 16.
 // ---------------------------------------------------------------------------
 
 // Exact interface recurrences (two plane chains across the slabs):
@@ -941,27 +950,33 @@ static __global__ void zslab_topfix(double* x_out, const double* xhat_top, const
     x_out[t] = __dadd_rn(__dadd_rn(xhat_top[t], __dmul_rn(Phi[s], d_in[t])), __dmul_rn(Psi[s], x_in[t]));
 }
 
-// Applies the inflow corrections to every value of the slab, skipping
-// shell-clamped voxels (their stored value is already the clamp).
-static __global__ void zslab_correct(double* rho, const double* d_in, const double* x_in, const double* phi, const double* psi,
-                              int nx, int ny, int nz_local, int S, Clamp cl)
+// Interface pre-pass of a slab, one thread per column (i, j, s), zero
+// inflow at both slab ends, ONE read of the slab:
+//   dhat  = forward value of the last row (the zero-inflow recurrence);
+//   xhat0 = back-substituted value of row 0 = sum_m (prod_{k<m} cb_k) f_m,
+// the back substitution x_m = f_m + cb_m x_{m+1} (x_{n-1} = f_{n-1}) unrolled
+// into the forward pass (all terms share the field's sign: no cancellation).
+static __global__ void zslab_interface(const double* rho, long long plane, int n, int S, const double* q,
+                                       const double* dinv, const double* cb, double* dhat, double* xhat0)
 {
-    const long long plane = static_cast<long long>(nx) * ny * S;
-    const long long total = plane * nz_local;
-    for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+    for (long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; t < plane;
          t += static_cast<long long>(gridDim.x) * blockDim.x) {
-        const long long pi = t % plane;
-        const int k = static_cast<int>(t / plane);
-        const int s = static_cast<int>(pi % S);
-        if ((cl.mask >> s) & 1ull) {
-            const long long vox = pi / S;
-            const int i = static_cast<int>(vox % nx), j = static_cast<int>(vox / nx);
-            if (i == 0 || i == nx - 1 || j == 0 || j == ny - 1 || kface(k, cl)) continue;
+        const int s = static_cast<int>(t % S);
+        const double qs = q[s];
+        double f = 0.0, acc = 0.0, prod = 1.0;
+#pragma unroll 8
+        for (int m = 0; m < n; ++m) {
+            const double v = rho[m * plane + t];
+            const double d = __ldg(dinv + static_cast<long long>(m) * S + s);
+            f = m == 0 ? fwd_first(v, d) : fwd(v, f, qs, d);
+            acc = __dadd_rn(acc, __dmul_rn(prod, f));
+            prod = __dmul_rn(prod, __ldg(cb + static_cast<long long>(m) * S + s));
         }
-        const double corr = __dadd_rn(__dmul_rn(d_in[pi], phi[k * S + s]), __dmul_rn(x_in[pi], psi[k * S + s]));
-        rho[t] = __dadd_rn(rho[t], corr);
+        dhat[t] = f;
+        xhat0[t] = acc;
     }
 }
+
 
 // DensityField::all_finite (mesh.cpp:95-99): flag = 1 if any value is NaN/inf.
 static __global__ void any_nonfinite(const double* a, long long n, int* flag)

@@ -216,7 +216,10 @@ __device__ __forceinline__ void solve_ring2(const Chain& c, bool active, uint64_
     };
     const int first_reloaded = nch - NS - 1; // chunks <= this are reloaded in the back substitution
 
-    double prev = 0.0;
+    // z-slab inflow: row 0 continues the previous slab's forward recurrence
+    // (fwd with D_{p-1} instead of fwd_first), the last row is back-substituted
+    // from X_{p+1} instead of keeping its forward value.
+    double prev = c.has_lo ? c.lo_val : 0.0;
     for (int k = 0; k < nch; ++k) {
         const int s = k % NS;
         wait_slot(s);
@@ -226,10 +229,11 @@ __device__ __forceinline__ void solve_ring2(const Chain& c, bool active, uint64_
             double* sl = slots + s * slot_doubles;
             const bool keep = k > first_reloaded;
             const bool constc = k > 0 && m0 >= c.settle && m0 + cnt <= n - 1;
+            const bool first = k == 0 && !c.has_lo;
             if (cnt == kChunk)
-                prev = fwd_chunk<true>(c, sl, lay, m0, cnt, k == 0, constc, keep, prev);
+                prev = fwd_chunk<true>(c, sl, lay, m0, cnt, first, constc, keep, prev);
             else
-                prev = fwd_chunk<false>(c, sl, lay, m0, cnt, k == 0, constc, keep, prev);
+                prev = fwd_chunk<false>(c, sl, lay, m0, cnt, first, constc, keep, prev);
             ckpt[k * kLanes + lane] = prev;
         }
         after_fwd(k);
@@ -241,7 +245,7 @@ __device__ __forceinline__ void solve_ring2(const Chain& c, bool active, uint64_
     }
     if (exp && active && exp->bottom) exp->bottom[exp->idx] = prev;
 
-    double next = prev; // final (unclamped) value of position n-1
+    double next = c.has_hi ? c.hi_val : prev; // without inflow: final (unclamped) value of position n-1
     for (int k = nch - 1; k >= 0; --k) {
         const int s = k % NS;
         const int m0 = k * kChunk;
@@ -250,12 +254,13 @@ __device__ __forceinline__ void solve_ring2(const Chain& c, bool active, uint64_
         if (k <= first_reloaded) {
             wait_slot(s);
             if (active) {
-                const double f = k > 0 ? ckpt[(k - 1) * kLanes + lane] : 0.0;
-                next = rbwd_chunk<CLAMP>(c, sl, lay, m0, k == 0, k > 0 && m0 >= c.settle, m0 >= c.settle, f, next);
+                const double f = k > 0 ? ckpt[(k - 1) * kLanes + lane] : (c.has_lo ? c.lo_val : 0.0);
+                next = rbwd_chunk<CLAMP>(c, sl, lay, m0, k == 0 && !c.has_lo, k > 0 && m0 >= c.settle,
+                                         m0 >= c.settle, f, next);
             }
         } else if (active) {
-            const bool top = k == nch - 1;
-            const bool constb = m0 >= c.settle;
+            const bool top = k == nch - 1 && !c.has_hi;
+            const bool constb = m0 >= c.settle && !(k == nch - 1 && c.has_hi); // row n-1's own c_back
             if (cnt == kChunk)
                 next = bwd_chunk<true, CLAMP>(c, sl, lay, m0, cnt, top, constb, next);
             else
@@ -311,7 +316,7 @@ __device__ __forceinline__ void solve_short2(const Chain& c, bool active, uint64
         for (int k = 0; k < nch; ++k) load(1, k, other + k, false);
     }
     __syncwarp();
-    double prev = 0.0;
+    double prev = c.has_lo ? c.lo_val : 0.0;
     for (int k = 0; k < nch; ++k) {
         wait_slot(base + k);
         const int m0 = k * kChunk;
@@ -319,21 +324,22 @@ __device__ __forceinline__ void solve_short2(const Chain& c, bool active, uint64
         if (active) {
             double* sl = slots + (base + k) * slot_doubles;
             const bool constc = k > 0 && m0 >= c.settle && m0 + cnt <= n - 1;
+            const bool first = k == 0 && !c.has_lo;
             if (cnt == kChunk)
-                prev = fwd_chunk<true>(c, sl, lay, m0, cnt, k == 0, constc, true, prev);
+                prev = fwd_chunk<true>(c, sl, lay, m0, cnt, first, constc, true, prev);
             else
-                prev = fwd_chunk<false>(c, sl, lay, m0, cnt, k == 0, constc, true, prev);
+                prev = fwd_chunk<false>(c, sl, lay, m0, cnt, first, constc, true, prev);
         }
     }
     if (exp && active && exp->bottom) exp->bottom[exp->idx] = prev;
-    double next = prev;
+    double next = c.has_hi ? c.hi_val : prev;
     for (int k = nch - 1; k >= 0; --k) {
         const int m0 = k * kChunk;
         const int cnt = min(kChunk, n - m0);
         if (active) {
             double* sl = slots + (base + k) * slot_doubles;
-            const bool top = k == nch - 1;
-            const bool constb = m0 >= c.settle;
+            const bool top = k == nch - 1 && !c.has_hi;
+            const bool constb = m0 >= c.settle && !(k == nch - 1 && c.has_hi);
             if (cnt == kChunk)
                 next = bwd_chunk<true, CLAMP>(c, sl, lay, m0, cnt, top, constb, next);
             else
@@ -432,8 +438,17 @@ __global__ void __launch_bounds__(kLanes) sweep_yz_ring2(const __grid_constant__
         const bool active = lane < width;
         const int e = e0 + (active ? lane : 0);
         const int s = e % a.S, i = e / a.S;
-        const Chain c = make_chain_yz(a, s, i, outer, r);
-        const SlabExport ex{a.exp_bottom, a.exp_top, static_cast<long long>(outer) * a.rowlen + e};
+        Chain c = make_chain_yz(a, s, i, outer, r);
+        const long long pidx = static_cast<long long>(outer) * a.rowlen + e; // column's index in a z plane
+        if (a.in_lo) {
+            c.has_lo = true;
+            c.lo_val = a.in_lo[pidx];
+        }
+        if (a.in_hi) {
+            c.has_hi = true;
+            c.hi_val = a.in_hi[pidx];
+        }
+        const SlabExport ex{a.exp_bottom, a.exp_top, pidx};
         auto has_next = [&] { return tn < a.tiles; };
         auto load = [&](int rel, int k, int slot, bool reload) { issue(rel ? dn : dc, k, slot, reload); };
         auto store = [&](int k, int slot) {

@@ -1,21 +1,22 @@
 // z-slab decomposition of the LOD step across GPUs.
 //
-// Slab p owns global planes [z0, z1). The x and y sweeps are local. The z
-// sweep runs with zero inflow on the slab using the GLOBAL factorisation rows
-// (so it is exactly the reference's recurrence except for the two missing
-// inflow terms), exporting the zero-inflow forward value of its last row
-// (dhat) and the unclamped back-substituted value of its first row (xhat_0).
-// By linearity the true solution is
-//   x_m = xhat_m + D_{p-1} * Phi_m + X_{p+1} * Psi_m
-// where D_{p-1} is the true forward value of the previous slab's last row and
-// X_{p+1} the true final value of the next slab's first row; Phi / Psi are
-// the slab's responses to unit inflows (host-precomputed, RHS-independent).
-// D and X follow exactly from two plane recurrences across the slabs:
+// Slab p owns global planes [z0, z1) and the GLOBAL factorisation rows of
+// its planes. The x and y sweeps are local. One read of the slab
+// (zslab_interface) gives, with zero inflow at its ends, the forward value of
+// its last row (dhat) and the back-substituted value of its first row
+// (xhat_0). D_{p-1} (the true forward value of the previous slab's last row)
+// and X_{p+1} (the true final value of the next slab's first row) then follow
+// exactly from two plane recurrences across the slabs (phi / Phi / Psi: the
+// slab's host-precomputed responses to unit inflows):
 //   forward : D_p = dhat_p + phi_p(last row) * D_{p-1}           p -> p+1
 //   backward: X_p = xhat_0,p + Phi_p(0) * D_{p-1} + Psi_p(0) * X_{p+1}   p -> p-1
+// Finally the z sweep runs the global recurrence on the slab with D_{p-1} as
+// the inflow into row 0 and X_{p+1} into the last row — no correction pass.
 // No coupling is truncated, so there is no minimum slab thickness; the result
-// differs from the single-domain solve only by rounding. Per step each
-// interface moves two nx*ny*S planes (33.6 MB at 1024^2 x 4).
+// differs from the single-domain solve only by rounding (the interface values
+// are formed in a different order). Per step a slab reads its field once more
+// (8 B/vsu) than a single domain, and each interface moves two nx*ny*S planes
+// (33.6 MB at 1024^2 x 4), pipelined in pieces.
 // Transports: NCCL send/recv on the session stream (one slab per rank, the
 // multi-GPU path) or device/peer copies between sessions of one process.
 #include "device.hpp"
@@ -111,8 +112,8 @@ void DeviceSession::configure_slab(int nz_global, int z0)
         ck(cudaMemsetAsync(*p, 0, bytes, static_cast<cudaStream_t>(stream_)), "cudaMemset plane");
     }
     choose_paths();
-    if (nz_global > 1 && !is_ring(path_[2]))
-        throw config_error("z-slab needs the TMA ring z-sweep (rows with an even number of doubles)");
+    if (nz_global > 1 && path_[2] != SweepPath::smem_ring2)
+        throw config_error("z-slab needs the ring2 z-sweep (rows with an even number of doubles)");
 }
 
 bool DeviceSession::is_boundary_local(int i, int j, int k_local) const
@@ -164,17 +165,34 @@ void DeviceSession::connect_nccl(const unsigned char* unique_id, int nranks, int
     nccl_ranks_ = nranks;
 }
 
-void DeviceSession::nccl_exchange(double* send, int send_peer, double* recv, int recv_peer)
+void DeviceSession::nccl_exchange(double* send, int send_peer, double* recv, int recv_peer, std::int64_t count)
 {
     if (!send && !recv) return;
     NcclApi& a = nccl();
     auto comm = static_cast<ncclComm_t>(nccl_comm_);
     auto st = static_cast<cudaStream_t>(stream_);
-    const size_t count = static_cast<size_t>(plane_count());
     nck(a.GroupStart(), "ncclGroupStart");
-    if (send) nck(a.Send(send, count, ncclFloat64, send_peer, comm, st), "ncclSend");
-    if (recv) nck(a.Recv(recv, count, ncclFloat64, recv_peer, comm, st), "ncclRecv");
+    if (send) nck(a.Send(send, static_cast<size_t>(count), ncclFloat64, send_peer, comm, st), "ncclSend");
+    if (recv) nck(a.Recv(recv, static_cast<size_t>(count), ncclFloat64, recv_peer, comm, st), "ncclRecv");
     nck(a.GroupEnd(), "ncclGroupEnd");
+}
+
+// The interface chains are serial over slabs; splitting each plane into
+// pieces (whole columns of S values, >= 1 MB) pipelines them: slab p+1 works
+// on piece 1 while piece 2 of slab p is still in flight.
+std::vector<std::pair<std::int64_t, std::int64_t>> DeviceSession::plane_pieces() const
+{
+    const std::int64_t plane = plane_count();
+    int want = std::max(1, std::atoi(std::getenv("BIODIFF_ZSLAB_PIECES") ? std::getenv("BIODIFF_ZSLAB_PIECES") : "8"));
+    const std::int64_t min_piece = (1 << 20) / 8;
+    want = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(want, plane / min_piece)));
+    std::vector<std::pair<std::int64_t, std::int64_t>> pieces;
+    const std::int64_t cols = plane / S_;
+    for (int i = 0; i < want; ++i) {
+        const std::int64_t c0 = cols * i / want, c1 = cols * (i + 1) / want;
+        if (c1 > c0) pieces.push_back({c0 * S_, (c1 - c0) * S_});
+    }
+    return pieces;
 }
 
 void DeviceSession::link_local(const std::vector<DeviceSession*>& slabs)
@@ -189,70 +207,89 @@ void DeviceSession::link_local(const std::vector<DeviceSession*>& slabs)
     }
 }
 
-void DeviceSession::slab_phase_sweeps()
+// x, y sweeps (local), then one read of the slab for its interface values
+// with zero inflow: dhat -> plane_bottom_, xhat0 -> plane_top_.
+void DeviceSession::slab_phase_xy()
 {
     check_ready(Axis::x);
-    if (ws_[2].active) {
-        launch_xy_sweeps();
-        launch_sweep(Axis::z, true);
-    } else {
+    if (!ws_[2].active) {
         launch_sweep(Axis::x, false);
         if (ws_[1].active) launch_sweep(Axis::y, false);
+        return;
     }
+    launch_xy_sweeps();
+    if (!has_prev() && !has_next()) return;
+    const DeviceWorkspace& w = ws_[2];
+    const long long plane = plane_count();
+    begin_kernel(kAux);
+    kernels::zslab_interface<<<sm_count_ * 8, 256, 0, static_cast<cudaStream_t>(stream_)>>>(
+        rho_, plane, mesh_.nz, S_, w.q, w.dinv, w.cb, plane_bottom_, plane_top_);
+    end_kernel(kAux);
 }
 
 // D_p = dhat_p + phi_last * D_{p-1} (needed only when a next slab exists).
-void DeviceSession::slab_phase_fwdfix()
+void DeviceSession::slab_phase_fwdfix(std::int64_t off, std::int64_t count)
 {
     if (!has_next()) return;
     if (!slab_philast_) throw state_error("z-slab spikes not set");
-    const long long plane = plane_count();
     const int block = 256;
     begin_kernel(kAux);
-    kernels::zslab_fwdfix<<<static_cast<unsigned>((plane + block - 1) / block), block, 0,
-                            static_cast<cudaStream_t>(stream_)>>>(plane_dout_, plane_bottom_, plane_din_,
-                                                                  slab_philast_, plane, S_);
+    kernels::zslab_fwdfix<<<static_cast<unsigned>((count + block - 1) / block), block, 0,
+                            static_cast<cudaStream_t>(stream_)>>>(plane_dout_ + off, plane_bottom_ + off,
+                                                                  plane_din_ + off, slab_philast_, count, S_);
     end_kernel(kAux);
 }
 
-// X_p = xhat_top + Phi_0 * D_{p-1} + Psi_0 * X_{p+1} (needed only when a previous slab exists).
-void DeviceSession::slab_phase_topfix()
+// X_p = xhat0 + Phi_0 * D_{p-1} + Psi_0 * X_{p+1} (needed only when a previous slab exists).
+void DeviceSession::slab_phase_topfix(std::int64_t off, std::int64_t count)
 {
     if (!has_prev()) return;
     if (!slab_phi_) throw state_error("z-slab spikes not set");
-    const long long plane = plane_count();
     const int block = 256;
     begin_kernel(kAux);
-    kernels::zslab_topfix<<<static_cast<unsigned>((plane + block - 1) / block), block, 0,
-                            static_cast<cudaStream_t>(stream_)>>>(plane_xtop_, plane_top_, plane_din_, plane_xin_,
-                                                                  slab_phi_, slab_psi_, plane, S_);
+    kernels::zslab_topfix<<<static_cast<unsigned>((count + block - 1) / block), block, 0,
+                            static_cast<cudaStream_t>(stream_)>>>(plane_xtop_ + off, plane_top_ + off,
+                                                                  plane_din_ + off, plane_xin_ + off, slab_phi_,
+                                                                  slab_psi_, count, S_);
     end_kernel(kAux);
+}
+
+// The global recurrence on the slab: row 0 continues from D_{p-1}, the last
+// row is back-substituted from X_{p+1}; the shell clamp is fused as usual.
+void DeviceSession::slab_phase_z()
+{
+    if (!ws_[2].active) return;
+    if (path_[2] != SweepPath::smem_ring2) throw state_error("z-slab inflows need the ring2 z-sweep");
+    z_in_lo_ = has_prev() ? plane_din_ : nullptr;
+    z_in_hi_ = has_next() ? plane_xin_ : nullptr;
+    launch_sweep(Axis::z, true);
+    z_in_lo_ = nullptr;
+    z_in_hi_ = nullptr;
 }
 
 void DeviceSession::slab_phase_finish(bool with_sources, double dt)
 {
-    if (has_prev() || has_next()) {
-        if (!slab_phi_) throw state_error("z-slab spikes not set");
-        kernels::Clamp cl{shell_values_, shell_mask_, z0_, nzg_};
-        begin_kernel(kAux);
-        kernels::zslab_correct<<<sm_count_ * 8, 256, 0, static_cast<cudaStream_t>(stream_)>>>(
-            rho_, plane_din_, plane_xin_, slab_phi_, slab_psi_, mesh_.nx, mesh_.ny, mesh_.nz, S_, cl);
-        end_kernel(kAux);
-    }
     launch_residual_dirichlet(false);
     if (with_sources) launch_sources(dt);
 }
 
-// One slab per rank: the two plane chains run on this stream through NCCL.
+// One slab per rank: the two plane chains run on this stream through NCCL,
+// pipelined over plane pieces.
 void DeviceSession::slab_step_nccl(bool with_sources, double dt)
 {
-    slab_phase_sweeps();
-    nccl_exchange(nullptr, 0, has_prev() ? plane_din_ : nullptr, nccl_rank_ - 1); // D_{p-1}
-    slab_phase_fwdfix();
-    nccl_exchange(has_next() ? plane_dout_ : nullptr, nccl_rank_ + 1, nullptr, 0); // D_p
-    nccl_exchange(nullptr, 0, has_next() ? plane_xin_ : nullptr, nccl_rank_ + 1); // X_{p+1}
-    slab_phase_topfix();
-    nccl_exchange(has_prev() ? plane_xtop_ : nullptr, nccl_rank_ - 1, nullptr, 0); // X_p
+    slab_phase_xy();
+    const auto pieces = plane_pieces();
+    for (const auto& [off, cnt] : pieces) { // forward chain D_0 -> D_{P-1}
+        nccl_exchange(nullptr, 0, has_prev() ? plane_din_ + off : nullptr, nccl_rank_ - 1, cnt);
+        slab_phase_fwdfix(off, cnt);
+        nccl_exchange(has_next() ? plane_dout_ + off : nullptr, nccl_rank_ + 1, nullptr, 0, cnt);
+    }
+    for (const auto& [off, cnt] : pieces) { // backward chain X_{P-1} -> X_0
+        nccl_exchange(nullptr, 0, has_next() ? plane_xin_ + off : nullptr, nccl_rank_ + 1, cnt);
+        slab_phase_topfix(off, cnt);
+        nccl_exchange(has_prev() ? plane_xtop_ + off : nullptr, nccl_rank_ - 1, nullptr, 0, cnt);
+    }
+    slab_phase_z();
     slab_phase_finish(with_sources, dt);
 }
 
@@ -280,7 +317,7 @@ void DeviceSession::group_advance(const std::vector<DeviceSession*>& slabs, std:
     for (std::int64_t step = 0; step < steps; ++step) {
         for (std::size_t p = 0; p < P; ++p) {
             on(p);
-            slabs[p]->slab_phase_sweeps();
+            slabs[p]->slab_phase_xy();
         }
         for (std::size_t p = 0; p < P; ++p) { // forward chain D_0 -> D_{P-1}
             on(p);
@@ -290,7 +327,7 @@ void DeviceSession::group_advance(const std::vector<DeviceSession*>& slabs, std:
                                        slabs[p - 1]->device_, bytes(p), stream(p)),
                    "copy D");
             }
-            slabs[p]->slab_phase_fwdfix();
+            slabs[p]->slab_phase_fwdfix(0, slabs[p]->plane_count());
             mark(p);
         }
         for (std::size_t pp = P; pp-- > 0;) { // backward chain X_{P-1} -> X_0
@@ -301,15 +338,16 @@ void DeviceSession::group_advance(const std::vector<DeviceSession*>& slabs, std:
                                        slabs[pp + 1]->device_, bytes(pp), stream(pp)),
                    "copy X");
             }
-            slabs[pp]->slab_phase_topfix();
+            slabs[pp]->slab_phase_topfix(0, slabs[pp]->plane_count());
             mark(pp);
         }
         for (std::size_t p = 0; p < P; ++p) {
             on(p);
+            slabs[p]->slab_phase_z();
             slabs[p]->slab_phase_finish(with_sources, dt);
             mark(p);
         }
-        for (std::size_t p = 0; p < P; ++p) { // next sweeps overwrite planes the neighbours read
+        for (std::size_t p = 0; p < P; ++p) { // next pre-pass overwrites planes the neighbours read
             on(p);
             for (std::size_t q : {p - 1, p + 1})
                 if (q < P) wait_on(p, q);

@@ -1,10 +1,11 @@
 """CPU, multi-process: the z-slab decomposition protocol of csrc/slab.cu,
 restated with the oracle's line solver, run by world_size-2 (and 3) gloo
 process groups that exchange the interface planes with torch.distributed
-send/recv exactly in the order the NCCL path does:
+send/recv exactly in the order the NCCL path does (pieces of the planes):
+    x, y sweeps ; interface pre-pass: dhat, xhat_0 with zero inflow (one read)
     recv D_{p-1} <- p-1 ; D_p = dhat_p + phi_last * D_{p-1} ; send D_p -> p+1
     recv X_{p+1} <- p+1 ; X_p = xhat_0 + Phi_0 D_{p-1} + Psi_0 X_{p+1} ; send X_p -> p-1
-    x += D_{p-1} Phi_m + X_{p+1} Psi_m ; Dirichlet ; sources
+    z solve with inflows D_{p-1} (row 0) and X_{p+1} (last row) ; Dirichlet ; sources
 The gathered result must match the single-domain oracle run to rounding."""
 import os
 import socket
@@ -49,6 +50,35 @@ def spikes(q, dinv, cb, n, S):
     return Phi, psi, phi[n - 1].copy()
 
 
+def interface(r3, q, d, c, S):
+    """zslab_interface: dhat (last-row forward) and xhat_0 = sum_m prod_{k<m} cb_k f_m, zero inflow."""
+    n, plane = r3.shape
+    s = np.arange(plane) % S
+    f = np.zeros(plane)
+    acc = np.zeros(plane)
+    prod = np.ones(plane)
+    for m in range(n):
+        f = r3[m] * d[m, s] if m == 0 else (r3[m] + q[s] * f) * d[m, s]
+        acc = acc + prod * f
+        prod = prod * c[m, s]
+    return f, acc
+
+
+def z_solve_inflow(r3, q, d, c, S, d_in, x_in):
+    """The global z recurrence on the slab: row 0 continues from d_in, the last row takes x_in."""
+    n, plane = r3.shape
+    s = np.arange(plane) % S
+    f = np.empty_like(r3)
+    for m in range(n):
+        prev = (d_in if d_in is not None else None) if m == 0 else f[m - 1]
+        f[m] = r3[m] * d[m, s] if (m == 0 and d_in is None) else (r3[m] + q[s] * prev) * d[m, s]
+    x = f[n - 1] + c[n - 1, s] * x_in if x_in is not None else f[n - 1]
+    r3[n - 1] = x
+    for m in range(n - 2, -1, -1):
+        x = f[m] + c[m, s] * x
+        r3[m] = x
+
+
 def _rank_main(rank, world, port, w, steps, out_path):
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     nx, ny, nz = w.n
@@ -82,22 +112,32 @@ def _rank_main(rank, world, port, w, steps, out_path):
     for _ in range(steps):
         Oracle.sweep(rho, shape, S, 0, ws[0])
         Oracle.sweep(rho, shape, S, 1, ws[1])
-        Oracle.sweep(rho, shape, S, 2, (qz, dz.ravel(), cz.ravel()))
-        dhat = rho[(n - 1) * plane:].copy()   # last row: forward value == final (no inflow)
-        xhat0 = rho[:plane].copy()
+        r3 = rho.reshape(n, plane)
+        dhat, xhat0 = interface(r3, qz, dz, cz, S)
         d_in = torch.zeros(plane, dtype=torch.float64)
         x_in = torch.zeros(plane, dtype=torch.float64)
-        if rank > 0:
-            dist.recv(d_in, src=rank - 1)
-        if rank < world - 1:
-            dout = dhat + np.tile(phi_last, nx * ny) * d_in.numpy()
-            dist.send(torch.from_numpy(dout), dst=rank + 1)
-            dist.recv(x_in, src=rank + 1)
-        if rank > 0:
-            xout = xhat0 + np.tile(Phi[0], nx * ny) * d_in.numpy() + np.tile(psi[0], nx * ny) * x_in.numpy()
-            dist.send(torch.from_numpy(xout), dst=rank - 1)
-        r3 = rho.reshape(n, plane)
-        r3 += np.tile(Phi, (1, nx * ny)) * d_in.numpy()[None, :] + np.tile(psi, (1, nx * ny)) * x_in.numpy()[None, :]
+        pieces = np.array_split(np.arange(plane // S), 3)  # whole columns, as DeviceSession::plane_pieces
+        for pc in pieces:  # forward chain, piece by piece
+            sl = slice(pc[0] * S, (pc[-1] + 1) * S)
+            if rank > 0:
+                buf = torch.zeros(sl.stop - sl.start, dtype=torch.float64)
+                dist.recv(buf, src=rank - 1)
+                d_in[sl] = buf
+            if rank < world - 1:
+                dout = dhat[sl] + np.tile(phi_last, pc.size) * d_in[sl].numpy()
+                dist.send(torch.from_numpy(dout), dst=rank + 1)
+        for pc in pieces:  # backward chain
+            sl = slice(pc[0] * S, (pc[-1] + 1) * S)
+            if rank < world - 1:
+                buf = torch.zeros(sl.stop - sl.start, dtype=torch.float64)
+                dist.recv(buf, src=rank + 1)
+                x_in[sl] = buf
+            if rank > 0:
+                xout = (xhat0[sl] + np.tile(Phi[0], pc.size) * d_in[sl].numpy()
+                        + np.tile(psi[0], pc.size) * x_in[sl].numpy())
+                dist.send(torch.from_numpy(xout), dst=rank - 1)
+        z_solve_inflow(r3, qz, dz, cz, S, d_in.numpy() if rank > 0 else None,
+                       x_in.numpy() if rank < world - 1 else None)
         Oracle.dirichlet(rho, S, dv, dm, dx_)
         if lgv.size:
             Oracle.sources(rho, S, (lgv, lgo, lorder), w.agent_vol, w.agent_sec, w.agent_upt, w.agent_sat,
