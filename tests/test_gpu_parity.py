@@ -311,3 +311,29 @@ def test_fused_xy_step_bitwise(shape, S, env, monkeypatch):
     if env.get("BIODIFF_XY_FUSED") != "1":
         assert t["sweep_xy"][0] == 0
     s.close()
+
+
+def _random_cases(n, seed=2024):
+    rng = np.random.default_rng(seed)
+    cases = []
+    for k in range(n):
+        shape = tuple(int(x) for x in rng.choice([1, 2, 3, 5, 16, 31, 32, 33, 63, 64, 65, 96, 97, 130], size=3))
+        if max(shape) == 1:
+            shape = (33, 2, 1)
+        S = int(rng.choice([1, 2, 3, 4, 5, 8]))
+        cases.append((shape, S, int(rng.integers(0, 400)), int(rng.integers(1, 9)), int(rng.integers(0, 6)), k))
+    return cases
+
+
+@pytest.mark.parametrize("shape,S,agents,steps,clamps,k", _random_cases(48))
+def test_random_shapes_bitwise(shape, S, agents, steps, clamps, k):
+    """Randomised shapes around the chunk (32) and tile boundaries, 1-D / 2-D /
+    3-D, substrate counts with and without the swizzled x path, agents and
+    interior clamps: full steps bit-identical to the oracle."""
+    w = W.make("rand", shape, S, agents, steps, seed=100 + k, interior_clamps=clamps, immune_fraction=0.3)
+    s = make_session(w)
+    s.advance(steps, w.dt, with_sources=True)
+    got = s.download_field()
+    want = Oracle.run(w, steps)
+    assert bits_equal(got, want), first_diff(got, want)
+    s.close()
