@@ -5,6 +5,7 @@
 #include "ring.cuh"
 #include "ring2.cuh"
 #include "xy2.cuh"
+#include "xyc.cuh"
 
 #include <cuda_runtime.h>
 
@@ -141,7 +142,8 @@ DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int devi
     const std::string persist = env_or("BIODIFF_RING_PERSIST", "x");
     ring_persist_x_ = persist != "0" && persist != "none";
     ring_persist_yz_ = persist == "1" || persist == "all";
-    xy_fused_ = std::atoi(env_or("BIODIFF_XY_FUSED", "0")) != 0;
+    xy_mode_ = std::atoi(env_or("BIODIFF_XY_FUSED", "0"));
+    xy_fused_ = xy_mode_ != 0;
     l2_hints_ = std::atoi(env_or("BIODIFF_L2_HINTS", "2")); // stores evict_first: C3 0.635 -> 0.629 ms; load hints slower
     if (replicas_ > 1) { // L2 replica batches (step_body_batches)
         const double replica_mb = static_cast<double>(mesh.voxel_count()) * substrates * 8.0 / 1e6;
@@ -751,6 +753,79 @@ bool DeviceSession::xy_fusable() const
 namespace {
 
 template <int NS>
+const void* xyc_pick_s(int S)
+{
+    if (S == 1) return reinterpret_cast<const void*>(kernels::sweep_xy_cluster<NS, 1>);
+    if (S == 2) return reinterpret_cast<const void*>(kernels::sweep_xy_cluster<NS, 2>);
+    return reinterpret_cast<const void*>(kernels::sweep_xy_cluster<NS, 4>);
+}
+
+} // namespace
+
+// x+y of each plane by one thread-block cluster through L2 (xyc.cuh).
+void DeviceSession::launch_xy_cluster()
+{
+    auto st = static_cast<cudaStream_t>(stream_);
+    const int S = S_;
+    const DeviceWorkspace& wx = ws_[0];
+    const DeviceWorkspace& wy = ws_[1];
+    kernels::XYCluster a{};
+    a.xcoef = kernels::Coef{wx.q,     wx.dinv, wx.cb, wx.dconst, wx.cconst, wx.settle, static_cast<long long>(wx.n) * S,
+                            wx.dinvT, wx.cbT, wx.n};
+    a.nx = mesh_.nx;
+    a.ny = mesh_.ny;
+    a.nz = mesh_.nz;
+    a.S = S;
+    a.rowlen = mesh_.nx * S;
+    a.planes = mesh_.nz * replicas_;
+    const int L = kernels::kLanes / S;
+    a.xi = (mesh_.ny + L - 1) / L;
+    a.yi = (a.rowlen + kernels::kLanes - 1) / kernels::kLanes;
+    kernels::StridedSweep& y = a.y;
+    y.coef = kernels::Coef{wy.q,     wy.dinv, wy.cb, wy.dconst, wy.cconst, wy.settle, static_cast<long long>(wy.n) * S,
+                           wy.dinvT, wy.cbT, wy.n};
+    y.axis = 1;
+    y.n = mesh_.ny;
+    y.n_outer = mesh_.nz;
+    y.rowlen = a.rowlen;
+    y.S = S;
+    y.nx = mesh_.nx;
+    y.clamp = kernels::Clamp{shell_values_, 0ull, z0_, nzg_};
+    const int ns = std::max(2, std::min(3, std::atoi(env_or("BIODIFF_XYC_SLOTS", "3"))));
+    const int wpc = std::max(1, std::min(8, std::atoi(env_or("BIODIFF_XYC_WARPS", "8"))));
+    const int cl = std::max(1, std::min(8, std::atoi(env_or("BIODIFF_XYC_CLUSTER", "4"))));
+    const int nch = (std::max(mesh_.nx * S / (2 * S) * 2 / 2, mesh_.ny) + kernels::kChunk - 1) / kernels::kChunk;
+    const int nchx = (mesh_.nx + kernels::kChunk - 1) / kernels::kChunk;
+    const int nchm = std::max(nch, nchx);
+    a.warp_bytes = ((ns * kernels::kChunk * kernels::kLanes * 8 + 128 + nchm * kernels::kLanes * 8 + 1023) / 1024) * 1024;
+    const int smem = 1024 + wpc * a.warp_bytes;
+    const void* fn = ns == 2 ? xyc_pick_s<2>(S) : xyc_pick_s<3>(S);
+    ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
+    cudaLaunchConfig_t cfg{};
+    cfg.blockDim = dim3(32 * wpc);
+    cfg.dynamicSmemBytes = static_cast<std::size_t>(smem);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(cl);
+    int max_clusters = 0;
+    ck(cudaOccupancyMaxActiveClusters(&max_clusters, fn, &cfg), "max active clusters");
+    const int clusters = std::max(1, std::min(max_clusters, a.planes));
+    cfg.gridDim = dim3(clusters * cl);
+    begin_kernel(kSweepXY);
+    void* args[] = {tmap_[0], tmap_[1], &a};
+    ck(cudaLaunchKernelExC(&cfg, fn, args), "launch xy cluster");
+    end_kernel(kSweepXY);
+}
+
+namespace {
+
+template <int NS>
 const void* xy2_pick_s(int S)
 {
     if (S == 1) return reinterpret_cast<const void*>(kernels::sweep_xy2<NS, 1>);
@@ -792,7 +867,10 @@ void DeviceSession::launch_xy_sweeps()
         if (ws_[1].active) launch_sweep(Axis::y, false);
         return;
     }
-    launch_xy2();
+    if (xy_mode_ == 2)
+        launch_xy_cluster();
+    else
+        launch_xy2();
 }
 
 namespace {

@@ -209,7 +209,9 @@ private:
     int sm_count_ = 148;
     bool ring_persist_x_ = true;   // persistent ring kernels per axis (BIODIFF_RING_PERSIST)
     bool ring_persist_yz_ = false;
-    bool xy_fused_ = false;          // BIODIFF_XY_FUSED=1 (opt-in)
+    bool xy_fused_ = false;          // BIODIFF_XY_FUSED=1 (lagged tickets) / 2 (plane clusters)
+    int xy_mode_ = 0;
+    void launch_xy_cluster();
     int l2_hints_ = 0;               // ring2 L2 cache hints, BIODIFF_L2_HINTS bitmask (1 loads, 2 stores)
     // Ensembles: replica batches that stay resident in L2 across several
     // steps (advance). rbn_ = 0: kernels cover every replica.

@@ -288,10 +288,13 @@ FUSED_ENVS = [
     {"BIODIFF_XY_FUSED": "1", "BIODIFF_XY_LAG": "1000000"},                     # all x items, then all y items
     {"BIODIFF_XY_FUSED": "1", "BIODIFF_XY_CTAS_PER_SM": "1", "BIODIFF_XY_LAG": "2"},  # few CTAs, many items each
     {"BIODIFF_XY_FUSED": "1", "BIODIFF_XY_SLOTS": "2"},                         # two-slot ring
+    {"BIODIFF_XY_FUSED": "2"},                                                  # plane clusters (xyc.cuh)
+    {"BIODIFF_XY_FUSED": "2", "BIODIFF_XYC_CLUSTER": "2", "BIODIFF_XYC_WARPS": "3", "BIODIFF_XYC_SLOTS": "2"},
 ]
 
 
-@pytest.mark.parametrize("env", FUSED_ENVS, ids=["unfused", "fused", "lag1", "lagmax", "1cta", "slots2"])
+@pytest.mark.parametrize("env", FUSED_ENVS, ids=["unfused", "fused", "lag1", "lagmax", "1cta", "slots2", "cluster",
+                                                 "cluster2x3"])
 @pytest.mark.parametrize("shape,S", SWEEP_SHAPES)
 def test_fused_xy_step_bitwise(shape, S, env, monkeypatch):
     """The fused x+y kernel (ticketed items, per-plane release/acquire
@@ -308,7 +311,7 @@ def test_fused_xy_step_bitwise(shape, S, env, monkeypatch):
     s.diffuse_decay_step()
     t = s.kernel_times()
     assert t["sweep_xy"][0] + t["sweep_x"][0] == 1
-    if env.get("BIODIFF_XY_FUSED") != "1":
+    if env.get("BIODIFF_XY_FUSED") not in ("1", "2"):
         assert t["sweep_xy"][0] == 0
     s.close()
 
