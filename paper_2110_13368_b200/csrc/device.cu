@@ -142,8 +142,15 @@ DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int devi
     const std::string persist = env_or("BIODIFF_RING_PERSIST", "x");
     ring_persist_x_ = persist != "0" && persist != "none";
     ring_persist_yz_ = persist == "1" || persist == "all";
-    xy_mode_ = std::atoi(env_or("BIODIFF_XY_FUSED", "0"));
-    xy_fused_ = xy_mode_ != 0;
+    // x+y fusion: BIODIFF_XY_FUSED = 0 off, 1 lagged tickets (xy2.cuh), 2
+    // plane clusters (xyc.cuh); default "auto" = plane clusters where they
+    // pay (xy_cluster_pays(): enough items per plane, the planes of all
+    // clusters fit in L2), else off.
+    {
+        const std::string m = env_or("BIODIFF_XY_FUSED", "auto");
+        xy_mode_ = m == "auto" ? -1 : std::atoi(m.c_str());
+        xy_fused_ = xy_mode_ != 0;
+    }
     l2_hints_ = std::atoi(env_or("BIODIFF_L2_HINTS", "2")); // stores evict_first: C3 0.635 -> 0.629 ms; load hints slower
     if (replicas_ > 1) { // L2 replica batches (step_body_batches)
         const double replica_mb = static_cast<double>(mesh.voxel_count()) * substrates * 8.0 / 1e6;
@@ -747,7 +754,23 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
 
 bool DeviceSession::xy_fusable() const
 {
-    return xy_fused_ && ws_[1].active && path_[0] == SweepPath::smem_ring2 && path_[1] == SweepPath::smem_ring2;
+    if (!(xy_fused_ && ws_[1].active && path_[0] == SweepPath::smem_ring2 && path_[1] == SweepPath::smem_ring2))
+        return false;
+    return xy_mode_ != -1 || xy_cluster_pays();
+}
+
+// Plane clusters pay off when each of a cluster's 32 warps has an x and a y
+// item per plane (C3: 32 + 32 items) and the planes the ~37 clusters hold at
+// once stay in L2 (C3: 37 x 2 MB; C4's 32 MB planes would not).
+bool DeviceSession::xy_cluster_pays() const
+{
+    if (replicas_ > 1 || !ws_[2].active) return false;
+    const int L = kernels::kLanes / S_;
+    const int xi = (mesh_.ny + L - 1) / L;
+    const int yi = (mesh_.nx * S_ + kernels::kLanes - 1) / kernels::kLanes;
+    const double plane_mb = static_cast<double>(mesh_.nx) * mesh_.ny * S_ * 8.0 / 1e6;
+    const double clusters = std::min(static_cast<double>(mesh_.nz), sm_count_ / 4.0);
+    return xi >= 16 && yi >= 16 && plane_mb * clusters <= 80.0;
 }
 
 namespace {
@@ -867,10 +890,10 @@ void DeviceSession::launch_xy_sweeps()
         if (ws_[1].active) launch_sweep(Axis::y, false);
         return;
     }
-    if (xy_mode_ == 2)
-        launch_xy_cluster();
-    else
+    if (xy_mode_ == 1)
         launch_xy2();
+    else
+        launch_xy_cluster();
 }
 
 namespace {

@@ -212,6 +212,7 @@ private:
     bool xy_fused_ = false;          // BIODIFF_XY_FUSED=1 (lagged tickets) / 2 (plane clusters)
     int xy_mode_ = 0;
     void launch_xy_cluster();
+    bool xy_cluster_pays() const;
     int l2_hints_ = 0;               // ring2 L2 cache hints, BIODIFF_L2_HINTS bitmask (1 loads, 2 stores)
     // Ensembles: replica batches that stay resident in L2 across several
     // steps (advance). rbn_ = 0: kernels cover every replica.

@@ -59,80 +59,98 @@ __device__ __forceinline__ void cluster_sync()
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// One x item (lines j0 .. j0+L-1 of plane P). The item's first min(NS, nch) chunks are issued here unless the previous
-// item prefetched them (`prefetched`).
+// Layout of either item kind in one form (so the cluster kernel holds ONE
+// copy of the ring2 chunk code): off(u) = row + t[u % P] + (u / P) * L * 16.
+//   x item: LayoutX<S> (swizzled rows of 16 doubles);
+//   y item: [position][lane] = lane + 32 u, i.e. row = lane, t[j] = 32 j
+//           (P * 32 = 16 * L doubles per piece step).
+template <int S>
+struct LayoutU {
+    static constexpr int L = kLanes / S;
+    static constexpr int P = 16 / S;
+    int row;
+    int t[P];
+    __device__ __forceinline__ void set_x(int l, int s)
+    {
+        const LayoutX<S> x(l, s);
+        row = x.row;
+#pragma unroll
+        for (int j = 0; j < P; ++j) t[j] = x.t[j];
+    }
+    __device__ __forceinline__ void set_y(int lane)
+    {
+        row = lane;
+#pragma unroll
+        for (int j = 0; j < P; ++j) t[j] = 32 * j;
+    }
+    __device__ __forceinline__ int off(int u) const { return row + t[u % P] + (u / P) * (L * 16); }
+};
+
+// One item of either kind. x: lines j0 = it*L .. of plane P; y: columns
+// e0 = it*32 .. of plane P. Issues its first chunks unless prefetched; a y
+// item prefetches the warp's next x item (plane Pn, item itn >= 0) into the
+// slots it frees. Returns whether it did.
 template <int NS, int S>
-__device__ __forceinline__ void xyc_x_item(const CUtensorMap* tmap_x, const XYCluster& a, const Ring2Smem& sm,
-                                        uint32_t& parity, int P, int it, bool prefetched)
+__device__ __forceinline__ bool xyc_item(const CUtensorMap* tmap_x, const CUtensorMap* tmap_y, const XYCluster& a,
+                                         const Ring2Smem& sm, uint32_t& parity, bool is_x, int P, int it,
+                                         bool prefetched, int Pn, int itn)
 {
     constexpr int kSlot = kChunk * kLanes;
     constexpr int L = kLanes / S;
     const int lane = threadIdx.x & 31;
     const int nchx = (a.nx + kChunk - 1) / kChunk;
-    const int j0 = it * L;
-    auto issue = [&](int k, int slot) {
+    const int nchy = (a.ny + kChunk - 1) / kChunk;
+    const int nch = is_x ? nchx : nchy;
+    const int rep = P / a.nz, kk = P % a.nz;
+    auto issue_x = [&](int Pq, int itq, int k, int slot) {
         ptx::mbar_arrive_expect_tx(&sm.bars[slot], kSlot * 8);
-        ptx::tma_load_4d(sm.slots + slot * kSlot, tmap_x, 0, j0, P, k * 2 * S, &sm.bars[slot]);
+        ptx::tma_load_4d(sm.slots + slot * kSlot, tmap_x, 0, itq * L, Pq, k * 2 * S, &sm.bars[slot]);
+    };
+    auto issue_y = [&](int k, int slot) {
+        ptx::mbar_arrive_expect_tx(&sm.bars[slot], kSlot * 8);
+        ptx::tma_load_4d(sm.slots + slot * kSlot, tmap_y, it * kLanes, k * kChunk, kk, rep, &sm.bars[slot]);
+    };
+    auto issue = [&](int k, int slot) {
+        if (is_x)
+            issue_x(P, it, k, slot);
+        else
+            issue_y(k, slot);
     };
     if (lane == 0 && !prefetched)
-        for (int k = 0; k < min(NS, nchx); ++k) issue(k, k);
+        for (int k = 0; k < min(NS, nch); ++k) issue(k, k);
     __syncwarp();
-    int xl, xs;
-    x_lane<S>(lane, xl, xs);
-    const LayoutX<S> lay(xl, xs);
-    Clamp none{nullptr, 0ull, 0, a.nz};
-    const Chain c = make_chain(a.xcoef, S, xs, a.nx, none, false, P / a.nz);
-    solve_ring2<NS, false>(
-        c, j0 + xl < a.ny, sm.bars, sm.slots, kSlot, sm.ckpt, lane, parity, [] { return false; }, lay,
-        [&](int, int k, int slot, bool) { issue(k, slot); },
-        [&](int k, int slot) {
-            ptx::tma_store_4d_hint(tmap_x, 0, j0, P, k * 2 * S, sm.slots + slot * kSlot, ptx::policy_evict_last());
-        },
-        nullptr);
-}
-
-// One y item (columns e0 .. e0+31 of plane P). While its slots drain it
-// prefetches the warp's next x item (plane Pn, item itn; itn < 0: none),
-// whose data does not depend on anything still running.
-template <int NS, int S>
-__device__ __forceinline__ bool xyc_y_item(const CUtensorMap* tmap_y, const CUtensorMap* tmap_x, const XYCluster& a,
-                                        const Ring2Smem& sm, uint32_t& parity, int P, int it, int Pn, int itn)
-{
-    constexpr int kSlot = kChunk * kLanes;
-    constexpr int L = kLanes / S;
-    const int lane = threadIdx.x & 31;
-    const int nchy = (a.ny + kChunk - 1) / kChunk;
-    const int nchx = (a.nx + kChunk - 1) / kChunk;
-    const int rep = P / a.nz, kk = P % a.nz;
-    const int e0 = it * kLanes;
-    auto issue = [&](int k, int slot) {
-        ptx::mbar_arrive_expect_tx(&sm.bars[slot], kSlot * 8);
-        ptx::tma_load_4d(sm.slots + slot * kSlot, tmap_y, e0, k * kChunk, kk, rep, &sm.bars[slot]);
-    };
-    if (lane == 0)
-        for (int k = 0; k < min(NS, nchy); ++k) issue(k, k);
-    __syncwarp();
-    const int width = min(kLanes, a.rowlen - e0);
-    const bool active = lane < width;
-    const int e = e0 + (active ? lane : 0);
-    const Chain c = make_chain_yz(a.y, e % S, e / S, kk, rep);
-    const LayoutYZ lay{lane};
-    // Next x item's chunk j goes to slot j (j < min(NS, nch_y)) as the y
-    // item's slots free up; only when both items have the same chunk count
-    // limits (else the x item issues its own loads).
-    const bool pf = itn >= 0 && min(NS, nchx) <= min(NS, nchy);
+    LayoutU<S> lay;
+    Chain c;
+    bool active;
+    if (is_x) {
+        int xl, xs;
+        x_lane<S>(lane, xl, xs);
+        lay.set_x(xl, xs);
+        Clamp none{nullptr, 0ull, 0, a.nz};
+        c = make_chain(a.xcoef, S, xs, a.nx, none, false, rep);
+        active = it * L + xl < a.ny;
+    } else {
+        lay.set_y(lane);
+        const int e0 = it * kLanes;
+        active = lane < min(kLanes, a.rowlen - e0);
+        const int e = e0 + (active ? lane : 0);
+        c = make_chain_yz(a.y, e % S, e / S, kk, rep);
+    }
+    const bool pf = !is_x && itn >= 0 && min(NS, nchx) <= min(NS, nchy);
+    const uint64_t pol = is_x ? ptx::policy_evict_last() : ptx::policy_evict_first();
     solve_ring2<NS, false>(
         c, active, sm.bars, sm.slots, kSlot, sm.ckpt, lane, parity, [&] { return pf; }, lay,
         [&](int rel, int k, int slot, bool) {
-            if (!rel) {
+            if (!rel)
                 issue(k, slot);
-            } else if (k < min(NS, nchx)) {
-                ptx::mbar_arrive_expect_tx(&sm.bars[slot], kSlot * 8);
-                ptx::tma_load_4d(sm.slots + slot * kSlot, tmap_x, 0, itn * L, Pn, k * 2 * S, &sm.bars[slot]);
-            }
+            else if (k < min(NS, nchx))
+                issue_x(Pn, itn, k, slot);
         },
         [&](int k, int slot) {
-            ptx::tma_store_4d_hint(tmap_y, e0, k * kChunk, kk, rep, sm.slots + slot * kSlot, ptx::policy_evict_first());
+            if (is_x)
+                ptx::tma_store_4d_hint(tmap_x, 0, it * L, P, k * 2 * S, sm.slots + slot * kSlot, pol);
+            else
+                ptx::tma_store_4d_hint(tmap_y, it * kLanes, k * kChunk, kk, rep, sm.slots + slot * kSlot, pol);
         },
         nullptr);
     return pf;
@@ -167,27 +185,34 @@ __global__ void __launch_bounds__(256) sweep_xy_cluster(const __grid_constant__ 
     const int P0 = static_cast<int>(cluster_id_x()), dP = static_cast<int>(ncluster_x());
     bool prefetched = false;
     for (int P = P0; P < a.planes; P += dP) {
-        // ---- x phase: this warp's x items of plane P ----------------------
-        for (int it = gw; it < a.xi; it += nw) {
-            xyc_x_item<NS, S>(&tmap_x, a, sm, parity, P, it, prefetched && it == gw);
-            prefetched = false;
-        }
-        // The plane's x results must be complete and visible before any warp
-        // of the cluster reads them through TMA.
-        if (lane == 0) {
-            ptx::bulk_wait_all();
-            ptx::fence_proxy_async_global();
-        }
-        __syncwarp();
-        cluster_sync();
-        if (lane == 0) ptx::fence_proxy_async_global();
-        __syncwarp();
-        // ---- y phase; the last y item prefetches the next plane's first x item
         const int Pn = P + dP;
         const int itn = (Pn < a.planes && gw < a.xi) ? gw : -1;
-        for (int it = gw; it < a.yi; it += nw) {
-            const bool last = it + nw >= a.yi;
-            prefetched = xyc_y_item<NS, S>(&tmap_y, &tmap_x, a, sm, parity, P, it, Pn, last ? itn : -1);
+        // Phase 0: this warp's x items of plane P; phase 1: its y items (the
+        // last one prefetches the next plane's first x item). One loop, one
+        // copy of the chunk code.
+#pragma unroll 1
+        for (int ph = 0; ph < 2; ++ph) {
+            if (ph == 1) {
+                // The plane's x results must be complete and visible before
+                // any warp of the cluster reads them through TMA.
+                if (lane == 0) {
+                    ptx::bulk_wait_all();
+                    ptx::fence_proxy_async_global();
+                }
+                __syncwarp();
+                cluster_sync();
+                if (lane == 0) ptx::fence_proxy_async_global();
+                __syncwarp();
+            }
+            const bool is_x = ph == 0;
+            const int items = is_x ? a.xi : a.yi;
+#pragma unroll 1
+            for (int it = gw; it < items; it += nw) {
+                const bool last_y = !is_x && it + nw >= items;
+                const bool pf = xyc_item<NS, S>(&tmap_x, &tmap_y, a, sm, parity, is_x, P, it,
+                                                is_x && prefetched && it == gw, Pn, last_y ? itn : -1);
+                prefetched = is_x ? false : pf;
+            }
         }
     }
     if (lane == 0) ptx::bulk_wait_all();
