@@ -355,6 +355,9 @@ void DeviceSession::set_workspace(Axis axis, int n, int dims, double dt, const d
         cc.insert(cc.end(), ccr.begin(), ccr.end());
     }
     if (std::getenv("BIODIFF_NO_SETTLE")) w.settle = n;
+#ifdef BIODIFF_DIAG_SETTLE1
+    w.settle = 1; // design probe only: wrong results, unsettled-row cost removed
+#endif
     w.dconst = dalloc_copy(dc.data(), dc.size(), st);
     w.cconst = dalloc_copy(cc.data(), cc.size(), st);
     {   // Substrate-major copies (same bits) for ring2's unsettled rows.
@@ -1382,3 +1385,11 @@ void cell_sources_sinks_step(DensityField& field, const AgentPopulation& agents,
 }
 
 } // namespace biodiff_b200
+
+#ifdef BIODIFF_XYC_TRACE
+// Design probe (variant builds only): copies the plane-cluster phase stamps.
+extern "C" int biodiff_debug_xyc_trace(unsigned long long* out, long long n)
+{
+    return static_cast<int>(cudaMemcpyFromSymbol(out, biodiff_b200::kernels::g_xyc_trace, n * 8));
+}
+#endif

@@ -85,6 +85,7 @@ struct Chain {
     double clamp_v;
     bool has_lo = false, has_hi = false; // z-slab inflows (ring2): row 0 continues the previous slab's
     double lo_val = 0.0, hi_val = 0.0;   // forward recurrence, row n-1 the next slab's back substitution
+    int s = 0, ts = 0;                   // substrate; stride between substrate columns of dT / cT
 };
 
 // Forward elimination over positions [m0, m1) (m0 >= 1); position m lives
@@ -243,6 +244,8 @@ __device__ __forceinline__ Chain make_chain(const Coef& coef, int S, int s, int 
     c.cc = coef.cconst[r * S + s];
     c.settle = coef.settle;
     c.n = n;
+    c.s = s;
+    c.ts = coef.n;
     c.clamp_s = (cl.mask >> s) & 1ull;
     c.clamp_v = c.clamp_s ? cl.values[s] : 0.0;
     c.face = face;

@@ -71,11 +71,15 @@ __device__ __forceinline__ void x_lane(int lane, int& l, int& s)
 
 // Forward elimination over positions u < cnt of one chunk (line positions
 // m0 + u). `first`: position 0 of the line (fwd_first). `constc`: every row
-// of the chunk is in the settled region. `keep`: store the forward values
+// of the chunk is in the settled region. `lastc`: the line's last chunk with
+// every row but n-1 settled — row n-1 uses `dlast` (= dT[n-1], loaded before
+// the chunk's wait), so the chunk needs no per-row coefficient loads (ncu:
+// chunks that load them ran ~2.3x slower). `keep`: store the forward values
 // (chunks that stay resident for the back substitution).
 template <bool FULL, class Lay>
 __device__ __forceinline__ double fwd_chunk(const Chain& c, double* sl, const Lay& lay, int m0, int cnt, bool first,
-                                            bool constc, bool keep, double prev)
+                                            bool constc, bool keep, double prev, bool lastc = false,
+                                            double dlast = 0.0)
 {
     double v[kChunk];
 #pragma unroll
@@ -86,6 +90,13 @@ __device__ __forceinline__ double fwd_chunk(const Chain& c, double* sl, const La
         for (int u = 0; u < kChunk; ++u)
             if (FULL || u < cnt) {
                 prev = fwd(v[u], prev, c.q, c.dc);
+                v[u] = prev;
+            }
+    } else if (lastc) {
+#pragma unroll
+        for (int u = 0; u < kChunk; ++u)
+            if (FULL || u < cnt) {
+                prev = fwd(v[u], prev, c.q, (FULL ? u == kChunk - 1 : u == cnt - 1) ? dlast : c.dc);
                 v[u] = prev;
             }
     } else {
@@ -222,18 +233,20 @@ __device__ __forceinline__ void solve_ring2(const Chain& c, bool active, uint64_
     double prev = c.has_lo ? c.lo_val : 0.0;
     for (int k = 0; k < nch; ++k) {
         const int s = k % NS;
-        wait_slot(s);
         const int m0 = k * kChunk;
         const int cnt = min(kChunk, n - m0);
+        const bool constc = k > 0 && m0 >= c.settle && m0 + cnt <= n - 1;
+        const bool lastc = k > 0 && m0 >= c.settle && m0 + cnt == n;
+        const double dlast = lastc && active ? __ldg(c.dT + n - 1) : 0.0;
+        wait_slot(s);
         if (active) {
             double* sl = slots + s * slot_doubles;
             const bool keep = k > first_reloaded;
-            const bool constc = k > 0 && m0 >= c.settle && m0 + cnt <= n - 1;
             const bool first = k == 0 && !c.has_lo;
             if (cnt == kChunk)
-                prev = fwd_chunk<true>(c, sl, lay, m0, cnt, first, constc, keep, prev);
+                prev = fwd_chunk<true>(c, sl, lay, m0, cnt, first, constc, keep, prev, lastc, dlast);
             else
-                prev = fwd_chunk<false>(c, sl, lay, m0, cnt, first, constc, keep, prev);
+                prev = fwd_chunk<false>(c, sl, lay, m0, cnt, first, constc, keep, prev, lastc, dlast);
             ckpt[k * kLanes + lane] = prev;
         }
         after_fwd(k);
@@ -318,17 +331,19 @@ __device__ __forceinline__ void solve_short2(const Chain& c, bool active, uint64
     __syncwarp();
     double prev = c.has_lo ? c.lo_val : 0.0;
     for (int k = 0; k < nch; ++k) {
-        wait_slot(base + k);
         const int m0 = k * kChunk;
         const int cnt = min(kChunk, n - m0);
+        const bool constc = k > 0 && m0 >= c.settle && m0 + cnt <= n - 1;
+        const bool lastc = k > 0 && m0 >= c.settle && m0 + cnt == n;
+        const double dlast = lastc && active ? __ldg(c.dT + n - 1) : 0.0;
+        wait_slot(base + k);
         if (active) {
             double* sl = slots + (base + k) * slot_doubles;
-            const bool constc = k > 0 && m0 >= c.settle && m0 + cnt <= n - 1;
             const bool first = k == 0 && !c.has_lo;
             if (cnt == kChunk)
-                prev = fwd_chunk<true>(c, sl, lay, m0, cnt, first, constc, true, prev);
+                prev = fwd_chunk<true>(c, sl, lay, m0, cnt, first, constc, true, prev, lastc, dlast);
             else
-                prev = fwd_chunk<false>(c, sl, lay, m0, cnt, first, constc, true, prev);
+                prev = fwd_chunk<false>(c, sl, lay, m0, cnt, first, constc, true, prev, lastc, dlast);
         }
     }
     if (exp && active && exp->bottom) exp->bottom[exp->idx] = prev;

@@ -156,6 +156,22 @@ __device__ __forceinline__ bool xyc_item(const CUtensorMap* tmap_x, const CUtens
     return pf;
 }
 
+#ifdef BIODIFF_XYC_TRACE
+// Design probe (variant builds only): per (plane, cluster warp) globaltimer
+// stamps at x start, x end, after the cluster barrier, y end.
+__device__ unsigned long long g_xyc_trace[4096 * 32 * 4];
+__device__ __forceinline__ unsigned long long xyc_now()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define XYC_STAMP(P, gw, i)                                                                                            \
+    if (lane == 0 && (P) < 4096 && (gw) < 32) g_xyc_trace[((P) * 32 + (gw)) * 4 + (i)] = xyc_now();
+#else
+#define XYC_STAMP(P, gw, i)
+#endif
+
 template <int NS, int S>
 __global__ void __launch_bounds__(256) sweep_xy_cluster(const __grid_constant__ CUtensorMap tmap_x,
                                                         const __grid_constant__ CUtensorMap tmap_y, XYCluster a)
@@ -192,6 +208,7 @@ __global__ void __launch_bounds__(256) sweep_xy_cluster(const __grid_constant__ 
         // copy of the chunk code.
 #pragma unroll 1
         for (int ph = 0; ph < 2; ++ph) {
+            XYC_STAMP(P, gw, ph == 0 ? 0 : 1)
             if (ph == 1) {
                 // The plane's x results must be complete and visible before
                 // any warp of the cluster reads them through TMA.
@@ -203,6 +220,7 @@ __global__ void __launch_bounds__(256) sweep_xy_cluster(const __grid_constant__ 
                 cluster_sync();
                 if (lane == 0) ptx::fence_proxy_async_global();
                 __syncwarp();
+                XYC_STAMP(P, gw, 2)
             }
             const bool is_x = ph == 0;
             const int items = is_x ? a.xi : a.yi;
@@ -214,6 +232,7 @@ __global__ void __launch_bounds__(256) sweep_xy_cluster(const __grid_constant__ 
                 prefetched = is_x ? false : pf;
             }
         }
+        XYC_STAMP(P, gw, 3)
     }
     if (lane == 0) ptx::bulk_wait_all();
 }
