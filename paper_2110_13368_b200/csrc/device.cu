@@ -818,8 +818,13 @@ void DeviceSession::launch_xy_cluster()
     y.nx = mesh_.nx;
     y.clamp = kernels::Clamp{shell_values_, 0ull, z0_, nzg_};
     const int ns = std::max(2, std::min(3, std::atoi(env_or("BIODIFF_XYC_SLOTS", "3"))));
-    const int wpc = std::max(1, std::min(8, std::atoi(env_or("BIODIFF_XYC_WARPS", "8"))));
-    const int cl = std::max(1, std::min(8, std::atoi(env_or("BIODIFF_XYC_CLUSTER", "4"))));
+    // 8 CTAs x 4 warps per cluster (32 warps: one x and one y item each at
+    // C3), two CTAs of DIFFERENT clusters per SM: their plane phases and
+    // barriers drift apart, so one cluster's x (DRAM) phase overlaps the
+    // other's y (L2) phase — 388 -> 378 us vs 4 CTAs x 8 warps (one CTA per
+    // SM); 2 x 16 and 1 x 16 (non-portable sizes) measured 410 / 409 us.
+    const int wpc = std::max(1, std::min(8, std::atoi(env_or("BIODIFF_XYC_WARPS", "4"))));
+    const int cl = std::max(1, std::min(16, std::atoi(env_or("BIODIFF_XYC_CLUSTER", "8"))));
     const int nch = (std::max(mesh_.nx * S / (2 * S) * 2 / 2, mesh_.ny) + kernels::kChunk - 1) / kernels::kChunk;
     const int nchx = (mesh_.nx + kernels::kChunk - 1) / kernels::kChunk;
     const int nchm = std::max(nch, nchx);
@@ -827,6 +832,7 @@ void DeviceSession::launch_xy_cluster()
     const int smem = 1024 + wpc * a.warp_bytes;
     const void* fn = ns == 2 ? xyc_pick_s<2>(S) : xyc_pick_s<3>(S);
     ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
+    if (cl > 8) ck(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1), "cluster 16");
     cudaLaunchConfig_t cfg{};
     cfg.blockDim = dim3(32 * wpc);
     cfg.dynamicSmemBytes = static_cast<std::size_t>(smem);

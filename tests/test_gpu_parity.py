@@ -290,11 +290,13 @@ FUSED_ENVS = [
     {"BIODIFF_XY_FUSED": "1", "BIODIFF_XY_SLOTS": "2"},                         # two-slot ring
     {"BIODIFF_XY_FUSED": "2"},                                                  # plane clusters (xyc.cuh)
     {"BIODIFF_XY_FUSED": "2", "BIODIFF_XYC_CLUSTER": "2", "BIODIFF_XYC_WARPS": "3", "BIODIFF_XYC_SLOTS": "2"},
+    {"BIODIFF_XY_FUSED": "2", "BIODIFF_XYC_CLUSTER": "4", "BIODIFF_XYC_WARPS": "8"},   # one CTA per SM
+    {"BIODIFF_XY_FUSED": "2", "BIODIFF_XYC_CLUSTER": "16", "BIODIFF_XYC_WARPS": "1"},  # non-portable cluster size
 ]
 
 
 @pytest.mark.parametrize("env", FUSED_ENVS, ids=["unfused", "fused", "lag1", "lagmax", "1cta", "slots2", "cluster",
-                                                 "cluster2x3"])
+                                                 "cluster2x3", "cluster4x8", "cluster16x1"])
 @pytest.mark.parametrize("shape,S", SWEEP_SHAPES)
 def test_fused_xy_step_bitwise(shape, S, env, monkeypatch):
     """The fused x+y kernel (ticketed items, per-plane release/acquire
