@@ -182,6 +182,7 @@ DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int devi
     // Ticket + per-plane counters of the fused x+y kernel (allocated here:
     // launches may be captured into graphs).
     ck(cudaMalloc(&xy_ctr_, sizeof(unsigned) * (1 + static_cast<std::size_t>(mesh.nz) * replicas_)), "cudaMalloc");
+    ck(cudaMalloc(&xyc_ctr_, sizeof(unsigned)), "cudaMalloc");
 }
 
 DeviceSession::~DeviceSession()
@@ -205,6 +206,7 @@ DeviceSession::~DeviceSession()
     dfree(dir_res_values_);
     dfree(shell_values_);
     dfree(xy_ctr_);
+    dfree(xyc_ctr_);
     release_agents();
     release_slab();
     for (auto& pe : pending_events_) {
@@ -828,6 +830,14 @@ void DeviceSession::launch_xy_cluster()
     const int nch = (std::max(mesh_.nx * S / (2 * S) * 2 / 2, mesh_.ny) + kernels::kChunk - 1) / kernels::kChunk;
     const int nchx = (mesh_.nx + kernels::kChunk - 1) / kernels::kChunk;
     const int nchm = std::max(nch, nchx);
+    // Odd clusters start ~half an x item later (~50 ns per x position): the
+    // two clusters sharing an SM then keep their DRAM-fed x phases and
+    // L2-fed y phases apart instead of starting in lockstep. C3: 381 -> 363
+    // us (0 / 9 / 12 / 15 us: 381 / 366 / 363 / 363; 3-8 groups no better).
+    a.stagger_ns = std::atoi(env_or("BIODIFF_XYC_STAGGER_NS", std::to_string(50 * mesh_.nx).c_str()));
+    a.stagger_groups = std::atoi(env_or("BIODIFF_XYC_STAGGER_GROUPS", "2"));
+    a.plane_ctr = std::atoi(env_or("BIODIFF_XYC_DYNAMIC", "1")) ? xyc_ctr_ : nullptr;
+    if (a.plane_ctr) ck(cudaMemsetAsync(xyc_ctr_, 0, sizeof(unsigned), st), "memset plane counter");
     a.warp_bytes = ((ns * kernels::kChunk * kernels::kLanes * 8 + 128 + nchm * kernels::kLanes * 8 + 1023) / 1024) * 1024;
     const int smem = 1024 + wpc * a.warp_bytes;
     const void* fn = ns == 2 ? xyc_pick_s<2>(S) : xyc_pick_s<3>(S);

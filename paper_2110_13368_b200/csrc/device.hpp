@@ -223,6 +223,7 @@ private:
     int batch_nr() const { return rbn_ ? rbn_ : replicas_; }
     void step_body_batches(bool with_sources, double dt, std::int64_t steps);
     unsigned* xy_ctr_ = nullptr;     // ticket + per-plane x-done counters of the fused kernel
+    unsigned* xyc_ctr_ = nullptr;    // plane counter of the plane-cluster kernel
     int xy_lag_ = 0;                 // chosen lag (planes) of the last fused launch
     int sweep_smem_bytes(int axis, bool bulk) const;
     int ring_slots(int axis) const;

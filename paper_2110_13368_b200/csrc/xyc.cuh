@@ -28,6 +28,9 @@ struct XYCluster {
     int xi, yi;      // x / y items per plane
     int rowlen;
     int warp_bytes;  // shared memory per warp (1024-aligned)
+    int stagger_ns;  // cluster c starts (c % stagger_groups) * stagger_ns later (phase offset; 0 = off)
+    int stagger_groups;
+    unsigned* plane_ctr; // dynamic plane scheduling (zeroed before the launch), or nullptr: static P += clusters
 };
 
 __device__ __forceinline__ uint32_t cluster_ctarank()
@@ -53,6 +56,15 @@ __device__ __forceinline__ uint32_t cluster_nctarank()
     uint32_t r;
     asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
     return r;
+}
+// Reads an int from the shared memory of CTA `rank` of this cluster (DSMEM).
+__device__ __forceinline__ int ld_cluster_int(const int* p, uint32_t rank)
+{
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(ptx::smem_addr(p)), "r"(rank));
+    int v;
+    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(r) : "memory");
+    return v;
 }
 __device__ __forceinline__ void cluster_sync()
 {
@@ -156,6 +168,13 @@ __device__ __forceinline__ bool xyc_item(const CUtensorMap* tmap_x, const CUtens
     return pf;
 }
 
+__device__ __forceinline__ unsigned long long xyc_clock()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 #ifdef BIODIFF_XYC_TRACE
 // Design probe (variant builds only): per (plane, cluster warp) globaltimer
 // stamps at x start, x end, after the cluster barrier, y end.
@@ -199,10 +218,23 @@ __global__ void __launch_bounds__(256) sweep_xy_cluster(const __grid_constant__ 
     __syncwarp();
     uint32_t parity = 0;
     const int P0 = static_cast<int>(cluster_id_x()), dP = static_cast<int>(ncluster_x());
+    if (a.stagger_ns > 0 && a.stagger_groups > 1 && P0 % a.stagger_groups) {
+        const unsigned long long wait = static_cast<unsigned long long>(a.stagger_ns) * (P0 % a.stagger_groups);
+        const unsigned long long t0 = xyc_clock();
+        while (xyc_clock() - t0 < wait) __nanosleep(1000);
+    }
+    // Plane scheduling: the first plane is the cluster's index; with
+    // a.plane_ctr the cluster's leader thread fetches the next one from a
+    // global counter during the x phase and publishes it in its shared memory
+    // (double-buffered by round), read by every warp after the x/y barrier —
+    // clusters that started late (stagger) or ran slow take fewer planes.
+    __shared__ int s_next[2];
+    const bool leader = cluster_ctarank() == 0 && threadIdx.x == 0;
     bool prefetched = false;
-    for (int P = P0; P < a.planes; P += dP) {
-        const int Pn = P + dP;
-        const int itn = (Pn < a.planes && gw < a.xi) ? gw : -1;
+    int round = 0;
+    for (int P = P0; P < a.planes; ++round) {
+        int Pn = P + dP, itn = -1;
+        if (a.plane_ctr && leader) s_next[round & 1] = dP + static_cast<int>(atomicAdd(a.plane_ctr, 1u));
         // Phase 0: this warp's x items of plane P; phase 1: its y items (the
         // last one prefetches the next plane's first x item). One loop, one
         // copy of the chunk code.
@@ -219,6 +251,12 @@ __global__ void __launch_bounds__(256) sweep_xy_cluster(const __grid_constant__ 
                 __syncwarp();
                 cluster_sync();
                 if (lane == 0) ptx::fence_proxy_async_global();
+                if (a.plane_ctr) {
+                    int v = 0;
+                    if (lane == 0) v = ld_cluster_int(&s_next[round & 1], 0);
+                    Pn = __shfl_sync(0xffffffffu, v, 0);
+                }
+                itn = (Pn < a.planes && gw < a.xi) ? gw : -1;
                 __syncwarp();
                 XYC_STAMP(P, gw, 2)
             }
@@ -233,6 +271,7 @@ __global__ void __launch_bounds__(256) sweep_xy_cluster(const __grid_constant__ 
             }
         }
         XYC_STAMP(P, gw, 3)
+        P = Pn;
     }
     if (lane == 0) ptx::bulk_wait_all();
 }
