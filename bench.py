@@ -36,7 +36,9 @@ METRIC = "voxel-substrate diffusion updates/sec (FP64) at 1/2/4/8 B200; % of HBM
 UNIT = "vsu/s"
 BYTES_PER_VSU_STEP = 48  # 3 sweeps x (8 B read + 8 B write), SURVEY.md §8 d2
 BYTES_PER_VSU_STEP_FUSED = 32  # DRAM bytes when x+y run fused through L2 (one read + one write) + z
-BYTES_PER_VSU_SWEEP = 16  # per value per sweep (a fused x+y launch performs two)
+BYTES_PER_VSU_STEP_XYZ = 16  # ensembles: x, y, z of a replica fused through L2 (one read + one write)
+BYTES_PER_VSU_SWEEP = 16  # per value per sweep (a fused x+y launch performs two, x+y+z three)
+SWEEPS_PER_LAUNCH = {"sweep_xyz": 3, "sweep_xy": 2, "sweep_x": 1, "sweep_y": 1, "sweep_z": 1}
 
 
 def peaks():
@@ -270,8 +272,9 @@ def main():
 
     # Roofline of the dominant kernel (largest share of the timed region).
     peak, peak_src = peaks()
-    sweep_classes = [c for c in ("sweep_xy", "sweep_x", "sweep_y", "sweep_z") if ktimes[c][0]]
+    sweep_classes = [c for c in ("sweep_xyz", "sweep_xy", "sweep_x", "sweep_y", "sweep_z") if ktimes[c][0]]
     fused = ktimes["sweep_xy"][0] > 0
+    fused3 = ktimes["sweep_xyz"][0] > 0
     # 16 B per value per sweep, 48 B/vsu per step. A fused
     # x+y launch performs two sweeps (32 B/value algorithmic); its DRAM
     # traffic (ncu, "traffic") is one read + one write — the fusion's gain.
@@ -279,7 +282,7 @@ def main():
     dom = max(sweep_classes, key=lambda c: ktimes[c][1])
     n_l, t_l = ktimes[dom]
     avg_ms = t_l / n_l
-    alg_bytes = BYTES_PER_VSU_SWEEP * local_values * (2 if dom == "sweep_xy" else 1)
+    alg_bytes = BYTES_PER_VSU_SWEEP * local_values * SWEEPS_PER_LAUNCH[dom]
     achieved = alg_bytes / (avg_ms / 1e3) / 1e9
     kernel_total = sum(v[1] for v in ktimes.values())
     step_achieved = bytes_per_vsu_step * vsu_total * args.steps / (ms / 1e3) / 1e9 / world
@@ -351,8 +354,9 @@ def main():
                 "kernel_share_of_step": t_l / kernel_total if kernel_total else None,
                 "step": {"achieved": step_achieved, "frac": step_achieved / peak,
                          "bytes_per_vsu": bytes_per_vsu_step, "note": "per GPU",
-                         "xy_fused": fused,
-                         "dram_bytes_per_vsu": BYTES_PER_VSU_STEP_FUSED if fused else BYTES_PER_VSU_STEP},
+                         "xy_fused": fused, "xyz_fused": fused3,
+                         "dram_bytes_per_vsu": (BYTES_PER_VSU_STEP_XYZ if fused3 else
+                                                BYTES_PER_VSU_STEP_FUSED if fused else BYTES_PER_VSU_STEP)},
                 "per_kernel_ms": {k: {"launches": v[0], "avg_ms": (v[1] / v[0]) if v[0] else None}
                                   for k, v in ktimes.items()},
             },

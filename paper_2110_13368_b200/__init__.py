@@ -33,7 +33,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", os.environ.get("BIODIFF_LIB", "libbiodiff_b200.so"))
 
 AXIS_X, AXIS_Y, AXIS_Z = 0, 1, 2
-KERNEL_CLASSES = ("sweep_x", "sweep_y", "sweep_z", "dirichlet", "sources", "aux", "sweep_xy")
+KERNEL_CLASSES = ("sweep_x", "sweep_y", "sweep_z", "dirichlet", "sources", "aux", "sweep_xy", "sweep_xyz")
 
 
 class BiodiffError(RuntimeError):

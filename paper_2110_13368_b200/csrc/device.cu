@@ -781,8 +781,13 @@ bool DeviceSession::xy_cluster_pays() const
 namespace {
 
 template <int NS>
-const void* xyc_pick_s(int S)
+const void* xyc_pick_s(int S, bool three)
 {
+    if (three) {
+        if (S == 1) return reinterpret_cast<const void*>(kernels::sweep_xyz_cluster<NS, 1>);
+        if (S == 2) return reinterpret_cast<const void*>(kernels::sweep_xyz_cluster<NS, 2>);
+        return reinterpret_cast<const void*>(kernels::sweep_xyz_cluster<NS, 4>);
+    }
     if (S == 1) return reinterpret_cast<const void*>(kernels::sweep_xy_cluster<NS, 1>);
     if (S == 2) return reinterpret_cast<const void*>(kernels::sweep_xy_cluster<NS, 2>);
     return reinterpret_cast<const void*>(kernels::sweep_xy_cluster<NS, 4>);
@@ -790,8 +795,10 @@ const void* xyc_pick_s(int S)
 
 } // namespace
 
-// x+y of each plane by one thread-block cluster through L2 (xyc.cuh).
-void DeviceSession::launch_xy_cluster()
+// x+y of each plane by one thread-block cluster through L2 (xyc.cuh); with
+// `three` (ensembles) x, y and z of each replica, the z phase with the
+// Dirichlet shell clamp.
+void DeviceSession::launch_xy_cluster(bool three)
 {
     auto st = static_cast<cudaStream_t>(stream_);
     const int S = S_;
@@ -805,7 +812,7 @@ void DeviceSession::launch_xy_cluster()
     a.nz = mesh_.nz;
     a.S = S;
     a.rowlen = mesh_.nx * S;
-    a.planes = mesh_.nz * replicas_;
+    a.planes = three ? replicas_ : mesh_.nz * replicas_;
     const int L = kernels::kLanes / S;
     a.xi = (mesh_.ny + L - 1) / L;
     a.yi = (a.rowlen + kernels::kLanes - 1) / kernels::kLanes;
@@ -819,7 +826,24 @@ void DeviceSession::launch_xy_cluster()
     y.S = S;
     y.nx = mesh_.nx;
     y.clamp = kernels::Clamp{shell_values_, 0ull, z0_, nzg_};
-    const int ns = std::max(2, std::min(3, std::atoi(env_or("BIODIFF_XYC_SLOTS", "3"))));
+    if (three) {
+        const DeviceWorkspace& wz = ws_[2];
+        kernels::StridedSweep& z = a.z;
+        z.coef = kernels::Coef{wz.q,     wz.dinv, wz.cb, wz.dconst, wz.cconst, wz.settle,
+                               static_cast<long long>(wz.n) * S, wz.dinvT, wz.cbT, wz.n};
+        z.axis = 2;
+        z.n = mesh_.nz;
+        z.n_outer = mesh_.ny;
+        z.rowlen = a.rowlen;
+        z.S = S;
+        z.nx = mesh_.nx;
+        z.clamp = kernels::Clamp{shell_values_, shell_mask_, z0_, nzg_};
+    }
+    // Three slots; two when no line of a 3-phase unit has more than two
+    // chunks (C5: 2.785 vs 2.819 ms per step) — no reloads either way.
+    const int nmax = std::max({mesh_.nx, mesh_.ny, three ? mesh_.nz : 0});
+    const char* ns_dflt = three && nmax <= 2 * kernels::kChunk ? "2" : "3";
+    const int ns = std::max(2, std::min(3, std::atoi(env_or("BIODIFF_XYC_SLOTS", ns_dflt))));
     // 8 CTAs x 4 warps per cluster (32 warps: one x and one y item each at
     // C3), two CTAs of DIFFERENT clusters per SM: their plane phases and
     // barriers drift apart, so one cluster's x (DRAM) phase overlaps the
@@ -829,7 +853,7 @@ void DeviceSession::launch_xy_cluster()
     const int cl = std::max(1, std::min(16, std::atoi(env_or("BIODIFF_XYC_CLUSTER", "8"))));
     const int nch = (std::max(mesh_.nx * S / (2 * S) * 2 / 2, mesh_.ny) + kernels::kChunk - 1) / kernels::kChunk;
     const int nchx = (mesh_.nx + kernels::kChunk - 1) / kernels::kChunk;
-    const int nchm = std::max(nch, nchx);
+    const int nchm = std::max({nch, nchx, three ? (mesh_.nz + kernels::kChunk - 1) / kernels::kChunk : 0});
     // Odd clusters start ~half an x item later (~50 ns per x position): the
     // two clusters sharing an SM then keep their DRAM-fed x phases and
     // L2-fed y phases apart instead of starting in lockstep. C3: 381 -> 363
@@ -840,7 +864,7 @@ void DeviceSession::launch_xy_cluster()
     if (a.plane_ctr) ck(cudaMemsetAsync(xyc_ctr_, 0, sizeof(unsigned), st), "memset plane counter");
     a.warp_bytes = ((ns * kernels::kChunk * kernels::kLanes * 8 + 128 + nchm * kernels::kLanes * 8 + 1023) / 1024) * 1024;
     const int smem = 1024 + wpc * a.warp_bytes;
-    const void* fn = ns == 2 ? xyc_pick_s<2>(S) : xyc_pick_s<3>(S);
+    const void* fn = ns == 2 ? xyc_pick_s<2>(S, three) : xyc_pick_s<3>(S, three);
     ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
     if (cl > 8) ck(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1), "cluster 16");
     cudaLaunchConfig_t cfg{};
@@ -859,10 +883,31 @@ void DeviceSession::launch_xy_cluster()
     ck(cudaOccupancyMaxActiveClusters(&max_clusters, fn, &cfg), "max active clusters");
     const int clusters = std::max(1, std::min(max_clusters, a.planes));
     cfg.gridDim = dim3(clusters * cl);
-    begin_kernel(kSweepXY);
-    void* args[] = {tmap_[0], tmap_[1], &a};
-    ck(cudaLaunchKernelExC(&cfg, fn, args), "launch xy cluster");
-    end_kernel(kSweepXY);
+    const KernelClass kc = three ? kSweepXYZ : kSweepXY;
+    begin_kernel(kc);
+    void* args2[] = {tmap_[0], tmap_[1], &a};
+    void* args3[] = {tmap_[0], tmap_[1], tmap_[2], &a};
+    ck(cudaLaunchKernelExC(&cfg, fn, three ? args3 : args2), "launch xy cluster");
+    end_kernel(kc);
+}
+
+// Ensembles: one cluster per replica for all three sweeps when every warp of
+// a cluster has an item per phase and the replicas the clusters hold at once
+// roughly fit in L2 (C5: 33-37 x 4.2 MB). BIODIFF_XYZ_CLUSTER=0/1 forces.
+bool DeviceSession::xyz_cluster_pays() const
+{
+    const std::string m = env_or("BIODIFF_XYZ_CLUSTER", "auto");
+    if (m == "0") return false;
+    if (replicas_ <= 1 || !ws_[1].active || !ws_[2].active || slab_ || batch_replicas_ > 0) return false;
+    if (!(S_ == 1 || S_ == 2 || S_ == 4)) return false;
+    for (int ax = 0; ax < 3; ++ax)
+        if (path_[ax] != SweepPath::smem_ring2) return false;
+    if (m == "1") return true;
+    const int L = kernels::kLanes / S_;
+    const long long xi = static_cast<long long>((mesh_.ny + L - 1) / L) * mesh_.nz;
+    const long long yi = static_cast<long long>((mesh_.nx * S_ + kernels::kLanes - 1) / kernels::kLanes);
+    const double replica_mb = static_cast<double>(mesh_.voxel_count()) * S_ * 8.0 / 1e6;
+    return xi >= 32 && yi * mesh_.nz >= 32 && yi * mesh_.ny >= 32 && replica_mb * (sm_count_ / 4.0) <= 160.0;
 }
 
 namespace {
@@ -912,7 +957,7 @@ void DeviceSession::launch_xy_sweeps()
     if (xy_mode_ == 1)
         launch_xy2();
     else
-        launch_xy_cluster();
+        launch_xy_cluster(false);
 }
 
 namespace {
@@ -1202,6 +1247,12 @@ void DeviceSession::step_body(bool with_sources, double dt)
     if (slab_ && (prev_slab_ || next_slab_))
         throw state_error("in-process z-slabs advance together: use the group advance");
     const Axis last = ws_[2].active ? Axis::z : ws_[1].active ? Axis::y : Axis::x;
+    if (last == Axis::z && xyz_cluster_pays()) {
+        launch_xy_cluster(true);
+        launch_residual_dirichlet(false);
+        if (with_sources) launch_sources(dt);
+        return;
+    }
     if (last == Axis::z) {
         launch_xy_sweeps();
     } else {

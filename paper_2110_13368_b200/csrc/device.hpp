@@ -27,8 +27,9 @@ enum KernelClass {
     kDirichlet = 3,
     kSources = 4,
     kAux = 5,
-    kSweepXY = 6, // fused x+y sweeps through L2 (xy2.cuh, opt-in)
-    kNumKernelClasses = 7
+    kSweepXY = 6, // fused x+y sweeps through L2 (plane clusters xyc.cuh, or xy2.cuh)
+    kSweepXYZ = 7, // ensembles: x, y and z of a replica by one cluster (xyc.cuh)
+    kNumKernelClasses = 8
 };
 
 // Device-side copy of one SolverWorkspace (solver.hpp:24-33).
@@ -211,8 +212,9 @@ private:
     bool ring_persist_yz_ = false;
     bool xy_fused_ = false;          // BIODIFF_XY_FUSED=1 (lagged tickets) / 2 (plane clusters)
     int xy_mode_ = 0;
-    void launch_xy_cluster();
+    void launch_xy_cluster(bool three);
     bool xy_cluster_pays() const;
+    bool xyz_cluster_pays() const;
     int l2_hints_ = 0;               // ring2 L2 cache hints, BIODIFF_L2_HINTS bitmask (1 loads, 2 stores)
     // Ensembles: replica batches that stay resident in L2 across several
     // steps (advance). rbn_ = 0: kernels cover every replica.

@@ -23,8 +23,9 @@ namespace kernels {
 struct XYCluster {
     Coef xcoef;
     StridedSweep y;  // y coefficients / geometry for make_chain_yz (axis 1)
+    StridedSweep z;  // z (axis 2; 3-phase kernel only, with the Dirichlet shell clamp)
     int nx, ny, nz, S;
-    int planes;      // nz * replicas
+    int planes;      // work units: planes (nz * replicas; 2-phase) or replicas (3-phase)
     int xi, yi;      // x / y items per plane
     int rowlen;
     int warp_bytes;  // shared memory per warp (1024-aligned)
@@ -98,38 +99,77 @@ struct LayoutU {
     __device__ __forceinline__ int off(int u) const { return row + t[u % P] + (u / P) * (L * 16); }
 };
 
-// One item of either kind. x: lines j0 = it*L .. of plane P; y: columns
-// e0 = it*32 .. of plane P. Issues its first chunks unless prefetched; a y
-// item prefetches the warp's next x item (plane Pn, item itn >= 0) into the
-// slots it frees. Returns whether it did.
-template <int NS, int S>
-__device__ __forceinline__ bool xyc_item(const CUtensorMap* tmap_x, const CUtensorMap* tmap_y, const XYCluster& a,
-                                         const Ring2Smem& sm, uint32_t& parity, bool is_x, int P, int it,
-                                         bool prefetched, int Pn, int itn)
+// Geometry of one item. 2-phase (plane units, THREE = false): x = lines
+// it*L.. of plane U, y = columns it*32.. of plane U. 3-phase (replica
+// units): x item it = (plane it / xi, line block it % xi), y item = (plane
+// it / yi, column block it % yi), z item = (row it / yi, column block
+// it % yi) of replica U. x: plane index P and line block j; y / z: replica
+// rep, outer index o (plane for y, row for z), column block eb.
+struct XycGeom {
+    int P, j, rep, o, eb;
+};
+
+template <bool THREE>
+__device__ __forceinline__ XycGeom xyc_geom(const XYCluster& a, int kind, int U, int it)
+{
+    XycGeom g;
+    if constexpr (THREE) {
+        g.P = U * a.nz + it / a.xi;
+        g.j = it % a.xi;
+        g.rep = U;
+        g.o = it / a.yi;
+        g.eb = it % a.yi;
+    } else {
+        g.P = U;
+        g.j = it;
+        g.rep = U / a.nz;
+        g.o = U % a.nz;
+        g.eb = it;
+    }
+    (void)kind;
+    return g;
+}
+
+// Issues chunk k of an item into `slot` (lane 0).
+template <int S, bool THREE>
+__device__ __forceinline__ void xyc_issue(const CUtensorMap* tmap_x, const CUtensorMap* tmap_y,
+                                          const CUtensorMap* tmap_z, const Ring2Smem& sm, int kind, const XycGeom& g,
+                                          int k, int slot)
+{
+    constexpr int kSlot = kChunk * kLanes;
+    constexpr int L = kLanes / S;
+    ptx::mbar_arrive_expect_tx(&sm.bars[slot], kSlot * 8);
+    if (kind == 0)
+        ptx::tma_load_4d(sm.slots + slot * kSlot, tmap_x, 0, g.j * L, g.P, k * 2 * S, &sm.bars[slot]);
+    else if (THREE && kind == 2)
+        ptx::tma_load_4d(sm.slots + slot * kSlot, tmap_z, g.eb * kLanes, g.o, k * kChunk, g.rep, &sm.bars[slot]);
+    else
+        ptx::tma_load_4d(sm.slots + slot * kSlot, tmap_y, g.eb * kLanes, k * kChunk, g.o, g.rep, &sm.bars[slot]);
+}
+
+// One item (kind 0 x, 1 y, 2 z). Issues its first chunks unless the
+// warp's previous item prefetched them; prefetches the warp's next item
+// (kind tk, unit tU, item tit >= 0: the next item of the same phase, or the
+// next unit's first x item after the last phase) into the slots it frees.
+// Returns whether it did.
+template <int NS, int S, bool THREE>
+__device__ __forceinline__ bool xyc_item(const CUtensorMap* tmap_x, const CUtensorMap* tmap_y,
+                                         const CUtensorMap* tmap_z, const XYCluster& a, const Ring2Smem& sm,
+                                         uint32_t& parity, int kind, int U, int it, bool prefetched, int tk, int tU,
+                                         int tit)
 {
     constexpr int kSlot = kChunk * kLanes;
     constexpr int L = kLanes / S;
     const int lane = threadIdx.x & 31;
-    const int nchx = (a.nx + kChunk - 1) / kChunk;
-    const int nchy = (a.ny + kChunk - 1) / kChunk;
-    const int nch = is_x ? nchx : nchy;
-    const int rep = P / a.nz, kk = P % a.nz;
-    auto issue_x = [&](int Pq, int itq, int k, int slot) {
-        ptx::mbar_arrive_expect_tx(&sm.bars[slot], kSlot * 8);
-        ptx::tma_load_4d(sm.slots + slot * kSlot, tmap_x, 0, itq * L, Pq, k * 2 * S, &sm.bars[slot]);
+    const bool is_x = kind == 0;
+    auto nch_of = [&](int kd) {
+        const int n = kd == 0 ? a.nx : (THREE && kd == 2 ? a.nz : a.ny);
+        return (n + kChunk - 1) / kChunk;
     };
-    auto issue_y = [&](int k, int slot) {
-        ptx::mbar_arrive_expect_tx(&sm.bars[slot], kSlot * 8);
-        ptx::tma_load_4d(sm.slots + slot * kSlot, tmap_y, it * kLanes, k * kChunk, kk, rep, &sm.bars[slot]);
-    };
-    auto issue = [&](int k, int slot) {
-        if (is_x)
-            issue_x(P, it, k, slot);
-        else
-            issue_y(k, slot);
-    };
+    const int nch = nch_of(kind);
+    const XycGeom g = xyc_geom<THREE>(a, kind, U, it);
     if (lane == 0 && !prefetched)
-        for (int k = 0; k < min(NS, nch); ++k) issue(k, k);
+        for (int k = 0; k < min(NS, nch); ++k) xyc_issue<S, THREE>(tmap_x, tmap_y, tmap_z, sm, kind, g, k, k);
     __syncwarp();
     LayoutU<S> lay;
     Chain c;
@@ -139,30 +179,35 @@ __device__ __forceinline__ bool xyc_item(const CUtensorMap* tmap_x, const CUtens
         x_lane<S>(lane, xl, xs);
         lay.set_x(xl, xs);
         Clamp none{nullptr, 0ull, 0, a.nz};
-        c = make_chain(a.xcoef, S, xs, a.nx, none, false, rep);
-        active = it * L + xl < a.ny;
+        c = make_chain(a.xcoef, S, xs, a.nx, none, false, g.rep);
+        active = g.j * L + xl < a.ny;
     } else {
         lay.set_y(lane);
-        const int e0 = it * kLanes;
+        const int e0 = g.eb * kLanes;
         active = lane < min(kLanes, a.rowlen - e0);
         const int e = e0 + (active ? lane : 0);
-        c = make_chain_yz(a.y, e % S, e / S, kk, rep);
+        c = make_chain_yz(THREE && kind == 2 ? a.z : a.y, e % S, e / S, g.o, g.rep);
     }
-    const bool pf = !is_x && itn >= 0 && min(NS, nchx) <= min(NS, nchy);
-    const uint64_t pol = is_x ? ptx::policy_evict_last() : ptx::policy_evict_first();
-    solve_ring2<NS, false>(
+    const int tnch = tit >= 0 ? min(NS, nch_of(tk)) : 0;
+    const bool pf = tit >= 0 && tnch <= min(NS, nch);
+    // x (and, 3-phase, y) results are read again by the next phase: keep them
+    // in L2; the last phase's results stream out.
+    const uint64_t pol = (is_x || (THREE && kind == 1)) ? ptx::policy_evict_last() : ptx::policy_evict_first();
+    solve_ring2<NS, THREE>(
         c, active, sm.bars, sm.slots, kSlot, sm.ckpt, lane, parity, [&] { return pf; }, lay,
         [&](int rel, int k, int slot, bool) {
             if (!rel)
-                issue(k, slot);
-            else if (k < min(NS, nchx))
-                issue_x(Pn, itn, k, slot);
+                xyc_issue<S, THREE>(tmap_x, tmap_y, tmap_z, sm, kind, g, k, slot);
+            else if (k < tnch)
+                xyc_issue<S, THREE>(tmap_x, tmap_y, tmap_z, sm, tk, xyc_geom<THREE>(a, tk, tU, tit), k, slot);
         },
         [&](int k, int slot) {
             if (is_x)
-                ptx::tma_store_4d_hint(tmap_x, 0, it * L, P, k * 2 * S, sm.slots + slot * kSlot, pol);
+                ptx::tma_store_4d_hint(tmap_x, 0, g.j * L, g.P, k * 2 * S, sm.slots + slot * kSlot, pol);
+            else if (THREE && kind == 2)
+                ptx::tma_store_4d_hint(tmap_z, g.eb * kLanes, g.o, k * kChunk, g.rep, sm.slots + slot * kSlot, pol);
             else
-                ptx::tma_store_4d_hint(tmap_y, it * kLanes, k * kChunk, kk, rep, sm.slots + slot * kSlot, pol);
+                ptx::tma_store_4d_hint(tmap_y, g.eb * kLanes, k * kChunk, g.o, g.rep, sm.slots + slot * kSlot, pol);
         },
         nullptr);
     return pf;
@@ -191,11 +236,10 @@ __device__ __forceinline__ unsigned long long xyc_now()
 #define XYC_STAMP(P, gw, i)
 #endif
 
-template <int NS, int S>
-__global__ void __launch_bounds__(256) sweep_xy_cluster(const __grid_constant__ CUtensorMap tmap_x,
-                                                        const __grid_constant__ CUtensorMap tmap_y, XYCluster a)
+template <int NS, int S, bool THREE>
+__device__ __forceinline__ void xyc_body(const CUtensorMap* tmap_x, const CUtensorMap* tmap_y,
+                                         const CUtensorMap* tmap_z, const XYCluster& a, unsigned char* smem_xyc)
 {
-    extern __shared__ __align__(1024) unsigned char smem_xyc[];
     constexpr int kSlot = kChunk * kLanes;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int wpc = blockDim.x >> 5;
@@ -209,8 +253,9 @@ __global__ void __launch_bounds__(256) sweep_xy_cluster(const __grid_constant__ 
     sm.ckpt = reinterpret_cast<double*>(mine + NS * kSlot * 8 + 128);
     if (lane == 0) {
         if (warp == 0) {
-            ptx::tma_prefetch_desc(&tmap_x);
-            ptx::tma_prefetch_desc(&tmap_y);
+            ptx::tma_prefetch_desc(tmap_x);
+            ptx::tma_prefetch_desc(tmap_y);
+            if (THREE) ptx::tma_prefetch_desc(tmap_z);
         }
         for (int s = 0; s < NS; ++s) ptx::mbar_init(&sm.bars[s], 1);
         ptx::fence_mbar_init();
@@ -234,14 +279,18 @@ __global__ void __launch_bounds__(256) sweep_xy_cluster(const __grid_constant__ 
     int round = 0;
     for (int P = P0; P < a.planes; ++round) {
         int Pn = P + dP, itn = -1;
+        constexpr int nph = THREE ? 3 : 2;
+        const int xitems = THREE ? a.xi * a.nz : a.xi;
         if (a.plane_ctr && leader) s_next[round & 1] = dP + static_cast<int>(atomicAdd(a.plane_ctr, 1u));
         // Phase 0: this warp's x items of plane P; phase 1: its y items (the
         // last one prefetches the next plane's first x item). One loop, one
         // copy of the chunk code.
 #pragma unroll 1
-        for (int ph = 0; ph < 2; ++ph) {
-            XYC_STAMP(P, gw, ph == 0 ? 0 : 1)
-            if (ph == 1) {
+        for (int ph = 0; ph < nph; ++ph) {
+            if (!THREE) {
+                XYC_STAMP(P, gw, ph == 0 ? 0 : 1)
+            }
+            if (ph >= 1) {
                 // The plane's x results must be complete and visible before
                 // any warp of the cluster reads them through TMA.
                 if (lane == 0) {
@@ -251,29 +300,59 @@ __global__ void __launch_bounds__(256) sweep_xy_cluster(const __grid_constant__ 
                 __syncwarp();
                 cluster_sync();
                 if (lane == 0) ptx::fence_proxy_async_global();
-                if (a.plane_ctr) {
+                if (ph == 1 && a.plane_ctr) {
                     int v = 0;
                     if (lane == 0) v = ld_cluster_int(&s_next[round & 1], 0);
                     Pn = __shfl_sync(0xffffffffu, v, 0);
                 }
-                itn = (Pn < a.planes && gw < a.xi) ? gw : -1;
+                itn = (Pn < a.planes && gw < xitems) ? gw : -1;
                 __syncwarp();
-                XYC_STAMP(P, gw, 2)
+                if (!THREE) {
+                    XYC_STAMP(P, gw, 2)
+                }
             }
             const bool is_x = ph == 0;
-            const int items = is_x ? a.xi : a.yi;
+            const int items = is_x ? xitems : (THREE ? a.yi * (ph == 1 ? a.nz : a.ny) : a.yi);
 #pragma unroll 1
             for (int it = gw; it < items; it += nw) {
-                const bool last_y = !is_x && it + nw >= items;
-                const bool pf = xyc_item<NS, S>(&tmap_x, &tmap_y, a, sm, parity, is_x, P, it,
-                                                is_x && prefetched && it == gw, Pn, last_y ? itn : -1);
-                prefetched = is_x ? false : pf;
+                // prefetch target: this warp's next item of the phase, else
+                // (last phase) its first x item of the next unit
+                int tk = ph, tU = P, tit = it + nw;
+                if (tit >= items) {
+                    tk = 0;
+                    tU = Pn;
+                    tit = ph == nph - 1 ? itn : -1;
+                }
+                prefetched = xyc_item<NS, S, THREE>(tmap_x, tmap_y, tmap_z, a, sm, parity, ph, P, it, prefetched, tk,
+                                                    tU, tit);
             }
         }
-        XYC_STAMP(P, gw, 3)
+        if (!THREE) {
+            XYC_STAMP(P, gw, 3)
+        }
         P = Pn;
     }
     if (lane == 0) ptx::bulk_wait_all();
+}
+
+template <int NS, int S>
+__global__ void __launch_bounds__(256) sweep_xy_cluster(const __grid_constant__ CUtensorMap tmap_x,
+                                                        const __grid_constant__ CUtensorMap tmap_y, XYCluster a)
+{
+    extern __shared__ __align__(1024) unsigned char smem_xyc[];
+    xyc_body<NS, S, false>(&tmap_x, &tmap_y, &tmap_y, a, smem_xyc);
+}
+
+// Ensembles: one cluster advances one replica through x, y and z (three
+// phases, two cluster barriers) while the replica stays in L2; the z phase
+// applies the fused Dirichlet shell like the separate z sweep.
+template <int NS, int S>
+__global__ void __launch_bounds__(256) sweep_xyz_cluster(const __grid_constant__ CUtensorMap tmap_x,
+                                                         const __grid_constant__ CUtensorMap tmap_y,
+                                                         const __grid_constant__ CUtensorMap tmap_z, XYCluster a)
+{
+    extern __shared__ __align__(1024) unsigned char smem_xyc[];
+    xyc_body<NS, S, true>(&tmap_x, &tmap_y, &tmap_z, a, smem_xyc);
 }
 
 } // namespace kernels

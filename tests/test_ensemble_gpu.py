@@ -31,11 +31,17 @@ def replicas(n, shape, S, agents, steps, clamps=0):
 
 # L2 replica batches (DeviceSession::step_body_batches): "0" = off; small
 # budgets force 1-2 replicas per batch and batch visits shorter than the run.
-BATCHING = [{"BIODIFF_L2_BATCH_MB": "0"}, {"BIODIFF_L2_BATCH_MB": "0.2", "BIODIFF_BATCH_STEPS": "3"},
-            {"BIODIFF_L2_BATCH_MB": "2.5", "BIODIFF_BATCH_STEPS": "4"}]
+# BIODIFF_XYZ_CLUSTER=1: one thread-block cluster per replica for x, y and z
+# (xyc.cuh sweep_xyz_cluster; S in {1, 2, 4}, else the separate sweeps).
+BATCHING = [{"BIODIFF_L2_BATCH_MB": "0", "BIODIFF_XYZ_CLUSTER": "0"},
+            {"BIODIFF_L2_BATCH_MB": "0.2", "BIODIFF_BATCH_STEPS": "3"},
+            {"BIODIFF_L2_BATCH_MB": "2.5", "BIODIFF_BATCH_STEPS": "4"},
+            {"BIODIFF_XYZ_CLUSTER": "1"},
+            {"BIODIFF_XYZ_CLUSTER": "1", "BIODIFF_XYC_SLOTS": "2", "BIODIFF_XYC_DYNAMIC": "0"},
+            {"BIODIFF_XYZ_CLUSTER": "1", "BIODIFF_XYC_WARPS": "3", "BIODIFF_XYC_CLUSTER": "2"}]
 
 
-@pytest.mark.parametrize("batching", BATCHING, ids=["off", "tiny", "small"])
+@pytest.mark.parametrize("batching", BATCHING, ids=["off", "tiny", "small", "xyz", "xyz_ns2_static", "xyz_2x3"])
 @pytest.mark.parametrize("n,shape,S,agents,steps,clamps", [
     (4, (24, 20, 18), 2, 200, 10, 3),
     (7, (32, 32, 32), 2, 300, 6, 0),
