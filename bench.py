@@ -50,14 +50,15 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(kernel_class):
-    """DRAM bytes per launch from the committed ncu --set full summary (or None)."""
+def ncu_traffic(workload, kernel_class):
+    """DRAM bytes per launch of `kernel_class` on `workload` from the committed
+    ncu --set full summaries (profiles/ncu_traffic.json), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
-    return d.get(kernel_class)
+    return d.get(workload, {}).get(kernel_class)
 
 
 class ClockSampler:
@@ -349,7 +350,7 @@ def main():
             "config": cfg,
             "roofline": {
                 "bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": ncu_traffic(dom) if not zslab else None,
+                "frac": achieved / peak, "traffic": ncu_traffic(args.workload, dom) if not zslab else None,
                 "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_ms, "peak_source": peak_src,
                 "kernel_share_of_step": t_l / kernel_total if kernel_total else None,
                 "step": {"achieved": step_achieved, "frac": step_achieved / peak,

@@ -881,7 +881,8 @@ void DeviceSession::launch_xy_cluster(bool three)
     cfg.gridDim = dim3(cl);
     int max_clusters = 0;
     ck(cudaOccupancyMaxActiveClusters(&max_clusters, fn, &cfg), "max active clusters");
-    const int clusters = std::max(1, std::min(max_clusters, a.planes));
+    const int cap = std::atoi(env_or("BIODIFF_XYC_MAX_CLUSTERS", "0"));
+    const int clusters = std::max(1, std::min({max_clusters, a.planes, cap > 0 ? cap : max_clusters}));
     cfg.gridDim = dim3(clusters * cl);
     const KernelClass kc = three ? kSweepXYZ : kSweepXY;
     begin_kernel(kc);
