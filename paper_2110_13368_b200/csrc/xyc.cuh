@@ -32,6 +32,8 @@ struct XYCluster {
     int stagger_ns;  // cluster c starts (c % stagger_groups) * stagger_ns later (phase offset; 0 = off)
     int stagger_groups;
     unsigned* plane_ctr; // dynamic plane scheduling (zeroed before the launch), or nullptr: static P += clusters
+    int reverse;         // 2-phase: visit planes from the top (unit U = plane planes-1-U)
+    int keep_planes;     // 2-phase: y results of planes k < keep_planes stay in L2 (evict_normal) for the z sweep
 };
 
 __device__ __forceinline__ uint32_t cluster_ctarank()
@@ -120,10 +122,11 @@ __device__ __forceinline__ XycGeom xyc_geom(const XYCluster& a, int kind, int U,
         g.o = it / a.yi;
         g.eb = it % a.yi;
     } else {
-        g.P = U;
+        const int Pp = a.reverse ? a.planes - 1 - U : U;
+        g.P = Pp;
         g.j = it;
-        g.rep = U / a.nz;
-        g.o = U % a.nz;
+        g.rep = Pp / a.nz;
+        g.o = Pp % a.nz;
         g.eb = it;
     }
     (void)kind;
@@ -192,7 +195,9 @@ __device__ __forceinline__ bool xyc_item(const CUtensorMap* tmap_x, const CUtens
     const bool pf = tit >= 0 && tnch <= min(NS, nch);
     // x (and, 3-phase, y) results are read again by the next phase: keep them
     // in L2; the last phase's results stream out.
-    const uint64_t pol = (is_x || (THREE && kind == 1)) ? ptx::policy_evict_last() : ptx::policy_evict_first();
+    const uint64_t pol = (is_x || (THREE && kind == 1)) ? ptx::policy_evict_last()
+                         : (!THREE && g.o < a.keep_planes) ? ptx::policy_evict_normal()
+                                                           : ptx::policy_evict_first();
     solve_ring2<NS, THREE>(
         c, active, sm.bars, sm.slots, kSlot, sm.ckpt, lane, parity, [&] { return pf; }, lay,
         [&](int rel, int k, int slot, bool) {

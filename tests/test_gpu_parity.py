@@ -292,11 +292,13 @@ FUSED_ENVS = [
     {"BIODIFF_XY_FUSED": "2", "BIODIFF_XYC_CLUSTER": "2", "BIODIFF_XYC_WARPS": "3", "BIODIFF_XYC_SLOTS": "2"},
     {"BIODIFF_XY_FUSED": "2", "BIODIFF_XYC_CLUSTER": "4", "BIODIFF_XYC_WARPS": "8"},   # one CTA per SM
     {"BIODIFF_XY_FUSED": "2", "BIODIFF_XYC_CLUSTER": "16", "BIODIFF_XYC_WARPS": "1"},  # non-portable cluster size
+    {"BIODIFF_XY_FUSED": "2", "BIODIFF_XYC_REVERSE": "0", "BIODIFF_XYC_DYNAMIC": "0",  # static planes, bottom up
+     "BIODIFF_XYC_STAGGER_NS": "0"},
 ]
 
 
 @pytest.mark.parametrize("env", FUSED_ENVS, ids=["unfused", "fused", "lag1", "lagmax", "1cta", "slots2", "cluster",
-                                                 "cluster2x3", "cluster4x8", "cluster16x1"])
+                                                 "cluster2x3", "cluster4x8", "cluster16x1", "cluster_static"])
 @pytest.mark.parametrize("shape,S", SWEEP_SHAPES)
 def test_fused_xy_step_bitwise(shape, S, env, monkeypatch):
     """The fused x+y kernel (ticketed items, per-plane release/acquire
