@@ -152,6 +152,7 @@ DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int devi
         xy_fused_ = xy_mode_ != 0;
     }
     l2_hints_ = std::atoi(env_or("BIODIFF_L2_HINTS", "2")); // stores evict_first: C3 0.635 -> 0.629 ms; load hints slower
+    l2_keep_from8_ = std::atoi(env_or("BIODIFF_L2_KEEP_FROM8", "4"));
     if (replicas_ > 1) { // L2 replica batches (step_body_batches)
         const double replica_mb = static_cast<double>(mesh.voxel_count()) * substrates * 8.0 / 1e6;
         const double budget = std::atof(env_or("BIODIFF_L2_BATCH_MB", "0")); // opt-in: measured slower (C5 latency-bound)
@@ -1024,6 +1025,16 @@ const void* x_ring2_pick(int ns, int S, bool short_lines)
 
 } // namespace
 
+// Long lines (C4: 32 chunks, ~300 MB between a chunk's first read and its
+// reload): the first loads of the later half of the reloaded chunks are
+// kept in L2 (hint bit 2), the rest stream — C4 43.5 -> 42.7 ms per step;
+// at C3's 8-chunk lines the same hint is slower (z 202 -> 213 us).
+int DeviceSession::long_line_hint(int nch) const
+{
+    const int from = std::atoi(env_or("BIODIFF_L2_LONG_CHUNKS", "16"));
+    return (from > 0 && nch >= from) ? 4 : 0;
+}
+
 // ring2 launch (ring2.cuh): x persistent over per-plane line tiles (next
 // tile's chunks prefetched), y / z one tile per CTA unless
 // BIODIFF_RING_PERSIST=all.
@@ -1050,7 +1061,8 @@ void DeviceSession::launch_ring2(int ax, bool do_clamp, const kernels::Clamp& cl
         x.S = S_;
         x.planes = mesh_.nz * batch_nr();
         x.P0 = (rbn_ ? rb0_ : 0) * mesh_.nz;
-        x.hints = l2_hints_;
+        x.hints = l2_hints_ | long_line_hint((mesh_.nx + kernels::kChunk - 1) / kernels::kChunk);
+        x.keep_from8 = l2_keep_from8_;
         const int L = kernels::kLanes / S_;
         x.xi = (mesh_.ny + L - 1) / L;
         x.tiles = static_cast<long long>(x.xi) * x.planes;
@@ -1074,7 +1086,8 @@ void DeviceSession::launch_ring2(int ax, bool do_clamp, const kernels::Clamp& cl
     y.tiles_per_row = (rowlen + kernels::kLanes - 1) / kernels::kLanes;
     y.reps = replicas_;
     y.r0 = rbn_ ? rb0_ : 0;
-    y.hints = l2_hints_;
+    y.hints = l2_hints_ | long_line_hint((y.n + kernels::kChunk - 1) / kernels::kChunk);
+    y.keep_from8 = l2_keep_from8_;
     y.tiles = y.tiles_per_row * y.n_outer * batch_nr();
     y.S = S_;
     y.nx = mesh_.nx;

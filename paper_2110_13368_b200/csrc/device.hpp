@@ -215,7 +215,9 @@ private:
     void launch_xy_cluster(bool three);
     bool xy_cluster_pays() const;
     bool xyz_cluster_pays() const;
+    int long_line_hint(int nch) const;
     int l2_hints_ = 0;               // ring2 L2 cache hints, BIODIFF_L2_HINTS bitmask (1 loads, 2 stores)
+    int l2_keep_from8_ = 4; // L2 hint bit 2: reloaded chunks k >= keep_from8/8 of them keep their first load
     // Ensembles: replica batches that stay resident in L2 across several
     // steps (advance). rbn_ = 0: kernels cover every replica.
     int rb0_ = 0, rbn_ = 0;

@@ -219,7 +219,8 @@ struct StridedSweep {
     int tiles;   // tiles_per_row * n_outer * reps
     int reps;    // ensemble replicas stacked along the 4th tensor dimension (ring kernel)
     int r0;      // first replica of this launch (ring2 replica batches), else 0
-    int hints;   // ring2 L2 cache hints: bit 0 loads, bit 1 stores (BIODIFF_L2_HINTS)
+    int hints;   // ring2 L2 cache hints: bit 0 loads, bit 1 stores, bit 2 loads of near reloads only (BIODIFF_L2_HINTS)
+    int keep_from8; // bit 2: first loads of reloaded chunks k >= keep_from8/8 of them stay in L2
     int S;
     int nx;
     long long stride;       // (plain kernel) doubles between positions along the axis

@@ -423,14 +423,17 @@ __global__ void __launch_bounds__(kLanes) sweep_yz_ring2(const __grid_constant__
     const int nch = (a.n + kChunk - 1) / kChunk;
     // L2 hints (a.hints bit 0): first loads of chunks the back substitution
     // will reload stay (evict_last); reloads and the other loads stream.
+    // Bit 2: only the later ones (k >= keep_from8/8 of them: the reloads with
+    // the shortest reuse distance) stay.
     const uint64_t keep_pol = ptx::policy_evict_last(), stream_pol = ptx::policy_evict_first();
     auto issue = [&](const TileAt& d, int k, int slot, bool reload = false) {
         const int c1 = a.axis == 2 ? d.outer : k * kChunk;
         const int c2 = a.axis == 2 ? k * kChunk : d.outer;
         ptx::mbar_arrive_expect_tx(&sm.bars[slot], kSlot * 8);
-        if (a.hints & 1)
+        if (a.hints & 5)
             ptx::tma_load_4d_hint(sm.slots + slot * kSlot, &tmap, d.e0, c1, c2, d.r, &sm.bars[slot],
-                                  (!reload && k < nch - NS) ? keep_pol : stream_pol);
+                                  (!reload && k < nch - NS && (!(a.hints & 4) || 8 * k >= a.keep_from8 * (nch - NS))) ? keep_pol
+                                                                                                     : stream_pol);
         else
             ptx::tma_load_4d(sm.slots + slot * kSlot, &tmap, d.e0, c1, c2, d.r, &sm.bars[slot]);
     };
@@ -491,7 +494,8 @@ struct XSweep2 {
     int nx, ny, nz, S;
     int planes; // nz * replicas (of this launch's replica batch)
     int P0;     // first plane (replica batch r0: r0 * nz)
-    int hints;  // L2 cache hints: bit 0 loads, bit 1 stores (BIODIFF_L2_HINTS)
+    int hints;  // L2 cache hints: bit 0 loads, bit 1 stores, bit 2 near reloads only (BIODIFF_L2_HINTS)
+    int keep_from8;
     int xi;     // tiles per plane
     long long tiles;
     Clamp clamp;
@@ -512,9 +516,10 @@ __global__ void __launch_bounds__(kLanes) sweep_x_ring2(const __grid_constant__ 
     const uint64_t keep_pol = ptx::policy_evict_last(), stream_pol = ptx::policy_evict_first();
     auto issue = [&](int P, int j0, int k, int slot, bool reload = false) {
         ptx::mbar_arrive_expect_tx(&sm.bars[slot], kSlot * 8);
-        if (a.hints & 1)
+        if (a.hints & 5)
             ptx::tma_load_4d_hint(sm.slots + slot * kSlot, &tmap, 0, j0, P, k * 2 * S, &sm.bars[slot],
-                                  (!reload && k < nch - NS) ? keep_pol : stream_pol);
+                                  (!reload && k < nch - NS && (!(a.hints & 4) || 8 * k >= a.keep_from8 * (nch - NS))) ? keep_pol
+                                                                                                     : stream_pol);
         else
             ptx::tma_load_4d(sm.slots + slot * kSlot, &tmap, 0, j0, P, k * 2 * S, &sm.bars[slot]);
     };
