@@ -249,8 +249,8 @@ def main():
     s.synchronize()
     barrier()
 
-    # Timed region: exactly K steps, per-kernel CUDA events on the session stream.
-    s.set_kernel_timing(True)
+    # Timed region: exactly K steps of the production path (advance = CUDA-graph
+    # replay), CUDA events on the session stream around it.
     l0 = s.launch_count()
     with ClockSampler(device) as clk:
         s.synchronize()
@@ -262,6 +262,19 @@ def main():
         s.synchronize()
         barrier()
     launches = s.launch_count() - l0
+    # Per-kernel pass for the roofline: the same K steps again with a CUDA
+    # event pair around every kernel (graphs off: events between kernels),
+    # so the launch durations are measured, not inferred. For launch-bound
+    # configs (C1, C2) this pass is slower than the graph-replayed region.
+    s.set_kernel_timing(True)
+    s.synchronize()
+    barrier()
+    s.event_record(6)
+    s.advance(args.steps, w.dt)
+    s.event_record(7)
+    ms_kernel_pass = s.event_elapsed(6, 7)
+    s.synchronize()
+    barrier()
     ktimes = s.kernel_times()
     s.set_kernel_timing(False)
     if dist is not None:
@@ -353,6 +366,7 @@ def main():
                 "frac": achieved / peak, "traffic": ncu_traffic(args.workload, dom) if not zslab else None,
                 "algorithmic_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_ms, "peak_source": peak_src,
                 "kernel_share_of_step": t_l / kernel_total if kernel_total else None,
+                "kernel_pass_ms_per_step": ms_kernel_pass / args.steps,
                 "step": {"achieved": step_achieved, "frac": step_achieved / peak,
                          "bytes_per_vsu": bytes_per_vsu_step, "note": "per GPU",
                          "xy_fused": fused, "xyz_fused": fused3,

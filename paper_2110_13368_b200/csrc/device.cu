@@ -153,6 +153,10 @@ DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int devi
     }
     l2_hints_ = std::atoi(env_or("BIODIFF_L2_HINTS", "2")); // stores evict_first: C3 0.635 -> 0.629 ms; load hints slower
     l2_keep_from8_ = std::atoi(env_or("BIODIFF_L2_KEEP_FROM8", "4"));
+    // Programmatic dependent launch of the step kernels: opt-in. Measured in
+    // graph replay: C1 28.2 -> 30.3 us, C2 49.3 -> 53.2 us per step, C3 no
+    // change (the kernels' griddepcontrol.wait is a no-op without it).
+    pdl_ = std::atoi(env_or("BIODIFF_PDL", "0")) != 0;
     if (replicas_ > 1) { // L2 replica batches (step_body_batches)
         const double replica_mb = static_cast<double>(mesh.voxel_count()) * substrates * 8.0 / 1e6;
         const double budget = std::atof(env_or("BIODIFF_L2_BATCH_MB", "0")); // opt-in: measured slower (C5 latency-bound)
@@ -872,11 +876,13 @@ void DeviceSession::launch_xy_cluster(bool three)
     cfg.blockDim = dim3(32 * wpc);
     cfg.dynamicSmemBytes = static_cast<std::size_t>(smem);
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = cl;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     cfg.gridDim = dim3(cl);
@@ -894,6 +900,7 @@ void DeviceSession::launch_xy_cluster(bool three)
     const int cap = std::atoi(env_or("BIODIFF_XYC_MAX_CLUSTERS", "0"));
     const int clusters = std::max(1, std::min({max_clusters, a.planes, cap > 0 ? cap : max_clusters}));
     cfg.gridDim = dim3(clusters * cl);
+    cfg.numAttrs = pdl_ ? 2 : 1;
     const KernelClass kc = three ? kSweepXYZ : kSweepXY;
     begin_kernel(kc);
     void* args2[] = {tmap_[0], tmap_[1], &a};
@@ -1035,6 +1042,29 @@ int DeviceSession::long_line_hint(int nch) const
     return (from > 0 && nch >= from) ? 4 : 0;
 }
 
+// Kernel launch on the session stream, with programmatic dependent launch
+// (PDL: the kernel's CTAs may be scheduled while the previous kernel drains;
+// every step kernel starts with griddepcontrol.wait) when pdl_ is on.
+void DeviceSession::launch_k(const void* fn, unsigned grid, unsigned block, void** args, std::size_t smem, const char* what)
+{
+    auto st = static_cast<cudaStream_t>(stream_);
+    if (!pdl_) {
+        ck(cudaLaunchKernel(fn, dim3(grid), dim3(block), args, smem, st), what);
+        return;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ck(cudaLaunchKernelExC(&cfg, fn, args), what);
+}
+
 // ring2 launch (ring2.cuh): x persistent over per-plane line tiles (next
 // tile's chunks prefetched), y / z one tile per CTA unless
 // BIODIFF_RING_PERSIST=all.
@@ -1073,7 +1103,7 @@ void DeviceSession::launch_ring2(int ax, bool do_clamp, const kernels::Clamp& cl
         const unsigned grid = ring_persist_x_ ? occupancy_grid(fn, x.tiles) : static_cast<unsigned>(x.tiles);
         if (!ring_persist_x_) ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
         void* args[] = {const_cast<CUtensorMap*>(&tm), &x};
-        ck(cudaLaunchKernel(fn, dim3(grid), dim3(kernels::kLanes), args, smem, st), "launch x ring2");
+        launch_k(fn, grid, kernels::kLanes, args, smem, "launch x ring2");
         return;
     }
     kernels::StridedSweep y{};
@@ -1107,7 +1137,7 @@ void DeviceSession::launch_ring2(int ax, bool do_clamp, const kernels::Clamp& cl
         grid = static_cast<unsigned>(y.tiles);
     }
     void* args[] = {const_cast<CUtensorMap*>(&tm), &y};
-    ck(cudaLaunchKernel(fn, dim3(grid), dim3(kernels::kLanes), args, smem, st), "launch yz ring2");
+    launch_k(fn, grid, kernels::kLanes, args, smem, "launch yz ring2");
 }
 
 // Fused x+y on ring2 (xy2.cuh).
@@ -1175,11 +1205,17 @@ void DeviceSession::launch_residual_dirichlet(bool all_entries)
     const long long total = count * S_;
     const int block = 256;
     begin_kernel(kDirichlet);
-    kernels::dirichlet_entries<<<static_cast<unsigned>((total + block - 1) / block), block, 0,
-                                 static_cast<cudaStream_t>(stream_)>>>(
-        rho_, S_, count, (all_entries ? dir_all_voxel_ : dir_res_voxel_) + first,
-        (all_entries ? dir_all_mask_ : dir_res_mask_) + first * S_,
-        (all_entries ? dir_all_values_ : dir_res_values_) + first * S_);
+    {
+        double* rho = rho_;
+        int S = S_;
+        long long cnt = count;
+        const int64_t* vox = (all_entries ? dir_all_voxel_ : dir_res_voxel_) + first;
+        const unsigned char* mask = (all_entries ? dir_all_mask_ : dir_res_mask_) + first * S_;
+        const double* vals = (all_entries ? dir_all_values_ : dir_res_values_) + first * S_;
+        void* args[] = {&rho, &S, &cnt, &vox, &mask, &vals};
+        launch_k(reinterpret_cast<const void*>(kernels::dirichlet_entries),
+                 static_cast<unsigned>((total + block - 1) / block), block, args, 0, "dirichlet entries");
+    }
     end_kernel(kDirichlet);
 }
 
@@ -1221,10 +1257,19 @@ void DeviceSession::launch_sources(double dt)
     const long long total = cap * S_;
     const int block = 128;
     begin_kernel(kSources);
-    kernels::sources_groups<<<static_cast<unsigned>((total + block - 1) / block), block, 0,
-                              static_cast<cudaStream_t>(stream_)>>>(rho_, S_, rep_groups_ + r0, rep_groups_ + r0 + nr,
-                                                                    group_voxel_, group_offsets_, agent_add_,
-                                                                    agent_den_);
+    {
+        double* rho = rho_;
+        int S = S_;
+        const int64_t* glo = rep_groups_ + r0;
+        const int64_t* ghi = rep_groups_ + r0 + nr;
+        const int64_t* gv = group_voxel_;
+        const int64_t* go = group_offsets_;
+        const double* add = agent_add_;
+        const double* den = agent_den_;
+        void* args[] = {&rho, &S, &glo, &ghi, &gv, &go, &add, &den};
+        launch_k(reinterpret_cast<const void*>(kernels::sources_groups),
+                 static_cast<unsigned>((total + block - 1) / block), block, args, 0, "sources");
+    }
     end_kernel(kSources);
 }
 

@@ -216,6 +216,8 @@ private:
     bool xy_cluster_pays() const;
     bool xyz_cluster_pays() const;
     int long_line_hint(int nch) const;
+    void launch_k(const void* fn, unsigned grid, unsigned block, void** args, std::size_t smem, const char* what);
+    bool pdl_ = false; // programmatic dependent launch of the step kernels
     int l2_hints_ = 0;               // ring2 L2 cache hints, BIODIFF_L2_HINTS bitmask (1 loads, 2 stores)
     int l2_keep_from8_ = 4; // L2 hint bit 2: reloaded chunks k >= keep_from8/8 of them keep their first load
     // Ensembles: replica batches that stay resident in L2 across several

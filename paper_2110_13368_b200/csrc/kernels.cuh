@@ -856,6 +856,8 @@ static __global__ void __launch_bounds__(128) sweep_global(GlobalSweep a)
 static __global__ void dirichlet_entries(double* rho, int S, long long count, const int64_t* voxel,
                                   const unsigned char* mask, const double* values)
 {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= count * S) return;
     if (mask[t]) rho[voxel[t / S] * S + (t % S)] = values[t];
@@ -893,6 +895,8 @@ static __global__ void sources_groups(double* rho, int S, const int64_t* g_lo, c
                                const int64_t* group_voxel, const int64_t* group_offsets, const double* add,
                                const double* den)
 {
+    ptx::griddep_wait();
+    ptx::griddep_launch();
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     const long long g0 = *g_lo;
     if (t >= (*g_hi - g0) * S) return;

@@ -142,6 +142,12 @@ __device__ __forceinline__ void tma_prefetch_desc(const void* tmap)
     asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }
 
+// Programmatic dependent launch: wait for the preceding grid (complete,
+// memory visible) / allow the next grid to launch. No-ops unless the launch
+// carries the programmatic-serialization attribute.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 
 // Waits until all of this thread's bulk stores have finished READING shared memory.

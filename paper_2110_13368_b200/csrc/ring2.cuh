@@ -409,6 +409,8 @@ __global__ void __launch_bounds__(kLanes) sweep_yz_ring2(const __grid_constant__
     const int G = gridDim.x;
     int t = blockIdx.x;
     if (t >= a.tiles) return;
+    ptx::griddep_wait();
+    ptx::griddep_launch();
     struct TileAt {
         int e0, outer, r;
     };
@@ -512,6 +514,8 @@ __global__ void __launch_bounds__(kLanes) sweep_x_ring2(const __grid_constant__ 
     const long long G = gridDim.x;
     long long t = blockIdx.x;
     if (t >= a.tiles) return;
+    ptx::griddep_wait();
+    ptx::griddep_launch();
     const int nch = (a.nx + kChunk - 1) / kChunk;
     const uint64_t keep_pol = ptx::policy_evict_last(), stream_pol = ptx::policy_evict_first();
     auto issue = [&](int P, int j0, int k, int slot, bool reload = false) {

@@ -252,6 +252,8 @@ __device__ __forceinline__ void xyc_body(const CUtensorMap* tmap_x, const CUtens
     const int nw = static_cast<int>(cluster_nctarank()) * wpc;       // warps per cluster
     const uint32_t base = ptx::smem_addr(smem_xyc);
     unsigned char* mine = smem_xyc + (((base + 1023u) & ~1023u) - base) + static_cast<size_t>(warp) * a.warp_bytes;
+    ptx::griddep_wait();
+    ptx::griddep_launch();
     Ring2Smem sm;
     sm.slots = reinterpret_cast<double*>(mine);
     sm.bars = reinterpret_cast<uint64_t*>(mine + NS * kSlot * 8);
