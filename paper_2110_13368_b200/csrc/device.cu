@@ -201,6 +201,9 @@ DeviceSession::~DeviceSession()
         dfree(w.cb);
         dfree(w.dconst);
         dfree(w.cconst);
+        dfree(w.dinvT);
+        dfree(w.cbT);
+        dfree(w.settle_r);
     }
     dfree(rho_);
     dfree(dir_all_voxel_);
@@ -347,24 +350,30 @@ void DeviceSession::set_workspace(Axis axis, int n, int dims, double dt, const d
     dfree(w.cconst);
     dfree(w.dinvT);
     dfree(w.cbT);
+    dfree(w.settle_r);
     // Ensembles: replicas_ consecutive coefficient sets (q[R*S], dinv/cb[R*n*S]);
-    // the settle row is the max over replicas (warp-uniform in the kernels).
+    // the settle row is the max over replicas (warp-uniform in the kernels);
+    // ring2 / cluster tiles hold one replica each and use the replica's own
+    // settle row (settle_r) instead.
     const std::size_t set = static_cast<std::size_t>(n) * S_;
     w.q = dalloc_copy(q, static_cast<std::size_t>(S_) * replicas_, st);
     w.dinv = dalloc_copy(dinv, set * replicas_, st);
     w.cb = dalloc_copy(cb, set * replicas_, st);
     std::vector<double> dc, cc;
     w.settle = 0;
+    std::vector<int> sr(static_cast<std::size_t>(replicas_));
     for (int r = 0; r < replicas_; ++r) {
         std::vector<double> dcr, ccr;
-        w.settle = std::max(w.settle, settle_row(n, S_, dinv + r * set, cb + r * set, dcr, ccr));
+        sr[r] = settle_row(n, S_, dinv + r * set, cb + r * set, dcr, ccr);
+        w.settle = std::max(w.settle, sr[r]);
         dc.insert(dc.end(), dcr.begin(), dcr.end());
         cc.insert(cc.end(), ccr.begin(), ccr.end());
     }
-    if (std::getenv("BIODIFF_NO_SETTLE")) w.settle = n;
-#ifdef BIODIFF_DIAG_SETTLE1
-    w.settle = 1; // design probe only: wrong results, unsettled-row cost removed
-#endif
+    if (std::getenv("BIODIFF_NO_SETTLE")) {
+        w.settle = n;
+        for (int& v : sr) v = n;
+    }
+    if (replicas_ > 1 && !std::getenv("BIODIFF_SETTLE_MAX")) w.settle_r = dalloc_copy(sr.data(), sr.size(), st);
     w.dconst = dalloc_copy(dc.data(), dc.size(), st);
     w.cconst = dalloc_copy(cc.data(), cc.size(), st);
     {   // Substrate-major copies (same bits) for ring2's unsettled rows.
@@ -645,9 +654,10 @@ void DeviceSession::launch_sweep(Axis axis, bool clamp)
     const int rowlen = mesh_.nx * S;
     kernels::Clamp cl{shell_values_, clamp ? shell_mask_ : 0ull, z0_, nzg_};
     const bool do_clamp = clamp && shell_mask_ != 0;
-    const kernels::Coef coef{w.q,        w.dinv, w.cb, w.dconst, w.cconst, w.settle, static_cast<long long>(w.n) * S,
-                             w.dinvT, w.cbT, w.n};
     const SweepPath p = path_[ax];
+    // per-replica settle rows only for ring2 (one replica per tile)
+    const kernels::Coef coef{w.q,        w.dinv, w.cb, w.dconst, w.cconst, w.settle, static_cast<long long>(w.n) * S,
+                             w.dinvT, w.cbT, w.n, p == SweepPath::smem_ring2 ? w.settle_r : nullptr};
     const bool bulk = p == SweepPath::smem_bulk;
     begin_kernel(ax);
     if (p == SweepPath::global) {
@@ -811,7 +821,7 @@ void DeviceSession::launch_xy_cluster(bool three)
     const DeviceWorkspace& wy = ws_[1];
     kernels::XYCluster a{};
     a.xcoef = kernels::Coef{wx.q,     wx.dinv, wx.cb, wx.dconst, wx.cconst, wx.settle, static_cast<long long>(wx.n) * S,
-                            wx.dinvT, wx.cbT, wx.n};
+                            wx.dinvT, wx.cbT, wx.n, wx.settle_r};
     a.nx = mesh_.nx;
     a.ny = mesh_.ny;
     a.nz = mesh_.nz;
@@ -823,7 +833,7 @@ void DeviceSession::launch_xy_cluster(bool three)
     a.yi = (a.rowlen + kernels::kLanes - 1) / kernels::kLanes;
     kernels::StridedSweep& y = a.y;
     y.coef = kernels::Coef{wy.q,     wy.dinv, wy.cb, wy.dconst, wy.cconst, wy.settle, static_cast<long long>(wy.n) * S,
-                           wy.dinvT, wy.cbT, wy.n};
+                           wy.dinvT, wy.cbT, wy.n, wy.settle_r};
     y.axis = 1;
     y.n = mesh_.ny;
     y.n_outer = mesh_.nz;
@@ -835,7 +845,7 @@ void DeviceSession::launch_xy_cluster(bool three)
         const DeviceWorkspace& wz = ws_[2];
         kernels::StridedSweep& z = a.z;
         z.coef = kernels::Coef{wz.q,     wz.dinv, wz.cb, wz.dconst, wz.cconst, wz.settle,
-                               static_cast<long long>(wz.n) * S, wz.dinvT, wz.cbT, wz.n};
+                               static_cast<long long>(wz.n) * S, wz.dinvT, wz.cbT, wz.n, wz.settle_r};
         z.axis = 2;
         z.n = mesh_.nz;
         z.n_outer = mesh_.ny;
@@ -909,12 +919,14 @@ void DeviceSession::launch_xy_cluster(bool three)
     end_kernel(kc);
 }
 
-// Ensembles: one cluster per replica for all three sweeps when every warp of
-// a cluster has an item per phase and the replicas the clusters hold at once
-// roughly fit in L2 (C5: 33-37 x 4.2 MB). BIODIFF_XYZ_CLUSTER=0/1 forces.
+// Ensembles: one cluster per replica for all three sweeps. Opt-in
+// (BIODIFF_XYZ_CLUSTER=1): with per-replica settle rows the separate ring2
+// sweeps are faster at C5 (2.613 vs 2.659 ms per step; before them the
+// clusters led, 2.785 vs 2.98 ms). "auto" would take it when every warp of a
+// cluster has an item per phase and the in-flight replicas roughly fit L2.
 bool DeviceSession::xyz_cluster_pays() const
 {
-    const std::string m = env_or("BIODIFF_XYZ_CLUSTER", "auto");
+    const std::string m = env_or("BIODIFF_XYZ_CLUSTER", "0");
     if (m == "0") return false;
     if (replicas_ <= 1 || !ws_[1].active || !ws_[2].active || slab_ || batch_replicas_ > 0) return false;
     if (!(S_ == 1 || S_ == 2 || S_ == 4)) return false;
@@ -1149,9 +1161,9 @@ void DeviceSession::launch_xy2()
     const DeviceWorkspace& wy = ws_[1];
     kernels::XYFused2 a{};
     a.xcoef = kernels::Coef{wx.q,     wx.dinv, wx.cb, wx.dconst, wx.cconst, wx.settle, static_cast<long long>(wx.n) * S,
-                            wx.dinvT, wx.cbT, wx.n};
+                            wx.dinvT, wx.cbT, wx.n, wx.settle_r};
     a.ycoef = kernels::Coef{wy.q,     wy.dinv, wy.cb, wy.dconst, wy.cconst, wy.settle, static_cast<long long>(wy.n) * S,
-                            wy.dinvT, wy.cbT, wy.n};
+                            wy.dinvT, wy.cbT, wy.n, wy.settle_r};
     a.nx = mesh_.nx;
     a.ny = mesh_.ny;
     a.nz = mesh_.nz;

@@ -45,7 +45,8 @@ struct DeviceWorkspace {
     double* cconst = nullptr; // [S] settled c_back
     double* dinvT = nullptr;  // [R][S][n] denom_inv, substrate-major (ring2 unsettled rows)
     double* cbT = nullptr;    // [R][S][n] c_back
-    int settle = 0;           // first row of the bit-constant region (n = none)
+    int settle = 0;           // first row of the bit-constant region (n = none); max over replicas
+    int* settle_r = nullptr;  // [R] per-replica settle rows (ensembles), or nullptr
 };
 
 // Which kernel implementation a sweep uses (chosen per axis at set-up; the

@@ -52,6 +52,7 @@ struct Coef {
     const double* dinvT = nullptr; // [R][S][n]: the same bits per substrate row-contiguous (ring2:
     const double* cbT = nullptr;   // row m0 + u of a chunk is an immediate offset from one base)
     int n = 0;
+    const int* settle_r = nullptr; // [R] per-replica settle rows (ring2 / cluster chains), or nullptr: settle
 };
 
 __device__ __forceinline__ double fwd_first(double v, double d) { return __dmul_rn(v, d); }
@@ -243,7 +244,7 @@ __device__ __forceinline__ Chain make_chain(const Coef& coef, int S, int s, int 
     c.q = coef.q[r * S + s];
     c.dc = coef.dconst[r * S + s];
     c.cc = coef.cconst[r * S + s];
-    c.settle = coef.settle;
+    c.settle = coef.settle_r ? __ldg(coef.settle_r + r) : coef.settle;
     c.n = n;
     c.s = s;
     c.ts = coef.n;
