@@ -128,12 +128,19 @@ int biodiff_agent_grouping(biodiff_session* session, int64_t* groups, int64_t* g
  *                         the session stream) for movers running on the GPU
  *   rebuild_voxel_grouping: agents.cpp:56-73 on the device; status 2 with
  *                         mesh.cpp:74-76's message if a position left the
- *                         domain (the grouping is then empty). */
+ *                         domain (the previous grouping is kept, as in the
+ *                         reference)
+ *   sample_agent_densities: what every agent senses — the density values of
+ *                         its cached voxel (field.values[agent.voxel*S + s],
+ *                         mesh.hpp:62-90, agents.hpp:22) — into host
+ *                         out[n*S] in agent-index order; agents outside this
+ *                         session's voxels (other z-slabs) read NaN. */
 int biodiff_agent_count(biodiff_session* session, int64_t* n);
 int biodiff_set_agent_positions(biodiff_session* session, const double* xyz, int64_t n);
 int biodiff_set_agent_position(biodiff_session* session, int64_t id, const double* xyz);
 int biodiff_agent_positions_device(biodiff_session* session, double** xyz);
 int biodiff_rebuild_voxel_grouping(biodiff_session* session);
+int biodiff_sample_agent_densities(biodiff_session* session, double* out, int64_t count);
 
 /* The device's agents in agent-index order (null outputs are skipped):
  * ids[n], xyz[3n], volume[n], secretion/uptake/saturation[n*S]. */
@@ -169,6 +176,9 @@ typedef struct biodiff_clock {
     int64_t per_mech, per_cell, total_steps;           /* derived by biodiff_clock_make */
     int64_t diffusion_steps, mechanics_steps, cell_steps; /* counters (in/out of a run) */
     double t_now;                                      /* diffusion_steps * dt_diff */
+    int64_t pending; /* boundary hooks not yet completed (1 snapshot, 2 mechanics, 4 cell): counters are
+                        bumped when a boundary is reached; a hook that aborts the run keeps its bit and
+                        is re-run first when the run resumes */
 } biodiff_clock;
 
 typedef struct biodiff_run_metrics {
@@ -232,6 +242,11 @@ int biodiff_cell_sources_sinks_step(biodiff_session* session, double dt);
  * (captured once into a CUDA graph per (steps-chunk, with_sources)). */
 int biodiff_advance(biodiff_session* session, int64_t steps, double dt, int32_t with_sources);
 
+/* Captures and instantiates the CUDA graphs biodiff_advance(steps, dt,
+ * with_sources) replays, without running any step (a timed advance then
+ * excludes the one-time capture). Same argument checks as biodiff_advance. */
+int biodiff_prepare_advance(biodiff_session* session, int64_t steps, double dt, int32_t with_sources);
+
 /* Blocks until all queued work of the session is done. */
 int biodiff_synchronize(biodiff_session* session);
 
@@ -291,12 +306,48 @@ int biodiff_zslab_create(const biodiff_mesh* global_mesh, int32_t substrates, in
                          biodiff_session** out);
 int biodiff_zslab_info(biodiff_session* session, int32_t* z0, int32_t* z1, int32_t* nz_global);
 
+/* ---- substrate shards (new) -------------------------------
+ * Substrates are independent in every part of the step (coefficients per
+ * substrate solver.cpp:72-95, Dirichlet masks per substrate solver.cpp:273,
+ * the reaction update per substrate agents.cpp:103-108), so a session may
+ * hold substrates [s0, s1) of an S-substrate problem and run with no
+ * communication; its results are bit-identical to those columns of the
+ * unsharded run. A shard may also be a z-slab (planes [z0, z1); pass 0, nz
+ * for the whole mesh): S/k substrate shards x P z-slabs.
+ * Like z-slabs, a shard takes the GLOBAL inputs — set_substrates(D[S],
+ * lambda[S]), set_dirichlet(mask/values [count*S]), set_agents(rates
+ * [n*S]), load_agents_csv(names[S]), fill_field(initial[S]) — and keeps
+ * its share. Field buffers of upload_field / download_field / nested /
+ * sample_agent_densities / download_agents are in the shard's own layout
+ * (values[v*(s1-s0) + s - s0] over its voxels); upload_field_global /
+ * download_field_global move the shard's part of a GLOBAL a1-layout field
+ * (values[v*S + s], every voxel of the global mesh; only the shard's
+ * columns and planes are read / written). save_agents_csv needs every
+ * substrate and is refused on a shard (status 2). */
+int biodiff_shard_create(const biodiff_mesh* global_mesh, int32_t substrates, int32_t s0, int32_t s1, int32_t z0,
+                         int32_t z1, int32_t device, biodiff_session** out);
+int biodiff_shard_info(biodiff_session* session, int32_t* s0, int32_t* s1, int32_t* substrates);
+int biodiff_upload_field_global(biodiff_session* session, const double* values, int64_t count);
+int biodiff_download_field_global(biodiff_session* session, double* values, int64_t count);
+
 /* One slab per process: NCCL communicator over all slabs (rank = slab index,
  * ordered by z). biodiff_nccl_unique_id fills 128 bytes on rank 0, to be
  * broadcast by the caller. biodiff_advance then runs the exchanges on the
  * session stream. */
 int biodiff_nccl_unique_id(uint8_t* out);
 int biodiff_zslab_connect_nccl(biodiff_session* session, const uint8_t* unique_id, int32_t nranks, int32_t rank);
+
+/* The same one-slab-per-process step with the planes moved by the CALLER:
+ * fn(user, send, send_peer, recv, recv_peer, count) must send `count`
+ * doubles from host `send` (when non-null) to rank send_peer and receive
+ * `count` doubles from recv_peer into host `recv` (when non-null); return 0
+ * on success. Called on the advancing thread, in the NCCL path's order and
+ * pieces (e.g. over a gloo process group; also how a non-NCCL caller plugs
+ * its own transport in). */
+typedef int (*biodiff_plane_exchange)(void* user, const double* send, int32_t send_peer, double* recv,
+                                      int32_t recv_peer, int64_t count);
+int biodiff_zslab_connect_host(biodiff_session* session, int32_t nranks, int32_t rank, biodiff_plane_exchange fn,
+                               void* user);
 
 /* Several slabs in one process (one or more GPUs): link them in z order and
  * advance them together (device/peer copies move the planes). */

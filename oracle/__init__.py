@@ -122,6 +122,8 @@ def ref_lib():
         L.ref_mutant_check.argtypes = [_P(ctypes.c_int)]
         L.ref_format_double.argtypes = [_d, ctypes.c_char_p, ctypes.c_int]
         L.ref_format_int.argtypes = [_i64, ctypes.c_char_p, ctypes.c_int]
+        L.ref_cross_check.argtypes = [_P(_d), _P(_d), _i64, ctypes.c_int, _d, _d, _P(_d), _P(_d), _P(_i64),
+                                      _P(ctypes.c_int)]
         L.ref_translate_vector_to_array.argtypes = [_P(_P(_d)), _P(_i64), _i64, _P(_d), _P(ctypes.c_int)]
         L.ref_translate_round_trip.argtypes = [_P(_d), _i64, ctypes.c_int, _P(_d)]
         L.ref_load_agents.argtypes = [_vp, ctypes.c_char_p, _P(ctypes.c_char_p), ctypes.c_int]
@@ -374,6 +376,16 @@ def ref_format_double(v: float) -> str:
     buf = ctypes.create_string_buffer(64)
     _rchk(ref_lib().ref_format_double(v, buf, 64))
     return buf.value.decode()
+
+
+def ref_cross_check(a, b, substrates: int, abs_tol: float, rel_tol: float):
+    """The reference's own cross_check (validation.cpp:112-137): (max_abs, max_rel, worst index, pass)."""
+    a = np.ascontiguousarray(a, np.float64)
+    b = np.ascontiguousarray(b, np.float64)
+    ma, mr, wi, p = _d(), _d(), _i64(), ctypes.c_int()
+    _rchk(ref_lib().ref_cross_check(_dp(a), _dp(b), a.size, substrates, abs_tol, rel_tol, ctypes.byref(ma),
+                                    ctypes.byref(mr), ctypes.byref(wi), ctypes.byref(p)))
+    return ma.value, mr.value, int(wi.value), bool(p.value)
 
 
 def ref_mutant_check():

@@ -181,6 +181,23 @@ int ref_translate_round_trip(const double* flat, int64_t count, int S, double* o
     });
 }
 
+// cross_check (validation.cpp:112-137) of the reference on two flat fields.
+int ref_cross_check(const double* a, const double* b, int64_t count, int S, double abs_tol, double rel_tol,
+                    double* max_abs, double* max_rel, int64_t* worst, int* pass)
+{
+    return guarded([&] {
+        DensityField fa, fb;
+        fa.substrates = fb.substrates = S;
+        fa.values.assign(a, a + count);
+        fb.values.assign(b, b + count);
+        const CrossCheckReport r = cross_check(fa, fb, abs_tol, rel_tol);
+        *max_abs = r.max_abs;
+        *max_rel = r.max_rel;
+        *worst = r.worst_value_index;
+        *pass = r.pass ? 1 : 0;
+    });
+}
+
 // format_int (text.cpp:16-21).
 int ref_format_int(int64_t v, char* out, int cap)
 {

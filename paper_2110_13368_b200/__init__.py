@@ -90,6 +90,8 @@ _d = ctypes.c_double
 _i32 = ctypes.c_int32
 _i64 = ctypes.c_int64
 _vp = ctypes.c_void_p
+# biodiff_plane_exchange (include/biodiff_b200.h)
+PLANE_EXCHANGE = ctypes.CFUNCTYPE(ctypes.c_int, _vp, _P(_d), _i32, _P(_d), _i32, _i64)
 
 _SIGNATURES = {
     "biodiff_last_error": (ctypes.c_char_p, []),
@@ -107,6 +109,7 @@ _SIGNATURES = {
     "biodiff_agent_grouping": (ctypes.c_int, [_vp, _P(_i64), _P(_i64), _P(_i64), _P(_i64)]),
     "biodiff_agent_count": (ctypes.c_int, [_vp, _P(_i64)]),
     "biodiff_set_agent_positions": (ctypes.c_int, [_vp, _P(_d), _i64]),
+    "biodiff_sample_agent_densities": (ctypes.c_int, [_vp, _P(_d), _i64]),
     "biodiff_set_agent_position": (ctypes.c_int, [_vp, _i64, _P(_d)]),
     "biodiff_agent_positions_device": (ctypes.c_int, [_vp, _P(_vp)]),
     "biodiff_rebuild_voxel_grouping": (ctypes.c_int, [_vp]),
@@ -131,7 +134,13 @@ _SIGNATURES = {
     "biodiff_apply_dirichlet": (ctypes.c_int, [_vp]),
     "biodiff_diffuse_decay_step": (ctypes.c_int, [_vp]),
     "biodiff_cell_sources_sinks_step": (ctypes.c_int, [_vp, _d]),
+    "biodiff_shard_create": (ctypes.c_int, [_P(Mesh), _i32, _i32, _i32, _i32, _i32, _i32, _P(_vp)]),
+    "biodiff_shard_info": (ctypes.c_int, [_vp, _P(_i32), _P(_i32), _P(_i32)]),
+    "biodiff_upload_field_global": (ctypes.c_int, [_vp, _P(_d), _i64]),
+    "biodiff_download_field_global": (ctypes.c_int, [_vp, _P(_d), _i64]),
+    "biodiff_zslab_connect_host": (ctypes.c_int, [_vp, _i32, _i32, PLANE_EXCHANGE, _vp]),
     "biodiff_advance": (ctypes.c_int, [_vp, _i64, _d, _i32]),
+    "biodiff_prepare_advance": (ctypes.c_int, [_vp, _i64, _d, _i32]),
     "biodiff_synchronize": (ctypes.c_int, [_vp]),
     "biodiff_session_stream": (ctypes.c_int, [_vp, _P(_vp)]),
     "biodiff_set_kernel_timing": (ctypes.c_int, [_vp, _i32]),
@@ -288,18 +297,35 @@ class Session:
     replaces WorkerPool& (backend.hpp:34). Mirrors the reference entry
     points; the field stays on the device until :meth:`download_field`."""
 
-    def __init__(self, mesh: Mesh, substrates: int, device: int = 0, zslab=None, replicas: int = 1):
+    def __init__(self, mesh: Mesh, substrates: int, device: int = 0, zslab=None, replicas: int = 1, shard=None):
         """zslab=(z0, z1): a z-slab session owning global planes [z0, z1) of
         `mesh` (the global mesh); its field holds only those planes.
+        shard=(s0, s1): a substrate shard holding substrates [s0, s1) of the
+        `substrates`-substrate problem (combinable with zslab). Parameter
+        arrays (set_substrates, set_dirichlet, set_agents, fill_field) are
+        GLOBAL ([substrates] columns); field buffers are the session's own
+        layout (``S`` = s1 - s0 values per voxel), or GLOBAL through
+        upload_field_global / download_field_global.
         replicas > 1: an ensemble of independent microenvironments stacked
         replica-major (values[(r*voxels + v)*S + s])."""
         self.mesh = mesh
+        self.S_total = int(substrates)
         self.S = int(substrates)
         self.zslab = None
+        self.shard = None
         self.replicas = int(replicas)
         h = _vp()
         if self.replicas > 1:
             _check(lib().biodiff_ensemble_create(ctypes.byref(mesh), self.S, self.replicas, device, ctypes.byref(h)))
+        elif shard is not None:
+            s0, s1 = (int(x) for x in shard)
+            z0, z1 = (int(z) for z in zslab) if zslab is not None else (0, int(mesh.nz))
+            _check(lib().biodiff_shard_create(ctypes.byref(mesh), self.S_total, s0, s1, z0, z1, device,
+                                              ctypes.byref(h)))
+            self.shard = (s0, s1)
+            self.S = s1 - s0
+            if (z0, z1) != (0, int(mesh.nz)):
+                self.zslab = (z0, z1)
         elif zslab is None:
             _check(lib().biodiff_session_create(ctypes.byref(mesh), self.S, device, ctypes.byref(h)))
         else:
@@ -314,6 +340,22 @@ class Session:
         buf = (ctypes.c_uint8 * 128)()
         _check(lib().biodiff_nccl_unique_id(buf))
         return bytes(buf)
+
+    def connect_host_transport(self, nranks: int, rank: int, exchange):
+        """One slab per process with the planes moved by `exchange(send, send_peer,
+        recv, recv_peer)` (numpy views of the pinned staging planes, or None):
+        send `send` to rank send_peer, fill `recv` from recv_peer (e.g. gloo)."""
+        def cb(_user, send, send_peer, recv, recv_peer, count):
+            try:
+                sv = np.ctypeslib.as_array(send, (count,)) if send else None
+                rv = np.ctypeslib.as_array(recv, (count,)) if recv else None
+                exchange(sv, int(send_peer), rv, int(recv_peer))
+                return 0
+            except BaseException as e:  # surfaced by the failing call
+                self._xchg_error = e
+                return 1
+        self._xchg_cb = PLANE_EXCHANGE(cb)  # keep alive as long as the session
+        _check(lib().biodiff_zslab_connect_host(self._h, nranks, rank, self._xchg_cb, None))
 
     def connect_nccl(self, unique_id: bytes, nranks: int, rank: int):
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(unique_id)
@@ -371,7 +413,8 @@ class Session:
     # -- set-up ---------------------------------------------------------
     def set_substrates(self, diffusion, decay, dt: float):
         """SolverWorkspaces::build (solver.cpp:277-287) + upload."""
-        _check(lib().biodiff_set_substrates(self._h, _dptr(_f64(diffusion, self.S)), _dptr(_f64(decay, self.S)), dt))
+        _check(lib().biodiff_set_substrates(self._h, _dptr(_f64(diffusion, self.S_total)),
+                                            _dptr(_f64(decay, self.S_total)), dt))
 
     def set_workspace(self, axis: int, dims: int, dt: float, off_diag, denom_inv, c_back):
         n = (self.mesh.nx, self.mesh.ny, self.mesh.nz)[axis]
@@ -381,8 +424,8 @@ class Session:
     def set_dirichlet(self, voxels, mask, values):
         """DirichletMap entries (mesh.hpp:113-141); add-merge semantics."""
         v = np.ascontiguousarray(np.asarray(voxels, dtype=np.int64).ravel())
-        m = np.ascontiguousarray(np.asarray(mask, dtype=np.uint8).reshape(v.size * self.S))
-        x = _f64(values, v.size * self.S)
+        m = np.ascontiguousarray(np.asarray(mask, dtype=np.uint8).reshape(v.size * self.S_total))
+        x = _f64(values, v.size * self.S_total)
         _check(lib().biodiff_set_dirichlet(self._h, v.size, v.ctypes.data_as(_P(_i64)),
                                            m.ctypes.data_as(_P(ctypes.c_uint8)), _dptr(x)))
 
@@ -392,7 +435,8 @@ class Session:
         n = ids.size
         _check(lib().biodiff_set_agents(
             self._h, n, ids.ctypes.data_as(_P(_i64)), _dptr(_f64(positions, 3 * n)), _dptr(_f64(volume, n)),
-            _dptr(_f64(secretion, n * self.S)), _dptr(_f64(uptake, n * self.S)), _dptr(_f64(saturation, n * self.S))))
+            _dptr(_f64(secretion, n * self.S_total)), _dptr(_f64(uptake, n * self.S_total)),
+            _dptr(_f64(saturation, n * self.S_total))))
 
     def agent_grouping(self):
         g = _i64()
@@ -434,6 +478,16 @@ class Session:
         """AgentPopulation::rebuild_voxel_grouping (agents.cpp:56-73), on the device."""
         _check(lib().biodiff_rebuild_voxel_grouping(self._h))
 
+    def sample_agent_densities(self, out=None):
+        """Densities at every agent's voxel (after the last rebuild) as [n, S], agent-index
+        order; agents outside this session's voxels read NaN. `out` may be a
+        preallocated (pinned) float64 buffer of n*S values."""
+        n, S = self.agent_count(), self.S
+        if out is None:
+            out = np.empty((n, S))
+        _check(lib().biodiff_sample_agent_densities(self._h, _dptr(out), n * S))
+        return out
+
     def download_agents(self):
         """(ids, xyz[n,3], volume, secretion[n,S], uptake[n,S], saturation[n,S]) in agent-index order."""
         n, S = self.agent_count(), self.S
@@ -450,13 +504,13 @@ class Session:
 
     def load_agents_csv(self, path: str, names):
         """load_agents (config.cpp:416-477) + set_agents."""
-        if len(names) != self.S:
+        if len(names) != self.S_total:
             raise ValueError("one name per substrate")
         _check(lib().biodiff_load_agents_csv(self._h, str(path).encode(), self._names(names)))
 
     def save_agents_csv(self, path: str, names):
         """save_agents (config.cpp:479-491) of the device's current agents."""
-        if len(names) != self.S:
+        if len(names) != self.S_total:
             raise ValueError("one name per substrate")
         _check(lib().biodiff_save_agents_csv(self._h, str(path).encode(), self._names(names)))
 
@@ -488,7 +542,19 @@ class Session:
 
     def fill_field(self, initial):
         """Every voxel := initial[S] (Microenvironment::create's initial condition)."""
-        _check(lib().biodiff_fill_field(self._h, _dptr(_f64(initial, self.S))))
+        _check(lib().biodiff_fill_field(self._h, _dptr(_f64(initial, self.S_total))))
+
+    def upload_field_global(self, values):
+        """This session's planes / substrate columns of a GLOBAL a1-layout field."""
+        a = _f64(values, self.mesh.voxel_count * self.S_total)
+        _check(lib().biodiff_upload_field_global(self._h, _dptr(a), a.size))
+
+    def download_field_global(self, out: np.ndarray) -> np.ndarray:
+        """Writes this session's planes / substrate columns into a GLOBAL a1-layout field."""
+        if out.dtype != np.float64 or not out.flags.c_contiguous or out.size != self.mesh.voxel_count * self.S_total:
+            raise ValueError("out must be a contiguous float64 global field")
+        _check(lib().biodiff_download_field_global(self._h, _dptr(out), out.size))
+        return out
 
     def download_field(self, out: Optional[np.ndarray] = None) -> np.ndarray:
         if out is None:
@@ -510,7 +576,16 @@ class Session:
         _check(lib().biodiff_cell_sources_sinks_step(self._h, dt))
 
     def advance(self, steps: int, dt: float, with_sources: bool = True):
-        _check(lib().biodiff_advance(self._h, int(steps), dt, 1 if with_sources else 0))
+        rc = lib().biodiff_advance(self._h, int(steps), dt, 1 if with_sources else 0)
+        err = getattr(self, "_xchg_error", None)
+        if rc != 0 and err is not None:  # a host-transport callback failed: its exception
+            self._xchg_error = None
+            raise err
+        _check(rc)
+
+    def prepare_advance(self, steps: int, dt: float, with_sources: bool = True):
+        """Instantiates the graphs advance(steps, ...) replays, running nothing."""
+        _check(lib().biodiff_prepare_advance(self._h, int(steps), dt, 1 if with_sources else 0))
 
     def synchronize(self):
         _check(lib().biodiff_synchronize(self._h))

@@ -156,6 +156,20 @@ __global__ void rep_group_bounds(const int64_t* group_voxel, const int64_t* coun
     rep_groups[r] = r == R ? G : lo;
 }
 
+// The densities each grouped agent senses (its cached voxel's values, the
+// reference's field.values[agent.voxel * S + s]) in input order; agents
+// outside this session's voxels (other z-slabs) keep the NaN fill.
+__global__ void agent_sample(const int64_t* keys_sorted, const int64_t* order, const int64_t* counts, long long N,
+                             int S, const double* rho, double* out)
+{
+    const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (t >= N * S) return;
+    const long long i = t / S;
+    if (i >= counts[1]) return;
+    const int s = static_cast<int>(t % S);
+    out[order[i] * S + s] = rho[keys_sorted[i] * S + s];
+}
+
 int bits_for(long long v)
 {
     int b = 1;
@@ -173,7 +187,7 @@ void DeviceSession::release_agents()
                      &agent_counts_, &rep_groups_})
         dfree(*p);
     for (auto** p : {&in_pos_, &in_vol_, &in_sec_, &in_upt_, &in_sat_, &agent_volume_, &agent_secretion_,
-                     &agent_uptake_, &agent_saturation_, &agent_add_, &agent_den_})
+                     &agent_uptake_, &agent_saturation_, &agent_add_, &agent_den_, &agent_sample_})
         dfree(*p);
     dfree(in_rep_);
     dfree(flags_);
@@ -296,12 +310,25 @@ void DeviceSession::rebuild_voxel_grouping()
     const int end_bit = bits_for(m.sentinel);
     const unsigned long long none = ~0ull;
     ck(cudaMemcpyAsync(agent_bad_, &none, sizeof(none), cudaMemcpyHostToDevice, st), "reset");
-    ck(cudaMemsetAsync(agent_counts_, 0, 2 * sizeof(long long), st), "reset");
-    ck(cudaMemsetAsync(group_offsets_, 0, sizeof(long long), st), "reset");
     const int block = 256;
     begin_kernel(kAux);
     agent_keys<<<blocks(N, block), block, 0, st>>>(in_pos_, in_rep_, N, m, id_order_, keys_a_, agent_bad_);
     end_kernel(kAux);
+    // The domain check comes before any group array is touched: a failed
+    // rebuild keeps the previous grouping, as the reference does (its
+    // nearest_voxel throws before groups_ is reassigned, agents.cpp:56-73).
+    unsigned long long bad = 0;
+    ck(cudaMemcpyAsync(&bad, agent_bad_, sizeof(bad), cudaMemcpyDeviceToHost, st), "download");
+    ck(cudaStreamSynchronize(st), "sync");
+    if (bad != ~0ull) {
+        // mesh.cpp:74-76 (nearest_voxel's std::domain_error, same message).
+        double p[3];
+        ck(cudaMemcpy(p, in_pos_ + 3 * bad, sizeof(p), cudaMemcpyDeviceToHost), "download");
+        throw std::domain_error("position (" + format_double(p[0]) + "," + format_double(p[1]) + "," +
+                                format_double(p[2]) + ") outside the simulation domain");
+    }
+    ck(cudaMemsetAsync(agent_counts_, 0, 2 * sizeof(long long), st), "reset");
+    ck(cudaMemsetAsync(group_offsets_, 0, sizeof(long long), st), "reset");
     std::size_t bytes = cub_bytes_;
     ck(cub::DeviceRadixSort::SortPairs(cub_tmp_, bytes, keys_a_, keys_b_, id_order_, vals_b_, N, 0, end_bit, st),
        "cub sort");
@@ -323,23 +350,29 @@ void DeviceSession::rebuild_voxel_grouping()
     rep_group_bounds<<<blocks(replicas_ + 1, block), block, 0, st>>>(group_voxel_, agent_counts_, m.key_span,
                                                                       replicas_, rep_groups_);
     end_kernel(kAux);
-    unsigned long long bad = 0;
     long long counts[2] = {0, 0};
-    ck(cudaMemcpyAsync(&bad, agent_bad_, sizeof(bad), cudaMemcpyDeviceToHost, st), "download");
     ck(cudaMemcpyAsync(counts, agent_counts_, sizeof(counts), cudaMemcpyDeviceToHost, st), "download");
     ck(cudaStreamSynchronize(st), "sync");
     factors_valid_ = false;
     groups_ = counts[0];
     grouped_agents_ = counts[1];
-    if (bad != ~0ull) {
-        // mesh.cpp:74-76 (nearest_voxel's std::domain_error, same message).
-        double p[3];
-        ck(cudaMemcpy(p, in_pos_ + 3 * bad, sizeof(p), cudaMemcpyDeviceToHost), "download");
-        groups_ = 0;
-        grouped_agents_ = 0;
-        throw std::domain_error("position (" + format_double(p[0]) + "," + format_double(p[1]) + "," +
-                                format_double(p[2]) + ") outside the simulation domain");
-    }
+}
+
+void DeviceSession::sample_agent_densities(double* out, std::int64_t count)
+{
+    if (count != n_agents_ * S_) throw std::invalid_argument("sample buffer size does not match agents x substrates");
+    if (count == 0) return;
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    auto st = static_cast<cudaStream_t>(stream_);
+    if (!agent_sample_) dalloc(agent_sample_, count);
+    ck(cudaMemsetAsync(agent_sample_, 0xff, sizeof(double) * count, st), "memset"); // NaN
+    const int block = 256;
+    begin_kernel(kAux);
+    agent_sample<<<blocks(count, block), block, 0, st>>>(keys_b_, vals_b_, agent_counts_, n_agents_, S_, rho_,
+                                                         agent_sample_);
+    end_kernel(kAux);
+    ck(cudaMemcpyAsync(out, agent_sample_, sizeof(double) * count, cudaMemcpyDeviceToHost, st), "download");
+    ck(cudaStreamSynchronize(st), "sync");
 }
 
 void DeviceSession::set_agent_positions(const double* xyz, std::int64_t n)

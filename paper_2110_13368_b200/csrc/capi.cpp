@@ -10,22 +10,26 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <optional>
 #include <memory>
 #include <new>
 #include <string>
+#include <type_traits>
 
 using namespace biodiff_b200;
 
 struct biodiff_session {
     std::unique_ptr<DeviceSession> dev;
     CartesianMesh mesh; // the GLOBAL mesh (for a z-slab, dev->mesh() is the slab)
-    int S = 0;
+    int S = 0;          // substrates of the GLOBAL problem (parameter arrays are [S])
+    int s0 = 0, s1 = 0; // substrate shard [s0, s1) held by this session (all: 0, S)
     bool slab = false;
     int z0 = 0, z1 = 0; // slab planes [z0, z1)
     int replicas = 1;   // ensemble size (stacked replica-major)
+    bool sharded() const { return s1 - s0 != S; }
 };
 
 namespace {
@@ -110,6 +114,33 @@ void need(const void* p, const char* what)
     if (!p) throw std::invalid_argument(std::string("null pointer: ") + what);
 }
 
+// A substrate shard keeps columns [s0, s1) of every per-substrate array.
+template <class T>
+std::vector<T> columns(const T* a, std::int64_t rows, int S, int s0, int s1)
+{
+    std::vector<T> out(static_cast<std::size_t>(rows) * (s1 - s0));
+    for (std::int64_t r = 0; r < rows; ++r)
+        std::copy(a + r * S + s0, a + r * S + s1, out.begin() + r * (s1 - s0));
+    return out;
+}
+
+// The shard's view of a validated population (same agents and ids, rates of
+// substrates [s0, s1) only). Substrates are independent in the reaction
+// update (agents.cpp:103-108), so the shard's result columns are bitwise
+// those of the unsharded step.
+AgentPopulation shard_population(const biodiff_session* s, const AgentPopulation& pop)
+{
+    if (!s->sharded()) return pop;
+    std::vector<CellAgent> v = pop.agents();
+    for (CellAgent& c : v) {
+        auto cut = [&](std::vector<double>& x) { x = std::vector<double>(x.begin() + s->s0, x.begin() + s->s1); };
+        cut(c.secretion_rates);
+        cut(c.uptake_rates);
+        cut(c.saturation_densities);
+    }
+    return AgentPopulation(std::move(v), s->mesh, s->s1 - s->s0);
+}
+
 // Uploads SolverWorkspaces built on the GLOBAL mesh. For a z-slab the z
 // workspace is sliced to the slab's rows (the global factorisation, so the
 // zero-inflow slab solve is the reference recurrence minus the inflow terms)
@@ -124,7 +155,7 @@ void upload_workspaces(biodiff_session* s, const SolverWorkspaces& ws)
         return;
     }
     if (!ws.x) throw state_error("solver workspaces not built");
-    const int S = s->S;
+    const int S = s->s1 - s->s0; // the workspaces hold the shard's substrates
     auto put = [&](const std::optional<SolverWorkspace>& w) {
         if (w) d.set_workspace(w->axis, w->n, w->dims, w->dt, w->off_diag.data(), w->denom_inv.data(), w->c_back.data());
     };
@@ -296,6 +327,7 @@ int biodiff_session_create(const biodiff_mesh* mesh, int32_t substrates, int32_t
         auto s = std::make_unique<biodiff_session>();
         s->mesh = to_mesh(mesh);
         s->S = substrates;
+        s->s1 = substrates;
         s->dev = std::make_unique<DeviceSession>(s->mesh, substrates, device);
         *out = s.release();
     });
@@ -311,11 +343,16 @@ int biodiff_set_substrates(biodiff_session* session, const double* diffusion, co
     return guarded([&] {
         need(diffusion, "diffusion");
         need(decay, "decay");
+        dev(session);
+        // Every substrate of the global problem is validated; a shard builds
+        // the workspaces of its own (the coefficients are per-substrate, so
+        // the bits equal the unsharded build's columns, solver.cpp:72-95).
         std::vector<SubstrateParams> params;
-        for (int s = 0; s < dev(session).substrates(); ++s) {
+        for (int s = 0; s < session->S; ++s) {
             if (diffusion[s] < 0.0) throw config_error("substrate has negative diffusion coefficient");
             if (decay[s] < 0.0) throw config_error("substrate has negative decay rate");
-            params.push_back({"s" + std::to_string(s), diffusion[s], decay[s], 0.0});
+            if (s >= session->s0 && s < session->s1)
+                params.push_back({"s" + std::to_string(s), diffusion[s], decay[s], 0.0});
         }
         upload_workspaces(session, SolverWorkspaces::build(session->mesh, params, dt));
     });
@@ -343,12 +380,24 @@ int biodiff_set_dirichlet(biodiff_session* session, int64_t count, const int64_t
             need(values, "values");
         }
         DeviceSession& d = dev(session);
-        const int S = d.substrates();
+        const int S = session->S;
         DirichletMap map;
         for (int64_t e = 0; e < count; ++e)
             map.add(voxel[e], std::vector<std::uint8_t>(mask + e * S, mask + (e + 1) * S),
                     std::vector<double>(values + e * S, values + (e + 1) * S),
                     session->mesh.voxel_count() * session->replicas, S);
+        if (session->sharded()) { // the merged entries' columns [s0, s1); entries that clamp none of them go
+            const int s0 = session->s0, s1 = session->s1;
+            DirichletMap cut;
+            for (const auto& e : map.entries()) {
+                std::vector<std::uint8_t> m(e.mask.begin() + s0, e.mask.begin() + s1);
+                if (std::none_of(m.begin(), m.end(), [](std::uint8_t b) { return b != 0; })) continue;
+                cut.add(e.voxel, std::move(m), std::vector<double>(e.values.begin() + s0, e.values.begin() + s1),
+                        session->mesh.voxel_count(), s1 - s0);
+            }
+            map = std::move(cut);
+        }
+        const int SL = session->s1 - session->s0;
         if (!session->slab) {
             d.set_dirichlet(map);
         } else { // keep the slab's entries, in local voxel indices
@@ -357,7 +406,7 @@ int biodiff_set_dirichlet(biodiff_session* session, int64_t count, const int64_t
             DirichletMap local;
             for (const auto& e : map.entries())
                 if (e.voxel >= lo && e.voxel < hi)
-                    local.add(e.voxel - lo, e.mask, e.values, hi - lo, S);
+                    local.add(e.voxel - lo, e.mask, e.values, hi - lo, SL);
             d.set_dirichlet(local);
         }
     });
@@ -376,10 +425,12 @@ std::vector<std::string> substrate_names(const biodiff_session* session, const c
     return v;
 }
 
-void install_agents(biodiff_session* session, const AgentPopulation& pop)
+// `pop` holds all S substrates; a shard installs its columns.
+void install_agents(biodiff_session* session, const AgentPopulation& full)
 {
     DeviceSession& d = dev(session);
     if (session->replicas > 1) throw state_error("ensembles take agents through biodiff_ensemble_set_agents");
+    const AgentPopulation pop = shard_population(session, full);
     if (!session->slab) {
         d.set_agents(pop);
     } else {
@@ -404,8 +455,8 @@ int biodiff_set_agents(biodiff_session* session, int64_t n, const int64_t* ids, 
             need(uptake, "uptake");
             need(saturation, "saturation");
         }
-        DeviceSession& d = dev(session);
-        const int S = d.substrates();
+        dev(session);
+        const int S = session->S;
         std::vector<CellAgent> agents(static_cast<std::size_t>(n));
         for (int64_t a = 0; a < n; ++a) {
             CellAgent& c = agents[a];
@@ -416,7 +467,6 @@ int biodiff_set_agents(biodiff_session* session, int64_t n, const int64_t* ids, 
             c.uptake_rates.assign(uptake + a * S, uptake + (a + 1) * S);
             c.saturation_densities.assign(saturation + a * S, saturation + (a + 1) * S);
         }
-        (void)d;
         install_agents(session, AgentPopulation(std::move(agents), session->mesh, S)); // host validation
     });
 }
@@ -472,6 +522,14 @@ int biodiff_rebuild_voxel_grouping(biodiff_session* session)
     return guarded([&] { dev(session).rebuild_voxel_grouping(); });
 }
 
+int biodiff_sample_agent_densities(biodiff_session* session, double* out, int64_t count)
+{
+    return guarded([&] {
+        need(out, "out");
+        dev(session).sample_agent_densities(out, count);
+    });
+}
+
 int biodiff_download_agents(biodiff_session* session, int64_t* ids, double* xyz, double* volume, double* secretion,
                             double* uptake, double* saturation)
 {
@@ -494,6 +552,9 @@ int biodiff_save_agents_csv(biodiff_session* session, const char* path, const ch
         need(path, "path");
         const auto v = substrate_names(session, names);
         DeviceSession& d = dev(session);
+        if (session->sharded())
+            throw state_error("a substrate shard holds only its substrates' rates: save agents from an unsharded "
+                              "session");
         const std::int64_t n = d.agent_count();
         const int S = session->S;
         std::vector<std::int64_t> ids(n);
@@ -528,6 +589,7 @@ void to_c_clock(const SimulationClock& c, biodiff_clock* o)
     o->mechanics_steps = c.mechanics_steps;
     o->cell_steps = c.cell_steps;
     o->t_now = c.t_now();
+    o->pending = c.pending;
 }
 
 } // namespace
@@ -552,6 +614,8 @@ int biodiff_run_simulation(biodiff_session* session, biodiff_clock* clock, int32
         c.diffusion_steps = clock->diffusion_steps;
         c.mechanics_steps = clock->mechanics_steps;
         c.cell_steps = clock->cell_steps;
+        if (clock->pending & ~std::int64_t{7}) throw std::invalid_argument("unknown pending bits in the clock");
+        c.pending = clock->pending;
         auto wrap = [&](biodiff_hook h, const char* which) -> std::function<void(const SimulationClock&)> {
             if (!h) return {};
             return [h, user, which](const SimulationClock& k) {
@@ -666,7 +730,53 @@ int biodiff_fill_field(biodiff_session* session, const double* initial)
 {
     return guarded([&] {
         need(initial, "initial");
-        dev(session).fill(initial);
+        dev(session).fill(initial + session->s0);
+    });
+}
+
+int biodiff_upload_field_global(biodiff_session* session, const double* values, int64_t count)
+{
+    return guarded([&] {
+        need(values, "values");
+        DeviceSession& d = dev(session);
+        if (session->replicas > 1) throw state_error("ensembles upload their stacked field with biodiff_upload_field");
+        if (count != session->mesh.voxel_count() * session->S)
+            throw state_error("global field size does not match the global mesh and substrates");
+        const std::int64_t plane = static_cast<std::int64_t>(session->mesh.nx) * session->mesh.ny;
+        const std::int64_t v0 = session->slab ? session->z0 * plane : 0;
+        const double* src = values + v0 * session->S;
+        if (!session->sharded()) {
+            d.upload(src, d.value_count());
+            return;
+        }
+        const std::int64_t nvox = d.value_count() / d.substrates();
+        const std::vector<double> packed = columns(src, nvox, session->S, session->s0, session->s1);
+        d.upload(packed.data(), static_cast<std::int64_t>(packed.size()));
+        d.synchronize();
+    });
+}
+
+int biodiff_download_field_global(biodiff_session* session, double* values, int64_t count)
+{
+    return guarded([&] {
+        need(values, "values");
+        DeviceSession& d = dev(session);
+        if (session->replicas > 1) throw state_error("ensembles download their stacked field with biodiff_download_field");
+        if (count != session->mesh.voxel_count() * session->S)
+            throw state_error("global field size does not match the global mesh and substrates");
+        const std::int64_t plane = static_cast<std::int64_t>(session->mesh.nx) * session->mesh.ny;
+        const std::int64_t v0 = session->slab ? session->z0 * plane : 0;
+        double* dst = values + v0 * session->S;
+        if (!session->sharded()) {
+            d.download(dst, d.value_count());
+            return;
+        }
+        const int SL = d.substrates();
+        std::vector<double> packed(static_cast<std::size_t>(d.value_count()));
+        d.download(packed.data(), d.value_count());
+        const std::int64_t nvox = d.value_count() / SL;
+        for (std::int64_t v = 0; v < nvox; ++v)
+            std::copy(packed.begin() + v * SL, packed.begin() + (v + 1) * SL, dst + v * session->S + session->s0);
     });
 }
 
@@ -701,6 +811,11 @@ int biodiff_cell_sources_sinks_step(biodiff_session* session, double dt)
 int biodiff_advance(biodiff_session* session, int64_t steps, double dt, int32_t with_sources)
 {
     return guarded([&] { dev(session).advance(steps, dt, with_sources != 0); });
+}
+
+int biodiff_prepare_advance(biodiff_session* session, int64_t steps, double dt, int32_t with_sources)
+{
+    return guarded([&] { dev(session).prepare_advance(steps, dt, with_sources != 0); });
 }
 
 int biodiff_synchronize(biodiff_session* session)
@@ -779,6 +894,7 @@ int biodiff_ensemble_create(const biodiff_mesh* mesh, int32_t substrates, int32_
         auto s = std::make_unique<biodiff_session>();
         s->mesh = to_mesh(mesh);
         s->S = substrates;
+        s->s1 = substrates;
         s->replicas = replicas;
         s->dev = std::make_unique<DeviceSession>(s->mesh, substrates, device, replicas);
         *out = s.release();
@@ -876,6 +992,7 @@ int biodiff_zslab_create(const biodiff_mesh* global_mesh, int32_t substrates, in
         s->mesh = to_mesh(global_mesh);
         if (z0 < 0 || z1 > s->mesh.nz || z0 >= z1) throw config_error("z-slab planes must satisfy 0 <= z0 < z1 <= nz");
         s->S = substrates;
+        s->s1 = substrates;
         s->slab = true;
         s->z0 = z0;
         s->z1 = z1;
@@ -886,6 +1003,49 @@ int biodiff_zslab_create(const biodiff_mesh* global_mesh, int32_t substrates, in
         s->dev = std::make_unique<DeviceSession>(local, substrates, device);
         s->dev->configure_slab(s->mesh.nz, z0);
         *out = s.release();
+    });
+}
+
+int biodiff_shard_create(const biodiff_mesh* global_mesh, int32_t substrates, int32_t s0, int32_t s1, int32_t z0,
+                         int32_t z1, int32_t device, biodiff_session** out)
+{
+    return guarded([&] {
+        need(out, "out");
+        *out = nullptr;
+        auto s = std::make_unique<biodiff_session>();
+        s->mesh = to_mesh(global_mesh);
+        if (substrates < 1) throw config_error("a shard needs at least one substrate");
+        if (s0 < 0 || s1 > substrates || s0 >= s1)
+            throw config_error("substrate shard must satisfy 0 <= s0 < s1 <= substrates");
+        if (z0 < 0 || z1 > s->mesh.nz || z0 >= z1) throw config_error("z-slab planes must satisfy 0 <= z0 < z1 <= nz");
+        s->S = substrates;
+        s->s0 = s0;
+        s->s1 = s1;
+        CartesianMesh local = s->mesh;
+        s->slab = !(z0 == 0 && z1 == s->mesh.nz);
+        if (s->slab) {
+            s->z0 = z0;
+            s->z1 = z1;
+            local.nz = z1 - z0;
+            local.z_min = s->mesh.z_min + z0 * s->mesh.dz;
+            local.z_max = s->mesh.z_min + z1 * s->mesh.dz;
+        }
+        s->dev = std::make_unique<DeviceSession>(local, s1 - s0, device);
+        if (s->slab) s->dev->configure_slab(s->mesh.nz, z0);
+        *out = s.release();
+    });
+}
+
+int biodiff_shard_info(biodiff_session* session, int32_t* s0, int32_t* s1, int32_t* substrates)
+{
+    return guarded([&] {
+        need(s0, "s0");
+        need(s1, "s1");
+        need(substrates, "substrates");
+        dev(session);
+        *s0 = session->s0;
+        *s1 = session->s1;
+        *substrates = session->S;
     });
 }
 
@@ -916,6 +1076,16 @@ int biodiff_zslab_connect_nccl(biodiff_session* session, const uint8_t* unique_i
         need(unique_id, "unique_id");
         if (!session || !session->slab) throw state_error("not a z-slab session");
         dev(session).connect_nccl(unique_id, nranks, rank);
+    });
+}
+
+int biodiff_zslab_connect_host(biodiff_session* session, int32_t nranks, int32_t rank, biodiff_plane_exchange fn,
+                               void* user)
+{
+    return guarded([&] {
+        if (!session || !session->slab) throw state_error("not a z-slab session");
+        static_assert(std::is_same_v<DeviceSession::HostExchange, biodiff_plane_exchange>, "callback ABI");
+        dev(session).connect_host_transport(nranks, rank, fn, user);
     });
 }
 

@@ -1320,7 +1320,7 @@ void DeviceSession::apply_dirichlet()
 // solver.cpp:289-299 with the clamp fused into the last active sweep.
 void DeviceSession::step_body(bool with_sources, double dt)
 {
-    if (slab_ && nccl_comm_) { // one slab per rank: exchanges on this stream (slab.cu)
+    if (slab_ && remote_) { // one slab per rank: exchanges on this stream (slab.cu)
         slab_step_nccl(with_sources, dt);
         return;
     }
@@ -1358,52 +1358,84 @@ void DeviceSession::sources(double dt)
     launch_sources(dt);
 }
 
+// The body advance() runs (or captures) for n steps.
+void DeviceSession::advance_body(std::int64_t n, double dt, bool with_sources)
+{
+    const bool batched = batch_replicas_ > 0 && !slab_ && path_[0] == SweepPath::smem_ring2 &&
+                         (!ws_[1].active || path_[1] == SweepPath::smem_ring2) &&
+                         (!ws_[2].active || path_[2] == SweepPath::smem_ring2) && !xy_fusable();
+    if (batched)
+        step_body_batches(with_sources, dt, n);
+    else
+        for (std::int64_t s = 0; s < n; ++s) step_body(with_sources, dt);
+}
+
+bool DeviceSession::uses_graphs() const { return !(timing_ || slab_ || std::getenv("BIODIFF_NO_GRAPH")); }
+
+// The instantiated graph of n steps (captured on first use).
+std::pair<void*, int>& DeviceSession::graph_for(std::int64_t n, double dt, bool with_sources)
+{
+    std::uint64_t bits;
+    std::memcpy(&bits, &dt, sizeof(bits));
+    GraphKey key{n, with_sources, bits};
+    auto it = graphs_.find(key);
+    if (it == graphs_.end()) {
+        auto st = static_cast<cudaStream_t>(stream_);
+        const std::int64_t before = launches_;
+        cudaGraph_t graph;
+        ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+        advance_body(n, dt, with_sources);
+        ck(cudaStreamEndCapture(st, &graph), "end capture");
+        cudaGraphExec_t exec;
+        ck(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
+        cudaGraphDestroy(graph);
+        const int kernels_in_graph = static_cast<int>(launches_ - before);
+        launches_ = before;
+        it = graphs_.emplace(key, std::make_pair(static_cast<void*>(exec), kernels_in_graph)).first;
+    }
+    return it->second;
+}
+
+void DeviceSession::check_advance(std::int64_t steps, double dt) const
+{
+    if (steps < 0) throw std::invalid_argument("step count must be non-negative");
+    if (!(dt > 0.0)) throw std::invalid_argument("reaction step size must be positive");
+    check_ready(Axis::x);
+    if (std::memcmp(&dt, &dt_, sizeof(double)) != 0)
+        throw state_error("advance dt does not match the solver workspace dt");
+}
+
+// Captures and instantiates every graph advance(steps, dt, with_sources)
+// would replay, without running anything: a caller that times advance()
+// excludes the one-time capture cost.
+void DeviceSession::prepare_advance(std::int64_t steps, double dt, bool with_sources)
+{
+    if (steps == 0) return;
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    check_advance(steps, dt);
+    if (with_sources) ensure_source_factors(dt);
+    if (!uses_graphs()) return;
+    if (steps / kGraphSteps) graph_for(kGraphSteps, dt, with_sources);
+    if (steps % kGraphSteps) graph_for(steps % kGraphSteps, dt, with_sources);
+}
+
 void DeviceSession::advance(std::int64_t steps, double dt, bool with_sources)
 {
     if (steps < 0) throw std::invalid_argument("step count must be non-negative");
     if (steps == 0) return;
-    if (!(dt > 0.0)) throw std::invalid_argument("reaction step size must be positive");
     ck(cudaSetDevice(device_), "cudaSetDevice");
-    check_ready(Axis::x);
-    if (std::memcmp(&dt, &dt_, sizeof(double)) != 0)
-        throw state_error("advance dt does not match the solver workspace dt");
+    check_advance(steps, dt);
     auto st = static_cast<cudaStream_t>(stream_);
     if (with_sources) ensure_source_factors(dt); // not inside the graph capture
-    const bool batched = batch_replicas_ > 0 && !slab_ && path_[0] == SweepPath::smem_ring2 &&
-                         (!ws_[1].active || path_[1] == SweepPath::smem_ring2) &&
-                         (!ws_[2].active || path_[2] == SweepPath::smem_ring2) && !xy_fusable();
-    auto body = [&](std::int64_t n) {
-        if (batched)
-            step_body_batches(with_sources, dt, n);
-        else
-            for (std::int64_t s = 0; s < n; ++s) step_body(with_sources, dt);
-    };
-    if (timing_ || slab_ || std::getenv("BIODIFF_NO_GRAPH")) {
-        body(steps);
+    if (!uses_graphs()) {
+        advance_body(steps, dt, with_sources);
         return;
     }
-    // Launch-bound small grids: replay a captured graph of up to kGraphSteps steps.
-    constexpr std::int64_t kGraphSteps = 50;
+    // Replay captured graphs of up to kGraphSteps steps (launch gaps vanish).
     auto run_chunk = [&](std::int64_t n) {
-        std::uint64_t bits;
-        std::memcpy(&bits, &dt, sizeof(bits));
-        GraphKey key{n, with_sources, bits};
-        auto it = graphs_.find(key);
-        if (it == graphs_.end()) {
-            const std::int64_t before = launches_;
-            cudaGraph_t graph;
-            ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
-            body(n);
-            ck(cudaStreamEndCapture(st, &graph), "end capture");
-            cudaGraphExec_t exec;
-            ck(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
-            cudaGraphDestroy(graph);
-            const int kernels_in_graph = static_cast<int>(launches_ - before);
-            launches_ = before;
-            it = graphs_.emplace(key, std::make_pair(static_cast<void*>(exec), kernels_in_graph)).first;
-        }
-        ck(cudaGraphLaunch(static_cast<cudaGraphExec_t>(it->second.first), st), "graph launch");
-        launches_ += it->second.second;
+        auto& g = graph_for(n, dt, with_sources);
+        ck(cudaGraphLaunch(static_cast<cudaGraphExec_t>(g.first), st), "graph launch");
+        launches_ += g.second;
     };
     const std::int64_t full = steps / kGraphSteps;
     for (std::int64_t c = 0; c < full; ++c) run_chunk(kGraphSteps);

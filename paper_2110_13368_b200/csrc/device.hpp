@@ -103,6 +103,8 @@ public:
     // Group CSR in (voxel, id) order: returns G; voxel[G], offsets[G+1], order[grouped agents].
     std::int64_t download_grouping(std::int64_t* group_voxel, std::int64_t* group_offsets, std::int64_t* order);
     void download_agents(std::int64_t* ids, double* pos, double* vol, double* sec, double* upt, double* sat);
+    // Densities at each agent's voxel (after the last rebuild), host out[N*S] in input order.
+    void sample_agent_densities(double* out, std::int64_t count);
 
     void upload(const double* values, std::int64_t count);
     void fill(const double* initial); // [S] per-substrate initial condition
@@ -113,6 +115,7 @@ public:
     void diffuse_decay_step();             // x, y, z (+ fused clamp) + residual clamp
     void sources(double dt);               // cell_sources_sinks_step
     void advance(std::int64_t steps, double dt, bool with_sources);
+    void prepare_advance(std::int64_t steps, double dt, bool with_sources); // capture graphs, run nothing
     void synchronize();
     void* stream() const { return stream_; }
     void event_record(int slot);
@@ -140,8 +143,16 @@ public:
     // Responses to a unit inflow at the slab top (Phi, back-substituted) and
     // bottom (psi), [n*S], and the forward response at the last row [S].
     void set_slab_spikes(const double* Phi, const double* psi, const double* phi_last);
-    // Neighbour transports: NCCL (one slab per rank) or in-process.
+    // Neighbour transports: NCCL (one slab per rank), a host callback (one
+    // slab per rank; the planes cross the host — e.g. a gloo process group —
+    // through pinned buffers), or in-process.
     void connect_nccl(const unsigned char* unique_id, int nranks, int rank);
+    // fn(user, send, send_peer, recv, recv_peer, count) moves `count` doubles:
+    // `send` (host, or null) to rank send_peer and from recv_peer into `recv`
+    // (host, or null); non-zero return = failure.
+    using HostExchange = int (*)(void* user, const double* send, std::int32_t send_peer, double* recv,
+                                 std::int32_t recv_peer, std::int64_t count);
+    void connect_host_transport(int nranks, int rank, HostExchange fn, void* user);
     static void link_local(const std::vector<DeviceSession*>& slabs);
     static void group_advance(const std::vector<DeviceSession*>& slabs, std::int64_t steps, double dt,
                               bool with_sources);
@@ -162,11 +173,16 @@ private:
     double* plane_xin_ = nullptr;      // X_{p+1} received (0 on the last slab)
     double* plane_xtop_ = nullptr;     // X_p, sent to slab p-1
     void* nccl_comm_ = nullptr;
+    HostExchange host_xchg_ = nullptr; // host-callback transport
+    void* host_xchg_user_ = nullptr;
+    double* host_send_ = nullptr;      // pinned staging planes of the host transport
+    double* host_recv_ = nullptr;
+    bool remote_ = false;              // one slab per rank (NCCL or host transport)
     int nccl_rank_ = 0, nccl_ranks_ = 1;
     DeviceSession* prev_slab_ = nullptr; // in-process transport
     DeviceSession* next_slab_ = nullptr;
-    bool has_prev() const { return nccl_comm_ ? nccl_rank_ > 0 : prev_slab_ != nullptr; }
-    bool has_next() const { return nccl_comm_ ? nccl_rank_ < nccl_ranks_ - 1 : next_slab_ != nullptr; }
+    bool has_prev() const { return remote_ ? nccl_rank_ > 0 : prev_slab_ != nullptr; }
+    bool has_next() const { return remote_ ? nccl_rank_ < nccl_ranks_ - 1 : next_slab_ != nullptr; }
     void slab_phase_xy();   // x, y sweeps + the interface pre-pass (dhat, xhat0)
     void slab_phase_fwdfix(std::int64_t off, std::int64_t count);
     void slab_phase_topfix(std::int64_t off, std::int64_t count);
@@ -193,6 +209,11 @@ private:
     void launch_residual_dirichlet(bool all_entries);
     void launch_sources(double dt);
     void step_body(bool with_sources, double dt);
+    void advance_body(std::int64_t n, double dt, bool with_sources);
+    void check_advance(std::int64_t steps, double dt) const;
+    bool uses_graphs() const;
+    static constexpr std::int64_t kGraphSteps = 50; // steps per captured graph
+    std::pair<void*, int>& graph_for(std::int64_t n, double dt, bool with_sources);
     void begin_kernel(int cls);
     void end_kernel(int cls);
     void invalidate_graphs();
@@ -288,6 +309,7 @@ private:
     double* agent_saturation_ = nullptr;
     double* agent_add_ = nullptr;     // [N*S] (f*sec)*target for factors_dt_
     double* agent_den_ = nullptr;     // [N*S] 1 + f*(sec+upt)
+    double* agent_sample_ = nullptr;  // [N*S] sample_agent_densities scratch
     std::uint64_t factors_dt_bits_ = 0;
     bool factors_valid_ = false;
     void ensure_source_factors(double dt);

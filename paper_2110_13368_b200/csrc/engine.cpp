@@ -78,33 +78,86 @@ RunMetrics run_simulation(DeviceSession& session, SimulationClock& clock, bool w
         snap_every = static_cast<std::int64_t>(std::llround(hooks.snapshot_interval / clock.dt_diff));
         if (snap_every < 1) throw config_error("snapshot interval shorter than one diffusion step");
     }
-    std::int64_t next_snap = snap_every;
-    while (clock.diffusion_steps < clock.total_steps) {
-        std::int64_t n = std::min(clock.per_mech - clock.diffusion_steps % clock.per_mech,
-                                  clock.total_steps - clock.diffusion_steps);
-        if (snap_every) n = std::min(n, next_snap - clock.diffusion_steps);
-        session.event_record(14);
-        session.advance(n, clock.dt_diff, with_sources);
-        session.event_record(15);
-        m.diffusion_seconds += session.event_elapsed(14, 15) / 1e3;
-        clock.diffusion_steps += n;
-        if (snap_every && clock.diffusion_steps == next_snap) {
-            const auto ts = std::chrono::steady_clock::now();
-            if (hooks.snapshot) hooks.snapshot(clock);
-            ++m.snapshots;
-            m.snapshot_seconds += seconds_since(ts);
-            next_snap += snap_every;
+    // Resume: the next snapshot is the first multiple of snap_every after the
+    // clock's position (a snapshot AT the position is pending or done).
+    std::int64_t next_snap = snap_every ? (clock.diffusion_steps / snap_every + 1) * snap_every : 0;
+
+    // Device time is accumulated per segment of uninterrupted device calls: an
+    // event pair around each segment, read (one host sync) only when a hook is
+    // about to run or at the end — null hooks never make the host wait.
+    bool open = false;
+    auto open_segment = [&] {
+        if (!open) {
+            session.event_record(14);
+            open = true;
         }
-        if (clock.diffusion_steps % clock.per_mech == 0) {
-            ++clock.mechanics_steps;
-            const auto th = std::chrono::steady_clock::now();
-            if (hooks.mechanics) hooks.mechanics(clock);
-            if (clock.mechanics_steps % clock.per_cell == 0) {
-                ++clock.cell_steps;
-                if (hooks.cell) hooks.cell(clock);
+    };
+    auto close_segment = [&] {
+        if (open) {
+            session.event_record(15);
+            m.diffusion_seconds += session.event_elapsed(14, 15) / 1e3;
+            open = false;
+        }
+    };
+    // Drains the pending boundary work in the reference order: snapshot,
+    // mechanics, cell. A hook that throws leaves its bit (and the later ones) set.
+    auto drain = [&] {
+        if (clock.pending & SimulationClock::kPendingSnapshot) {
+            if (hooks.snapshot) {
+                close_segment();
+                const auto ts = std::chrono::steady_clock::now();
+                hooks.snapshot(clock);
+                m.snapshot_seconds += seconds_since(ts);
             }
-            m.hook_seconds += seconds_since(th);
+            ++m.snapshots;
+            clock.pending &= ~SimulationClock::kPendingSnapshot;
         }
+        if (clock.pending & SimulationClock::kPendingMechanics) {
+            if (hooks.mechanics) {
+                close_segment();
+                const auto th = std::chrono::steady_clock::now();
+                hooks.mechanics(clock);
+                m.hook_seconds += seconds_since(th);
+            }
+            clock.pending &= ~SimulationClock::kPendingMechanics;
+        }
+        if (clock.pending & SimulationClock::kPendingCell) {
+            if (hooks.cell) {
+                close_segment();
+                const auto th = std::chrono::steady_clock::now();
+                hooks.cell(clock);
+                m.hook_seconds += seconds_since(th);
+            }
+            clock.pending &= ~SimulationClock::kPendingCell;
+        }
+    };
+    try {
+        drain(); // work left over from an aborted run
+        while (clock.diffusion_steps < clock.total_steps) {
+            std::int64_t n = std::min(clock.per_mech - clock.diffusion_steps % clock.per_mech,
+                                      clock.total_steps - clock.diffusion_steps);
+            if (snap_every) n = std::min(n, next_snap - clock.diffusion_steps);
+            open_segment();
+            session.advance(n, clock.dt_diff, with_sources);
+            clock.diffusion_steps += n;
+            if (snap_every && clock.diffusion_steps == next_snap) {
+                clock.pending |= SimulationClock::kPendingSnapshot;
+                next_snap += snap_every;
+            }
+            if (clock.diffusion_steps % clock.per_mech == 0) {
+                ++clock.mechanics_steps;
+                clock.pending |= SimulationClock::kPendingMechanics;
+                if (clock.mechanics_steps % clock.per_cell == 0) {
+                    ++clock.cell_steps;
+                    clock.pending |= SimulationClock::kPendingCell;
+                }
+            }
+            drain();
+        }
+        close_segment();
+    } catch (...) {
+        open = false; // the open segment's time is dropped with the aborted run
+        throw;
     }
     session.synchronize();
     m.wall_seconds = seconds_since(t0);

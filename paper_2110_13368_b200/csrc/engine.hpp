@@ -18,6 +18,11 @@ struct SimulationClock {
     double dt_diff = 0.01, dt_mech = 0.1, dt_cell = 6.0, t_max = 60.0;
     std::int64_t per_mech = 10, per_cell = 60, total_steps = 6000;
     std::int64_t diffusion_steps = 0, mechanics_steps = 0, cell_steps = 0;
+    // Boundary work not yet completed (a hook that threw is re-run first on
+    // resume): the counters are bumped when a boundary is reached, the bits
+    // are cleared when the matching hook returns.
+    enum : std::int64_t { kPendingSnapshot = 1, kPendingMechanics = 2, kPendingCell = 4 };
+    std::int64_t pending = 0;
     double t_now() const { return static_cast<double>(diffusion_steps) * dt_diff; }
     // Validated clock (config_error on non-integral ratios, config.cpp:237-244).
     static SimulationClock make(double dt_diff, double dt_mech, double dt_cell, double t_max);

@@ -1007,7 +1007,10 @@ static __global__ void fill_field(double* rho, long long total, const double* in
 }
 
 // cross_check (validation.cpp:112-137) reductions. Non-negative doubles
-// order like their bit patterns, so atomicMax on the bits is exact.
+// order like their bit patterns, so atomicMax on the bits is exact. NaN
+// differences behave as in the reference: every comparison with NaN is false,
+// so they neither fail the check nor enter max_abs / max_rel (fmax drops NaN
+// exactly like std::max(current, NaN) keeps `current`).
 static __global__ void cross_check_max(const double* a, const double* b, long long n, unsigned long long* max_abs_bits,
                                 unsigned long long* max_rel_bits, double abs_tol, double rel_tol, int* fail)
 {
@@ -1021,7 +1024,7 @@ static __global__ void cross_check_max(const double* a, const double* b, long lo
         const double rel = (diff == 0.0 || mag == 0.0) ? 0.0 : diff / mag;
         my_abs = fmax(my_abs, diff);
         my_rel = fmax(my_rel, rel);
-        if (diff > abs_tol + rel_tol * mag || diff != diff) my_fail = 1;
+        if (diff > abs_tol + rel_tol * mag) my_fail = 1;
     }
     for (int o = 16; o > 0; o >>= 1) {
         my_abs = fmax(my_abs, __shfl_xor_sync(0xffffffffu, my_abs, o));

@@ -158,16 +158,53 @@ void DeviceSession::connect_nccl(const unsigned char* unique_id, int nranks, int
     ck(cudaSetDevice(device_), "cudaSetDevice");
     ncclUniqueId id;
     std::memcpy(&id, unique_id, sizeof(id));
+    if (remote_ || prev_slab_ || next_slab_) throw state_error("z-slab transport already connected");
     ncclComm_t comm;
     nck(a.CommInitRank(&comm, nranks, id, rank), "ncclCommInitRank");
     nccl_comm_ = comm;
     nccl_rank_ = rank;
     nccl_ranks_ = nranks;
+    remote_ = true;
 }
 
+void DeviceSession::connect_host_transport(int nranks, int rank, HostExchange fn, void* user)
+{
+    if (!slab_) throw state_error("not a z-slab session");
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw config_error("bad transport rank / size");
+    if (!fn) throw std::invalid_argument("null exchange callback");
+    if (remote_ || prev_slab_ || next_slab_) throw state_error("z-slab transport already connected");
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    const std::size_t bytes = sizeof(double) * plane_count();
+    ck(cudaMallocHost(&host_send_, bytes), "cudaMallocHost");
+    ck(cudaMallocHost(&host_recv_, bytes), "cudaMallocHost");
+    host_xchg_ = fn;
+    host_xchg_user_ = user;
+    nccl_rank_ = rank;
+    nccl_ranks_ = nranks;
+    remote_ = true;
+}
+
+// The one exchange primitive of slab_step_remote: NCCL send/recv on the
+// session stream, or — host transport — the stream is drained, the send
+// piece staged to pinned memory, the callback moves it, and the received
+// piece is queued back onto the stream (same order, same pieces).
 void DeviceSession::nccl_exchange(double* send, int send_peer, double* recv, int recv_peer, std::int64_t count)
 {
     if (!send && !recv) return;
+    auto st0 = static_cast<cudaStream_t>(stream_);
+    if (!nccl_comm_) {
+        const std::size_t bytes = sizeof(double) * static_cast<std::size_t>(count);
+        if (send) ck(cudaMemcpyAsync(host_send_, send, bytes, cudaMemcpyDeviceToHost, st0), "D2H plane");
+        ck(cudaStreamSynchronize(st0), "sync");
+        if (host_xchg_(host_xchg_user_, send ? host_send_ : nullptr, send_peer, recv ? host_recv_ : nullptr, recv_peer,
+                       count) != 0)
+            throw state_error("z-slab plane exchange callback failed");
+        if (recv) {
+            ck(cudaMemcpyAsync(recv, host_recv_, bytes, cudaMemcpyHostToDevice, st0), "H2D plane");
+            ck(cudaStreamSynchronize(st0), "sync"); // the staging buffer is reused by the next exchange
+        }
+        return;
+    }
     NcclApi& a = nccl();
     auto comm = static_cast<ncclComm_t>(nccl_comm_);
     auto st = static_cast<cudaStream_t>(stream_);
@@ -184,7 +221,8 @@ std::vector<std::pair<std::int64_t, std::int64_t>> DeviceSession::plane_pieces()
 {
     const std::int64_t plane = plane_count();
     int want = std::max(1, std::atoi(std::getenv("BIODIFF_ZSLAB_PIECES") ? std::getenv("BIODIFF_ZSLAB_PIECES") : "8"));
-    const std::int64_t min_piece = (1 << 20) / 8;
+    const char* mp = std::getenv("BIODIFF_ZSLAB_MIN_PIECE"); // doubles per piece (tests: force several pieces)
+    const std::int64_t min_piece = std::max<std::int64_t>(S_, mp ? std::atoll(mp) : (1 << 20) / 8);
     want = static_cast<int>(std::max<std::int64_t>(1, std::min<std::int64_t>(want, plane / min_piece)));
     std::vector<std::pair<std::int64_t, std::int64_t>> pieces;
     const std::int64_t cols = plane / S_;
@@ -200,6 +238,7 @@ void DeviceSession::link_local(const std::vector<DeviceSession*>& slabs)
     for (std::size_t p = 0; p < slabs.size(); ++p) {
         DeviceSession* s = slabs[p];
         if (!s->slab_) throw state_error("link_local needs z-slab sessions");
+        if (s->remote_) throw state_error("z-slab transport already connected");
         if (p + 1 < slabs.size() && s->z0_ + s->mesh_.nz != slabs[p + 1]->z0_)
             throw config_error("z-slabs must be contiguous and in order");
         s->prev_slab_ = p > 0 ? slabs[p - 1] : nullptr;
@@ -273,8 +312,8 @@ void DeviceSession::slab_phase_finish(bool with_sources, double dt)
     if (with_sources) launch_sources(dt);
 }
 
-// One slab per rank: the two plane chains run on this stream through NCCL,
-// pipelined over plane pieces.
+// One slab per rank: the two plane chains run on this stream through the
+// rank transport (NCCL, or the host callback), pipelined over plane pieces.
 void DeviceSession::slab_step_nccl(bool with_sources, double dt)
 {
     slab_phase_xy();
@@ -300,12 +339,36 @@ void DeviceSession::group_advance(const std::vector<DeviceSession*>& slabs, std:
                                   bool with_sources)
 {
     const std::size_t P = slabs.size();
-    if (P == 0) return;
-    for (auto* s : slabs)
+    if (steps < 0) throw std::invalid_argument("step count must be non-negative");
+    if (P == 0 || steps == 0) return;
+    if (!(dt > 0.0)) throw std::invalid_argument("reaction step size must be positive");
+    // The checks advance() makes, for every slab.
+    for (auto* s : slabs) {
         if (!s->slab_) throw state_error("group advance needs z-slab sessions");
-    std::vector<cudaEvent_t> ev(P);
+        ck(cudaSetDevice(s->device_), "cudaSetDevice");
+        s->check_ready(Axis::x);
+        if (std::memcmp(&dt, &s->dt_, sizeof(double)) != 0)
+            throw state_error("advance dt does not match the solver workspace dt");
+    }
+    // Events are released on every exit path (a failed launch throws).
+    struct Events {
+        std::vector<cudaEvent_t> ev;
+        std::vector<int> dev;
+        ~Events()
+        {
+            for (std::size_t p = 0; p < ev.size(); ++p)
+                if (ev[p]) {
+                    cudaSetDevice(dev[p]);
+                    cudaEventDestroy(ev[p]);
+                }
+        }
+    } events;
+    events.ev.assign(P, nullptr);
+    events.dev.assign(P, 0);
+    std::vector<cudaEvent_t>& ev = events.ev;
     for (std::size_t p = 0; p < P; ++p) {
         ck(cudaSetDevice(slabs[p]->device_), "cudaSetDevice");
+        events.dev[p] = slabs[p]->device_;
         ck(cudaEventCreateWithFlags(&ev[p], cudaEventDisableTiming), "cudaEventCreate");
         if (with_sources) slabs[p]->ensure_source_factors(dt);
     }
@@ -356,7 +419,6 @@ void DeviceSession::group_advance(const std::vector<DeviceSession*>& slabs, std:
     for (std::size_t p = 0; p < P; ++p) {
         on(p);
         ck(cudaStreamSynchronize(stream(p)), "sync");
-        cudaEventDestroy(ev[p]);
     }
 }
 
@@ -369,6 +431,11 @@ void DeviceSession::release_slab()
     }
     if (nccl_comm_ && nccl().CommDestroy) nccl().CommDestroy(static_cast<ncclComm_t>(nccl_comm_));
     nccl_comm_ = nullptr;
+    if (host_send_) cudaFreeHost(host_send_);
+    if (host_recv_) cudaFreeHost(host_recv_);
+    host_send_ = host_recv_ = nullptr;
+    host_xchg_ = nullptr;
+    remote_ = false;
 }
 
 void DeviceSession::set_agents_range(const AgentPopulation& agents, const CartesianMesh& global_mesh,

@@ -24,7 +24,7 @@ _i64, _d = ctypes.c_int64, ctypes.c_double
 class CClock(ctypes.Structure):  # include/biodiff_b200.h biodiff_clock
     _fields_ = [("dt_diff", _d), ("dt_mech", _d), ("dt_cell", _d), ("t_max", _d), ("per_mech", _i64),
                 ("per_cell", _i64), ("total_steps", _i64), ("diffusion_steps", _i64), ("mechanics_steps", _i64),
-                ("cell_steps", _i64), ("t_now", _d)]
+                ("cell_steps", _i64), ("t_now", _d), ("pending", _i64)]
 
 
 class CMetrics(ctypes.Structure):  # biodiff_run_metrics
@@ -58,6 +58,7 @@ class SimulationClock:  # SPEC.md:275-281 (validated by the native SimulationClo
     diffusion_steps: int = 0
     mechanics_steps: int = 0
     cell_steps: int = 0
+    pending: int = 0  # boundary hooks still to run on resume (1 snapshot, 2 mechanics, 4 cell)
 
     def __post_init__(self):
         c = CClock()
@@ -70,13 +71,15 @@ class SimulationClock:  # SPEC.md:275-281 (validated by the native SimulationClo
 
     def _c(self) -> CClock:
         c = CClock()
-        for f in ("dt_diff", "dt_mech", "dt_cell", "t_max", "diffusion_steps", "mechanics_steps", "cell_steps"):
+        for f in ("dt_diff", "dt_mech", "dt_cell", "t_max", "diffusion_steps", "mechanics_steps", "cell_steps",
+                  "pending"):
             setattr(c, f, getattr(self, f))
         return c
 
     def _sync(self, c: CClock):
         self.diffusion_steps, self.mechanics_steps, self.cell_steps = (int(c.diffusion_steps),
                                                                        int(c.mechanics_steps), int(c.cell_steps))
+        self.pending = int(c.pending)
 
 
 @dataclass

@@ -161,18 +161,26 @@ def cross_check(a, b, substrates: int, abs_tol: float, rel_tol: float) -> CrossC
         raise ValueError("cross_check fields have different shapes")
     if abs_tol < 0 or rel_tol < 0:
         raise ValueError("cross_check tolerances must be non-negative")
-    diff = np.abs(a - b)
-    mag = np.maximum(np.abs(a), np.abs(b))
-    with np.errstate(divide="ignore", invalid="ignore"):
+    with np.errstate(invalid="ignore", divide="ignore", over="ignore"):
+        diff = np.abs(a - b)
+        # std::max(|a|, |b|) returns |a| unless |a| < |b| (a NaN |a| stays)
+        mag = np.where(np.abs(a) < np.abs(b), np.abs(b), np.abs(a))
         rel = np.where((diff == 0) | (mag == 0), 0.0, diff / np.where(mag == 0, 1, mag))
+        fails = diff > abs_tol + rel_tol * mag
     r = CrossCheckReport()
     if diff.size:
-        i = int(np.argmax(diff))
-        if diff[i] > 0:
-            r.max_abs, r.worst_value_index = float(diff[i]), i
-            r.worst_voxel, r.worst_substrate = i // substrates, i % substrates
-        r.max_rel = float(rel.max())
-        r.passed = not bool(np.any(diff > abs_tol + rel_tol * mag))
+        # Every comparison with NaN is false in the reference loop: NaN
+        # differences never become the maximum and never fail the check.
+        ok = ~np.isnan(diff)
+        if ok.any():
+            d = np.where(ok, diff, -1.0)
+            i = int(np.argmax(d))
+            if d[i] > 0:
+                r.max_abs, r.worst_value_index = float(d[i]), i
+                r.worst_voxel, r.worst_substrate = i // substrates, i % substrates
+        okr = ~np.isnan(rel)
+        r.max_rel = float(rel[okr].max()) if okr.any() else 0.0
+        r.passed = not bool(np.any(fails))
     return r
 
 

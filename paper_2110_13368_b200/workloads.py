@@ -227,6 +227,22 @@ def c4(steps=20):
     return make("C4: 1024^3 x 4 substrates, 1M cells", 1024, 4, 1000000, steps, immune_fraction=0.1)
 
 
+def c4_sample(w: Workload, planes: int = 64) -> Workload:
+    """A bounded CPU sample of C4 (the reference cannot time 1024^3 x 4 in a
+    few minutes): the central `planes` z-planes of the same grid — 1024-point
+    x and y lines, the same substrates — with C4's cells in those planes.
+    Bounds stay centred, so the planes and cell positions are C4's own."""
+    nx, ny, nz = w.n
+    smp = Workload(name=f"C4 sample: central {planes} of {nz} planes ({nx}x{ny}x{planes} x {w.S}), "
+                        f"C4's cells in them", n=(nx, ny, planes), dx=w.dx, substrates=list(w.substrates),
+                   dt=w.dt, steps=w.steps, seed=w.seed)
+    half = w.dx * planes / 2
+    sel = np.abs(w.agent_pos[:, 2]) < half
+    smp.agent_ids, smp.agent_pos, smp.agent_vol = w.agent_ids[sel], w.agent_pos[sel], w.agent_vol[sel]
+    smp.agent_sec, smp.agent_upt, smp.agent_sat = w.agent_sec[sel], w.agent_upt[sel], w.agent_sat[sel]
+    return smp
+
+
 def c5_replica(r: int, steps=100):
     """One replica of C5 (512 x 64^3 x 2): seeded per-replica D/lambda (+-50%) and layout."""
     w = make(f"C5 replica {r}: 64^3 x 2, 1k cells", 64, 2, 1000, steps, seed=1000 + r)

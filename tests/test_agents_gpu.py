@@ -92,10 +92,16 @@ def test_set_position_by_id_and_errors():
         s.set_agent_position(10 ** 12, p)
     # A position outside the domain: nearest_voxel's domain_error (mesh.cpp:74-76).
     bad = p + np.array([0.0, 0.0, 1.0])
+    before = s.agent_grouping()
     s.set_agent_position(aid, bad)
     with pytest.raises(B.StateError, match=r"outside the simulation domain"):
         s.rebuild_voxel_grouping()
-    assert s.agent_grouping()[0].size == 0
+    # the failed rebuild keeps the previous grouping (the
+    # reference throws before reassigning groups_), and steps still use it.
+    assert all(np.array_equal(a, b) for a, b in zip(s.agent_grouping(), before))
+    s.advance(3, w.dt, with_sources=True)
+    assert bits_equal(s.download_field(), Oracle.run(w, 3))
+    s.upload_field(w.initial_field())
     s.set_agent_position(aid, p)
     s.rebuild_voxel_grouping()
     assert all(np.array_equal(a, b) for a, b in zip(s.agent_grouping(), _oracle_grouping(w)))
@@ -167,3 +173,26 @@ def test_zslab_agents_cross_slabs():
     assert total == w.n_agents  # each agent grouped by exactly one slab
     g.close()
     single.close()
+
+
+def test_sample_agent_densities_reads_each_agents_voxel():
+    """What each agent senses: field.values[agent.voxel * S + s] (agents.hpp:22,
+    mesh.hpp:62-90), in agent-index order, after steps and after a move."""
+    w = W.make("t", (20, 18, 16), 2, 400, 1, seed=4, immune_fraction=0.3)
+    s = make_session(w)
+    rng = np.random.default_rng(2)
+    for _ in range(2):
+        s.advance(5, w.dt)
+        f = s.download_field().reshape(-1, w.S)
+        gv, go, order = _oracle_grouping(w)
+        vox = np.empty(w.n_agents, np.int64)
+        for g in range(gv.size):
+            vox[order[go[g]:go[g + 1]]] = gv[g]
+        got = s.sample_agent_densities()
+        assert bits_equal(got, f[vox])
+        w.agent_pos = _move(rng, w)
+        s.set_agent_positions(w.agent_pos)
+        s.rebuild_voxel_grouping()
+    with pytest.raises(B.StateError):
+        B._check(B.lib().biodiff_sample_agent_densities(s._h, B._dptr(np.zeros(3)), 3))
+    s.close()

@@ -92,3 +92,64 @@ def test_engine_hook_error_stops_the_run_and_resumes():
     ref = make_session(w)
     ref.advance(100, w.dt)
     assert bits_equal(s.download_field(), ref.download_field())
+
+
+@pytest.mark.gpu
+def test_engine_resume_with_snapshots_keeps_the_snapshot_grid():
+    """a run resumed with snapshots on continues the snapshot grid
+    from the clock's position (no negative advance, no repeated snapshot)."""
+    if B.device_count() == 0:
+        pytest.fail("no sm_100 device visible")
+    w = W.make("engine4", (10, 10, 10), 1, 20, 1, seed=3)
+    s = make_session(w)
+    c = SimulationClock(t_max=1.0)
+    snaps, mech = [], []
+
+    def boom(k):
+        mech.append(k.mechanics_steps)
+        if k.mechanics_steps == 4:
+            raise RuntimeError("stop here")
+
+    with pytest.raises(RuntimeError, match="stop here"):
+        run_simulation(s, c, mech_hook=boom, snapshot_interval=0.15,
+                       snapshot_hook=lambda t, f: snaps.append(round(t, 9)))
+    assert (c.diffusion_steps, c.mechanics_steps) == (40, 4) and snaps == [0.15, 0.3]
+    m = run_simulation(s, c, mech_hook=lambda k: mech.append(k.mechanics_steps), snapshot_interval=0.15,
+                       snapshot_hook=lambda t, f: snaps.append(round(t, 9)))
+    # the aborted mechanics hook (step 4) is re-run first, then the grid continues
+    assert mech == [1, 2, 3, 4, 4, 5, 6, 7, 8, 9, 10]
+    assert snaps == [0.15, 0.3, 0.45, 0.6, 0.75, 0.9] and m.snapshots == 4
+    assert (c.diffusion_steps, c.mechanics_steps, c.pending) == (100, 10, 0)
+    ref = make_session(w)
+    ref.advance(100, w.dt)
+    assert bits_equal(s.download_field(), ref.download_field())
+
+
+@pytest.mark.gpu
+def test_engine_aborted_boundary_hooks_are_pending_and_rerun():
+    """a snapshot hook that aborts at a mechanics boundary must not
+    lose that mechanics step (or its cell step) on resume."""
+    if B.device_count() == 0:
+        pytest.fail("no sm_100 device visible")
+    w = W.make("engine5", (10, 10, 10), 1, 0, 1)
+    s = make_session(w)
+    c = SimulationClock(t_max=1.2, dt_cell=0.3)  # per_cell = 3
+    snaps, mech, cell = [], [], []
+    state = {"fail": True}
+
+    def snap(t, f):
+        if round(t, 9) == 0.3 and state["fail"]:
+            state["fail"] = False
+            raise RuntimeError("disk full")
+        snaps.append(round(t, 9))
+
+    hooks = dict(mech_hook=lambda k: mech.append(k.mechanics_steps),
+                 cell_hook=lambda k: cell.append(k.mechanics_steps), snapshot_interval=0.3, snapshot_hook=snap)
+    with pytest.raises(RuntimeError, match="disk full"):
+        run_simulation(s, c, **hooks)
+    assert (c.diffusion_steps, c.mechanics_steps, c.cell_steps) == (30, 3, 1)
+    assert c.pending == 1 | 2 | 4 and mech == [1, 2] and cell == []
+    run_simulation(s, c, **hooks)
+    assert snaps == [0.3, 0.6, 0.9, 1.2]
+    assert mech == list(range(1, 13)) and cell == [3, 6, 9, 12]
+    assert (c.diffusion_steps, c.mechanics_steps, c.cell_steps, c.pending) == (120, 12, 4, 0)

@@ -109,7 +109,12 @@ def test_golden_fixture_advance_graph(name):
     if bool(z["initial_clamp"]) or not bool(z["with_sources"]):
         pytest.skip("advance() runs the plain engine loop")
     s = make_session(w)
+    # prepare_advance instantiates the graphs and runs nothing
+    s.prepare_advance(w.steps, w.dt, with_sources=True)
+    assert bits_equal(s.download_field(), w.initial_field())
+    l0 = s.launch_count()
     s.advance(w.steps, w.dt, with_sources=True)
+    assert s.launch_count() > l0
     got = s.download_field()
     assert bits_equal(got, z["field"]), first_diff(got, z["field"])
     s.close()
@@ -262,6 +267,24 @@ def test_cross_check_semantics():
     rep = s.cross_check(g, 1e-9, 1e-9)
     assert not rep.passed and rep.worst_value_index == 123 and rep.worst_voxel == 61 and rep.worst_substrate == 1
     assert s.cross_check(f, 0.0, 0.0).passed
+    s.close()
+
+
+def test_cross_check_nan_inf_matches_reference_device():
+    """the device cross_check gives the reference's verdict on
+    NaN / Inf entries (comparisons with NaN are false), not a stricter one."""
+    import oracle
+    from tests.test_validation import _nan_inf_cases
+    if not oracle.reference_available():
+        pytest.skip("reference build absent")
+    w = W.make("t", (2, 2, 1), 3, 0, 1)
+    s = make_session(w)
+    for a, b in _nan_inf_cases():
+        s.upload_field(a)
+        for tol in [(1e-9, 1e-9), (0.0, 0.0)]:
+            rep = s.cross_check(b, *tol)
+            ma, mr, wi, ok = oracle.ref_cross_check(a, b, 3, *tol)
+            assert (rep.max_abs, rep.max_rel, rep.worst_value_index, rep.passed) == (ma, mr, wi, ok), (a, b, tol)
     s.close()
 
 

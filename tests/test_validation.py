@@ -54,6 +54,31 @@ def test_cross_check_semantics_host():
     assert V.cross_check(a, a, 3, 0.0, 0.0).passed
 
 
+def _nan_inf_cases():
+    """(a, b) pairs with NaN / Inf entries: ADVICE r01 — the reference's loop
+    compares with NaN as false, so NaN differences neither fail nor count."""
+    base = np.linspace(0.5, 3.0, 12)
+    cases = []
+    for ai, bi in [(np.nan, 1.0), (1.0, np.nan), (np.nan, np.nan), (np.inf, np.inf), (np.inf, 1.0),
+                   (-np.inf, np.inf), (np.inf, np.nan)]:
+        a, b = base.copy(), base.copy()
+        a[4], b[4] = ai, bi
+        cases.append((a, b))
+        a2, b2 = a.copy(), b.copy()
+        b2[9] += 1e-3  # plus one ordinary failing difference
+        cases.append((a2, b2))
+    return cases
+
+
+@needs_ref
+@pytest.mark.parametrize("tol", [(1e-9, 1e-9), (0.0, 0.0), (1e-2, 0.0)])
+def test_cross_check_nan_inf_matches_reference_host(tol):
+    for a, b in _nan_inf_cases():
+        r = V.cross_check(a, b, 3, *tol)
+        ma, mr, wi, ok = oracle.ref_cross_check(a, b, 3, *tol)
+        assert (r.max_abs, r.max_rel, r.worst_value_index, r.passed) == (ma, mr, wi, ok), (a, b)
+
+
 def test_analytic_solution_values():
     assert V.analytic_solution_1d(0.0, 0.0, 1000.0, 2000.0, 1) == 2.0
     assert abs(V.analytic_solution_1d(500.0, 1e6, 1000.0, 2000.0, 4) - 1.0) < 1e-12

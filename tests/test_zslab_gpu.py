@@ -96,3 +96,20 @@ def test_zslab_upload_download_roundtrip_and_split():
     g.upload_field(f)
     assert np.array_equal(g.download_field(), f)
     g.close()
+
+
+def test_zslab_group_advance_checks_like_advance():
+    """the group advance makes advance()'s checks for every slab."""
+    w = W.make("chk", (12, 10, 40), 2, 50, 1, seed=5)
+    g = ZSlabGroup(w, 2)
+    with pytest.raises(B.StateError, match="does not match the solver workspace dt"):
+        B.Session.group_advance(g.sessions, 2, w.dt * 2)
+    with pytest.raises(B.StateError, match="positive"):
+        B.Session.group_advance(g.sessions, 2, 0.0)
+    with pytest.raises(B.StateError, match="non-negative"):
+        B.Session.group_advance(g.sessions, -1, w.dt)
+    g.advance(3)  # still usable after the rejected calls
+    single = make_session(w)
+    single.advance(3, w.dt)
+    assert rel_err(g.download_field(), single.download_field()) <= 1e-13
+    g.close()
