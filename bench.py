@@ -333,7 +333,8 @@ def main():
 
     # Roofline of the dominant kernel (largest share of the timed region).
     peak, peak_src = peaks()
-    sweep_classes = [c for c in ("sweep_xyz", "sweep_xy", "sweep_x", "sweep_y", "sweep_z") if ktimes[c][0]]
+    sweep_classes = [c for c in ("resident", "sweep_xyz", "sweep_xy", "sweep_x", "sweep_y", "sweep_z")
+                     if ktimes[c][0]]
     fused = ktimes["sweep_xy"][0] > 0
     fused3 = ktimes["sweep_xyz"][0] > 0
     # 16 B per value per sweep, 48 B/vsu per step. A fused
@@ -343,7 +344,10 @@ def main():
     dom = max(sweep_classes, key=lambda c: ktimes[c][1])
     n_l, t_l = ktimes[dom]
     avg_ms = t_l / n_l
-    alg_bytes = BYTES_PER_VSU_SWEEP * local_values * SWEEPS_PER_LAUNCH[dom]
+    if dom == "resident":  # one cooperative launch runs every step of the advance() call
+        alg_bytes = BYTES_PER_VSU_STEP * local_values * args.steps
+    else:
+        alg_bytes = BYTES_PER_VSU_SWEEP * local_values * SWEEPS_PER_LAUNCH[dom]
     achieved = alg_bytes / (avg_ms / 1e3) / 1e9
     kernel_total = sum(v[1] for v in ktimes.values())
     step_achieved = bytes_per_vsu_step * vsu_total * args.steps / (ms / 1e3) / 1e9 / world

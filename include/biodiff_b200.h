@@ -222,6 +222,10 @@ int biodiff_fill_field(biodiff_session* session, const double* initial);
 /* Host <-> device copies of the DensityField values (a1 layout). */
 int biodiff_upload_field(biodiff_session* session, const double* values, int64_t count);
 int biodiff_download_field(biodiff_session* session, double* values, int64_t count);
+/* values[offset, offset + count) of the session's device field (the flat
+ * array download_field returns), e.g. to read back a 34 GB field in pieces.
+ * Status 2 when the range leaves the field. */
+int biodiff_download_field_range(biodiff_session* session, int64_t offset, int64_t count, double* values);
 
 /* diffusion_sweep (solver.hpp:51-52, solver.cpp:248-265) along one axis. */
 int biodiff_diffusion_sweep(biodiff_session* session, int32_t axis);

@@ -102,6 +102,7 @@ def ref_lib():
         L.ref_mesh_dims.argtypes = [_vp, _P(ctypes.c_int)]
         L.ref_set_field.argtypes = [_vp, _P(_d), _i64]
         L.ref_get_field.argtypes = [_vp, _P(_d), _i64]
+        L.ref_get_field_range.argtypes = [_vp, _i64, _i64, _P(_d)]
         L.ref_add_dirichlet.argtypes = [_vp, _i64, _P(_i64), _P(_u8), _P(_d)]
         L.ref_dirichlet_size.argtypes = [_vp]
         L.ref_dirichlet_size.restype = _i64
@@ -145,6 +146,21 @@ class RefError(RuntimeError):
 def _rchk(code):
     if code != 0:
         raise RefError(code, ref_lib().ref_last_error().decode())
+
+
+def field_sha256(read_range, count: int, chunk: int = 1 << 25) -> str:
+    """SHA-256 of a float64 field's little-endian bytes, read in pieces:
+    read_range(offset, n, out) fills out[:n] with values[offset, offset+n).
+    Fixes the full-length / full-size parity runs in tests/golden/digests.json
+    without holding two copies of a 34 GB field."""
+    import hashlib
+    h = hashlib.sha256()
+    buf = np.empty(min(chunk, max(count, 1)), np.float64)
+    for off in range(0, count, chunk):
+        n = min(chunk, count - off)
+        read_range(off, n, buf)
+        h.update(buf[:n].astype("<f8", copy=False).tobytes())
+    return h.hexdigest()
 
 
 # --------------------------------------------------------------------------
@@ -303,6 +319,12 @@ class Reference:
         out = np.empty(self.count)
         _rchk(ref_lib().ref_get_field(self.h, _dp(out), out.size))
         return out
+
+    def field_range(self, offset, count, out):
+        _rchk(ref_lib().ref_get_field_range(self.h, int(offset), int(count), _dp(out)))
+
+    def field_digest(self) -> str:
+        return field_sha256(self.field_range, self.count)
 
     def set_field(self, values):
         v = _f(values)

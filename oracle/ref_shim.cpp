@@ -267,6 +267,18 @@ int ref_get_field(void* h, double* v, int64_t count)
     });
 }
 
+// values[offset, offset + count) of the field: lets the tests hash a C4-sized
+// (34 GB) field in pieces instead of holding a second copy of it.
+int ref_get_field_range(void* h, int64_t offset, int64_t count, double* v)
+{
+    return guarded([&] {
+        auto* c = static_cast<RefCtx*>(h);
+        if (offset < 0 || count < 0 || static_cast<std::size_t>(offset + count) > c->env.field.values.size())
+            throw std::invalid_argument("field range out of bounds");
+        std::memcpy(v, c->env.field.values.data() + offset, sizeof(double) * count);
+    });
+}
+
 // DirichletMap::add (mesh.cpp:138-159), one call per entry in caller order.
 int ref_add_dirichlet(void* h, int64_t count, const int64_t* voxel, const uint8_t* mask, const double* values)
 {

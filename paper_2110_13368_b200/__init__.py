@@ -33,7 +33,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", os.environ.get("BIODIFF_LIB", "libbiodiff_b200.so"))
 
 AXIS_X, AXIS_Y, AXIS_Z = 0, 1, 2
-KERNEL_CLASSES = ("sweep_x", "sweep_y", "sweep_z", "dirichlet", "sources", "aux", "sweep_xy", "sweep_xyz")
+KERNEL_CLASSES = ("sweep_x", "sweep_y", "sweep_z", "dirichlet", "sources", "aux", "sweep_xy", "sweep_xyz",
+                  "resident")
 
 
 class BiodiffError(RuntimeError):
@@ -130,6 +131,7 @@ _SIGNATURES = {
     "biodiff_field_all_finite": (ctypes.c_int, [_vp, _P(_i32)]),
     "biodiff_fill_field": (ctypes.c_int, [_vp, _P(_d)]),
     "biodiff_download_field": (ctypes.c_int, [_vp, _P(_d), _i64]),
+    "biodiff_download_field_range": (ctypes.c_int, [_vp, _i64, _i64, _P(_d)]),
     "biodiff_diffusion_sweep": (ctypes.c_int, [_vp, _i32]),
     "biodiff_apply_dirichlet": (ctypes.c_int, [_vp]),
     "biodiff_diffuse_decay_step": (ctypes.c_int, [_vp]),
@@ -561,6 +563,15 @@ class Session:
             out = np.empty(self.value_count, np.float64)
         _check(lib().biodiff_download_field(self._h, _dptr(out), out.size))
         return out
+
+    def download_field_range(self, offset: int, count: int, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """values[offset, offset + count) of the device field (download_field's flat array)."""
+        if out is None:
+            out = np.empty(count, np.float64)
+        if out.dtype != np.float64 or not out.flags.c_contiguous or out.size < count:
+            raise ValueError("out must be a contiguous float64 array of at least `count` values")
+        _check(lib().biodiff_download_field_range(self._h, int(offset), int(count), _dptr(out)))
+        return out[:count]
 
     # -- the hot path ---------------------------------------------------
     def diffusion_sweep(self, axis: int):

@@ -788,6 +788,14 @@ int biodiff_download_field(biodiff_session* session, double* values, int64_t cou
     });
 }
 
+int biodiff_download_field_range(biodiff_session* session, int64_t offset, int64_t count, double* values)
+{
+    return guarded([&] {
+        need(values, "values");
+        dev(session).download_range(values, offset, count);
+    });
+}
+
 int biodiff_diffusion_sweep(biodiff_session* session, int32_t axis)
 {
     return guarded([&] { dev(session).sweep(to_axis(axis)); });

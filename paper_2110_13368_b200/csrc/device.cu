@@ -6,6 +6,7 @@
 #include "ring2.cuh"
 #include "xy2.cuh"
 #include "xyc.cuh"
+#include "resident.cuh"
 
 #include <cuda_runtime.h>
 
@@ -188,6 +189,15 @@ DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int devi
     // launches may be captured into graphs).
     ck(cudaMalloc(&xy_ctr_, sizeof(unsigned) * (1 + static_cast<std::size_t>(mesh.nz) * replicas_)), "cudaMalloc");
     ck(cudaMalloc(&xyc_ctr_, sizeof(unsigned)), "cudaMalloc");
+    {
+        // auto: off when another kernel family is forced for an A/B run
+        const std::string m = env_or("BIODIFF_RESIDENT", "auto");
+        resident_mode_ = m == "auto" ? -1 : std::atoi(m.c_str());
+        for (const char* k : {"BIODIFF_SWEEP_PATH", "BIODIFF_XY_FUSED", "BIODIFF_XYZ_CLUSTER", "BIODIFF_L2_BATCH_MB",
+                              "BIODIFF_RING_SLOTS", "BIODIFF_NO_GRAPH"})
+            if (resident_mode_ == -1 && std::getenv(k) && std::string(std::getenv(k)) != "auto") resident_mode_ = 0;
+    }
+    ck(cudaMalloc(&res_bar_, 2 * sizeof(unsigned)), "cudaMalloc");
 }
 
 DeviceSession::~DeviceSession()
@@ -215,6 +225,7 @@ DeviceSession::~DeviceSession()
     dfree(shell_values_);
     dfree(xy_ctr_);
     dfree(xyc_ctr_);
+    dfree(res_bar_);
     release_agents();
     release_slab();
     for (auto& pe : pending_events_) {
@@ -545,6 +556,16 @@ void DeviceSession::download(double* values, std::int64_t count)
     ck(cudaSetDevice(device_), "cudaSetDevice");
     auto st = static_cast<cudaStream_t>(stream_);
     ck(cudaMemcpyAsync(values, rho_, sizeof(double) * count, cudaMemcpyDeviceToHost, st), "download");
+    ck(cudaStreamSynchronize(st), "sync");
+}
+
+void DeviceSession::download_range(double* values, std::int64_t offset, std::int64_t count)
+{
+    if (offset < 0 || count < 0 || offset + count > value_count())
+        throw std::invalid_argument("field range out of bounds");
+    ck(cudaSetDevice(device_), "cudaSetDevice");
+    auto st = static_cast<cudaStream_t>(stream_);
+    ck(cudaMemcpyAsync(values, rho_ + offset, sizeof(double) * count, cudaMemcpyDeviceToHost, st), "download");
     ck(cudaStreamSynchronize(st), "sync");
 }
 
@@ -1304,6 +1325,92 @@ void DeviceSession::step_body_batches(bool with_sources, double dt, std::int64_t
     rbn_ = 0;
 }
 
+// ---- resident multi-step kernel (resident.cuh) -----------------------------
+
+// Shared memory per warp: one x tile (32/S lines, padded rows) or one y / z
+// tile (32 columns x the line length), whichever is larger.
+int DeviceSession::resident_smem_per_warp() const
+{
+    const int rowlen = mesh_.nx * S_;
+    const int xrow = rowlen + ((S_ - rowlen) % 16 + 16) % 16;
+    long long d = static_cast<long long>(kernels::kLanes / S_) * xrow;
+    if (ws_[1].active) d = std::max<long long>(d, static_cast<long long>(mesh_.ny) * kernels::kLanes);
+    if (ws_[2].active) d = std::max<long long>(d, static_cast<long long>(mesh_.nz) * kernels::kLanes);
+    return static_cast<int>(std::min<long long>(d * 8, 1 << 30));
+}
+
+// Single fields whose lines fit a warp's shared-memory tile (4 warps per CTA)
+// and, by default, whose field fits comfortably in L2 (BIODIFF_RESIDENT_MB,
+// default 32 MB: C1 1 MB, C2 16 MB). BIODIFF_RESIDENT=0 / 1 forces it off /
+// on (where supported).
+bool DeviceSession::resident_path() const
+{
+    if (resident_mode_ == 0 || replicas_ != 1 || slab_ || S_ > kernels::kLanes || !ws_[0].active) return false;
+    if (4 * resident_smem_per_warp() > 227 * 1024) return false;
+    if (resident_mode_ == 1) return true;
+    const double mb = static_cast<double>(value_count()) * 8.0 / 1e6;
+    return mb <= std::atof(env_or("BIODIFF_RESIDENT_MB", "32"));
+}
+
+void DeviceSession::launch_resident(std::int64_t steps, double dt, bool with_sources)
+{
+    auto st = static_cast<cudaStream_t>(stream_);
+    kernels::Resident a{};
+    a.rho = rho_;
+    a.nx = mesh_.nx;
+    a.ny = mesh_.ny;
+    a.nz = mesh_.nz;
+    a.S = S_;
+    for (int ax = 0; ax < 3; ++ax) {
+        const DeviceWorkspace& w = ws_[ax];
+        a.ax[ax] = kernels::ResAxis{w.q, w.dinv, w.cb, w.dconst, w.cconst, w.settle, w.n, w.active ? 1 : 0};
+    }
+    a.last = ws_[2].active ? 2 : ws_[1].active ? 1 : 0;
+    a.clamp = kernels::Clamp{shell_values_, shell_mask_, z0_, nzg_};
+    a.dir_count = dir_res_count_;
+    a.dir_voxel = dir_res_voxel_;
+    a.dir_mask = dir_res_mask_;
+    a.dir_values = dir_res_values_;
+    a.sources = with_sources && n_agents_ > 0 ? 1 : 0;
+    if (a.sources) {
+        ensure_source_factors(dt);
+        a.g_lo = rep_groups_;
+        a.g_hi = rep_groups_ + 1;
+        a.group_voxel = group_voxel_;
+        a.group_offsets = group_offsets_;
+        a.add = agent_add_;
+        a.den = agent_den_;
+    }
+    a.steps = steps;
+    a.bar = res_bar_;
+    const int rowlen = mesh_.nx * S_;
+    a.xrow = rowlen + ((S_ - rowlen) % 16 + 16) % 16;
+    const int per_warp = resident_smem_per_warp();
+    a.warp_doubles = per_warp / 8;
+    constexpr int kWarps = 4;
+    const int block = kWarps * kernels::kLanes;
+    const int smem = kWarps * per_warp;
+    const void* fn = reinterpret_cast<const void*>(kernels::step_resident);
+    ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
+    int per_sm = 0;
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem), "occupancy");
+    if (per_sm < 1) throw state_error("resident kernel does not fit an SM");
+    // Enough warps for the largest phase, at most what is co-resident.
+    const long long L = kernels::kLanes / S_;
+    const long long tpr = (rowlen + kernels::kLanes - 1) / kernels::kLanes;
+    long long tiles = (static_cast<long long>(mesh_.ny) * mesh_.nz + L - 1) / L;
+    if (ws_[1].active) tiles = std::max(tiles, tpr * mesh_.nz);
+    if (ws_[2].active) tiles = std::max(tiles, tpr * mesh_.ny);
+    const long long grid = std::max<long long>(1, std::min<long long>(static_cast<long long>(per_sm) * sm_count_,
+                                                                      (tiles + kWarps - 1) / kWarps));
+    ck(cudaMemsetAsync(res_bar_, 0, 2 * sizeof(unsigned), st), "barrier reset");
+    void* args[] = {&a};
+    begin_kernel(kResident);
+    ck(cudaLaunchCooperativeKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(block), args, smem, st),
+       "resident launch");
+    end_kernel(kResident);
+}
+
 void DeviceSession::sweep(Axis axis)
 {
     ck(cudaSetDevice(device_), "cudaSetDevice");
@@ -1414,7 +1521,7 @@ void DeviceSession::prepare_advance(std::int64_t steps, double dt, bool with_sou
     ck(cudaSetDevice(device_), "cudaSetDevice");
     check_advance(steps, dt);
     if (with_sources) ensure_source_factors(dt);
-    if (!uses_graphs()) return;
+    if (!uses_graphs() || resident_path()) return;
     if (steps / kGraphSteps) graph_for(kGraphSteps, dt, with_sources);
     if (steps % kGraphSteps) graph_for(steps % kGraphSteps, dt, with_sources);
 }
@@ -1427,6 +1534,10 @@ void DeviceSession::advance(std::int64_t steps, double dt, bool with_sources)
     check_advance(steps, dt);
     auto st = static_cast<cudaStream_t>(stream_);
     if (with_sources) ensure_source_factors(dt); // not inside the graph capture
+    if (resident_path()) { // every step in one cooperative launch
+        launch_resident(steps, dt, with_sources);
+        return;
+    }
     if (!uses_graphs()) {
         advance_body(steps, dt, with_sources);
         return;

@@ -29,7 +29,8 @@ enum KernelClass {
     kAux = 5,
     kSweepXY = 6, // fused x+y sweeps through L2 (plane clusters xyc.cuh, or xy2.cuh)
     kSweepXYZ = 7, // ensembles: x, y and z of a replica by one cluster (xyc.cuh)
-    kNumKernelClasses = 8
+    kResident = 8, // L2-resident grids: every step of an advance() in one cooperative launch (resident.cuh)
+    kNumKernelClasses = 9
 };
 
 // Device-side copy of one SolverWorkspace (solver.hpp:24-33).
@@ -109,6 +110,9 @@ public:
     void upload(const double* values, std::int64_t count);
     void fill(const double* initial); // [S] per-substrate initial condition
     void download(double* values, std::int64_t count);
+    void download_range(double* values, std::int64_t offset, std::int64_t count); // values[offset, +count)
+    // advance() runs as one cooperative launch of the resident kernel (L2-resident grids).
+    bool resident_path() const;
 
     void sweep(Axis axis);                 // diffusion_sweep, no clamp
     void apply_dirichlet();                // apply_dirichlet_conditions
@@ -160,6 +164,12 @@ public:
                           std::int64_t vox_hi);
 
 private:
+    // ---- resident multi-step kernel (resident.cuh) -------------------------
+    int resident_mode_ = -1;       // BIODIFF_RESIDENT: 0 off, 1 forced where supported, -1 auto
+    unsigned* res_bar_ = nullptr;  // grid barrier words
+    int resident_smem_per_warp() const;
+    void launch_resident(std::int64_t steps, double dt, bool with_sources);
+
     bool slab_ = false;
     int nzg_ = 0;
     int z0_ = 0;

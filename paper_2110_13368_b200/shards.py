@@ -64,14 +64,9 @@ def shard_session(w, s_range, z_range=None, device: int = 0) -> B.Session:
     z0, z1 = z_range if z_range is not None else (0, w.n[2])
     s = B.Session(mesh, w.S, device, zslab=(z0, z1), shard=tuple(s_range))
     s.set_substrates(w.diffusion, w.decay, w.dt)
-    if (z0, z1) == (0, w.n[2]):
-        if w.boundary_clamp()[0].any() or w.interior_dirichlet is not None:
-            v, m, x = w.dirichlet_entries()
-            s.set_dirichlet(v, m, x)
-    else:
-        v, m, x = slab_dirichlet(w, z0, z1)
-        if v.size:
-            s.set_dirichlet(v, m, x)
+    v, m, x = slab_dirichlet(w, z0, z1)  # the global entries of these planes, built plane by plane
+    if v.size:
+        s.set_dirichlet(v, m, x)
     if w.n_agents:
         s.set_agents(w.agent_ids, w.agent_pos, w.agent_vol, w.agent_sec, w.agent_upt, w.agent_sat)
     s.fill_field(w.initial)

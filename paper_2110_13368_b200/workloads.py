@@ -274,10 +274,18 @@ def session_for(w: Workload, device: int = 0):
     mesh = B.mesh_from_bounds(*w.bounds(), w.dx, w.dx, w.dx)
     s = B.Session(mesh, w.S, device)
     s.set_substrates(w.diffusion, w.decay, w.dt)
+    big = w.voxels * w.S > (1 << 27)  # C4: no whole-grid host arrays (34 GB field, 8 GB index grids)
     if w.boundary_clamp()[0].any() or w.interior_dirichlet is not None:
-        v, m, x = w.dirichlet_entries()
+        if big:
+            from paper_2110_13368_b200.zslab import slab_dirichlet
+            v, m, x = slab_dirichlet(w, 0, w.n[2])  # the same entries, generated plane by plane
+        else:
+            v, m, x = w.dirichlet_entries()
         s.set_dirichlet(v, m, x)
     if w.n_agents:
         s.set_agents(w.agent_ids, w.agent_pos, w.agent_vol, w.agent_sec, w.agent_upt, w.agent_sat)
-    s.upload_field(w.initial_field())
+    if big:
+        s.fill_field(w.initial)  # the uniform initial condition, set on the device
+    else:
+        s.upload_field(w.initial_field())
     return s

@@ -102,9 +102,12 @@ def test_golden_fixture_bitwise(name, path, monkeypatch):
     s.close()
 
 
+@pytest.mark.parametrize("resident", ["0", "1"])
 @pytest.mark.parametrize("name", golden_names())
-def test_golden_fixture_advance_graph(name):
-    """Same runs through advance() (CUDA-graph replay of the SPEC.md:297 loop)."""
+def test_golden_fixture_advance_graph(name, resident, monkeypatch):
+    """Same runs through advance(): CUDA-graph replay of the SPEC.md:297 loop,
+    or the resident multi-step kernel."""
+    monkeypatch.setenv("BIODIFF_RESIDENT", resident)
     w, z = load_golden(name)
     if bool(z["initial_clamp"]) or not bool(z["with_sources"]):
         pytest.skip("advance() runs the plain engine loop")
@@ -204,7 +207,12 @@ def test_no_agents_no_dirichlet_and_empty_inputs():
     s.close()
 
 
-def test_advance_equals_stepwise_and_counts_launches():
+@pytest.mark.parametrize("resident", ["0", "1"])
+def test_advance_equals_stepwise_and_counts_launches(resident, monkeypatch):
+    """advance(57) == 57 x [diffuse_decay_step; cell_sources_sinks_step]: graph
+    replay launches the same kernels; the resident kernel runs all 57 steps
+    in one cooperative launch (plus the once-per-dt source factors)."""
+    monkeypatch.setenv("BIODIFF_RESIDENT", resident)
     w = W.make("t", (32, 24, 20), 2, 300, 1, seed=5)
     a = make_session(w)
     b = make_session(w)
@@ -213,9 +221,46 @@ def test_advance_equals_stepwise_and_counts_launches():
         b.diffuse_decay_step()
         b.cell_sources_sinks_step(w.dt)
     assert bits_equal(a.download_field(), b.download_field())
-    assert a.launch_count() == b.launch_count() > 0
+    if resident == "0":
+        assert a.launch_count() == b.launch_count() > 0
+    else:
+        assert a.launch_count() == 2 and b.launch_count() > 57
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("shape,S", SWEEP_SHAPES)
+def test_resident_kernel_full_steps_bitwise(shape, S, monkeypatch):
+    """The resident multi-step kernel (resident.cuh, one cooperative launch per
+    advance) over every sweep shape: 1-D / 2-D / n=1 axes, odd rows, S up to
+    40 (falls back where a tile does not fit), agents with collisions and
+    interior clamps: bit-identical to the oracle."""
+    monkeypatch.setenv("BIODIFF_RESIDENT", "1")
+    w = W.make("t", shape, S, 120, 7, seed=sum(shape) + S, interior_clamps=3, immune_fraction=0.3)
+    s = make_session(w)
+    s.set_kernel_timing(True)
+    s.advance(7, w.dt)
+    got = s.download_field()
+    t = s.kernel_times()
+    want = Oracle.run(w, 7)
+    assert bits_equal(got, want), first_diff(got, want)
+    if S <= 32:
+        assert t["resident"][0] == 1 and t["sweep_x"][0] == 0
+    s.close()
+
+
+@pytest.mark.parametrize("cfg,steps", [("c1", 2000), ("c2", 300)])
+def test_resident_kernel_configs_bitwise(cfg, steps):
+    """C1 / C2 at full size take the resident kernel by default."""
+    w = W.CONFIGS[cfg](steps)
+    s = make_session(w)
+    s.set_kernel_timing(True)
+    s.advance(steps, w.dt)
+    assert s.kernel_times()["resident"][0] == 1
+    got = s.download_field()
+    want = Oracle.run(w, steps)
+    assert bits_equal(got, want), first_diff(got, want)
+    s.close()
 
 
 @pytest.mark.parametrize("fused", ["1", "0"])
