@@ -198,6 +198,7 @@ void DeviceSession::release_agents()
     n_agents_ = 0;
     groups_ = 0;
     grouped_agents_ = 0;
+    res_grp_valid_ = false;
     id_index_.clear();
     rep_agents_.clear();
 }
@@ -354,6 +355,7 @@ void DeviceSession::rebuild_voxel_grouping()
     ck(cudaMemcpyAsync(counts, agent_counts_, sizeof(counts), cudaMemcpyDeviceToHost, st), "download");
     ck(cudaStreamSynchronize(st), "sync");
     factors_valid_ = false;
+    res_grp_valid_ = false;
     groups_ = counts[0];
     grouped_agents_ = counts[1];
 }

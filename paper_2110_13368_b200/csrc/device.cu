@@ -8,6 +8,7 @@
 #include "xyc.cuh"
 #include "resident.cuh"
 
+#include <cstdio>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -81,6 +82,7 @@ int settle_row(int n, int S, const double* dinv, const double* cb, std::vector<d
 void DeviceSession::build_tensor_maps()
 {
     for (auto& ok : tmap_ok_) ok = false;
+    res_tmap_ok_ = false;
     const long long rowlen = static_cast<long long>(mesh_.nx) * S_;
     if (rowlen % 2 != 0) return; // strides must be multiples of 16 bytes
     void* fn = nullptr;
@@ -110,6 +112,21 @@ void DeviceSession::build_tensor_maps()
                             xb, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         tmap_ok_[0] = (r == CUDA_SUCCESS);
+    }
+    // resident kernel (L2-resident grids): y / z boxes of 32 columns x ceil(n/4) positions
+    res_tmap_ok_ = false;
+    if (replicas_ == 1 && mesh_.ny <= 1024 && mesh_.nz <= 1024) {
+        const cuuint32_t py = static_cast<cuuint32_t>((mesh_.ny + 3) / 4), pz = static_cast<cuuint32_t>((mesh_.nz + 3) / 4);
+        const cuuint32_t by[4] = {static_cast<cuuint32_t>(kernels::kLanes), py, 1, 1};
+        const cuuint32_t bz[4] = {static_cast<cuuint32_t>(kernels::kLanes), 1, pz, 1};
+        res_tmap_ok_ = py <= 256 && pz <= 256 &&
+                       encode(reinterpret_cast<CUtensorMap*>(res_tmap_[0]), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, rho_,
+                              dims, strides, by, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
+                       encode(reinterpret_cast<CUtensorMap*>(res_tmap_[1]), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, rho_,
+                              dims, strides, bz, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
+                       std::getenv("BIODIFF_RES_NO_TMA") == nullptr;
     }
     for (int ax = 1; ax <= 2; ++ax) {
         const cuuint32_t box[4] = {static_cast<cuuint32_t>(kernels::kLanes),
@@ -197,7 +214,15 @@ DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int devi
                               "BIODIFF_RING_SLOTS", "BIODIFF_NO_GRAPH"})
             if (resident_mode_ == -1 && std::getenv(k) && std::string(std::getenv(k)) != "auto") resident_mode_ = 0;
     }
-    ck(cudaMalloc(&res_bar_, 2 * sizeof(unsigned)), "cudaMalloc");
+    {
+        const std::size_t tiles = static_cast<std::size_t>(resident_tpr()) * mesh.ny;
+        ck(cudaMalloc(&res_cnt_, sizeof(unsigned) * kernels::kCntPad *
+                                     (static_cast<std::size_t>(mesh.nz) + resident_tpr() + 2 * mesh.ny)),
+           "cudaMalloc");
+        ck(cudaMalloc(&res_tile_cnt_, sizeof(int) * tiles), "cudaMalloc");
+        ck(cudaMalloc(&res_dir_off_, sizeof(int) * (tiles + 1)), "cudaMalloc");
+        ck(cudaMalloc(&res_grp_off_, sizeof(int) * (tiles + 1)), "cudaMalloc");
+    }
 }
 
 DeviceSession::~DeviceSession()
@@ -225,7 +250,14 @@ DeviceSession::~DeviceSession()
     dfree(shell_values_);
     dfree(xy_ctr_);
     dfree(xyc_ctr_);
-    dfree(res_bar_);
+    dfree(res_cnt_);
+    dfree(res_tile_cnt_);
+    dfree(res_dir_off_);
+    dfree(res_dir_idx_);
+    dfree(res_grp_off_);
+    dfree(res_grp_idx_);
+    dfree(res_grp_tile_);
+    dfree(res_grp_desc_);
     release_agents();
     release_slab();
     for (auto& pe : pending_events_) {
@@ -518,6 +550,7 @@ void DeviceSession::set_dirichlet(const DirichletMap& map)
         dir_res_rep_off_[r] = std::lower_bound(rvox.begin(), rvox.end(), static_cast<std::int64_t>(r) * mesh_.voxel_count()) -
                               rvox.begin();
     shell_mask_ = shell;
+    res_dir_valid_ = false;
     ck(cudaMemcpyAsync(shell_values_, shell_vals.data(), sizeof(double) * S, cudaMemcpyHostToDevice, st), "shell");
     ck(cudaStreamSynchronize(st), "sync");
     invalidate_graphs();
@@ -1327,29 +1360,53 @@ void DeviceSession::step_body_batches(bool with_sources, double dt, std::int64_t
 
 // ---- resident multi-step kernel (resident.cuh) -----------------------------
 
-// Shared memory per warp: one x tile (32/S lines, padded rows) or one y / z
-// tile (32 columns x the line length), whichever is larger.
+// Pivots of the three axes (dinv, cb), kept in shared memory by the kernel.
+int DeviceSession::resident_coef_doubles() const { return 2 * (mesh_.nx + mesh_.ny + mesh_.nz) * S_; }
+
+// Shared memory per warp: one 32-chain column block of the longest axis.
 int DeviceSession::resident_smem_per_warp() const
 {
-    const int rowlen = mesh_.nx * S_;
-    const int xrow = rowlen + ((S_ - rowlen) % 16 + 16) % 16;
-    long long d = static_cast<long long>(kernels::kLanes / S_) * xrow;
-    if (ws_[1].active) d = std::max<long long>(d, static_cast<long long>(mesh_.ny) * kernels::kLanes);
-    if (ws_[2].active) d = std::max<long long>(d, static_cast<long long>(mesh_.nz) * kernels::kLanes);
-    return static_cast<int>(std::min<long long>(d * 8, 1 << 30));
+    const int nmax = std::max(mesh_.nx, std::max(mesh_.ny, mesh_.nz));
+    const long long rows = 4LL * ((nmax + 3) / 4); // TMA boxes of ceil(n/4) rows, zero-filled past n
+    return static_cast<int>(std::min<long long>(rows * kernels::kLanes * 8, 1 << 30));
 }
 
-// Single fields whose lines fit a warp's shared-memory tile (4 warps per CTA)
-// and, by default, whose field fits comfortably in L2 (BIODIFF_RESIDENT_MB,
-// default 32 MB: C1 1 MB, C2 16 MB). BIODIFF_RESIDENT=0 / 1 forces it off /
-// on (where supported).
+// 3-D single fields (every axis active, >= 2 points) whose lines fit a warp's
+// shared-memory column block and, by default, whose field fits comfortably in
+// L2 (BIODIFF_RESIDENT_MB, default 32 MB: C1 1 MB, C2 16 MB).
+// BIODIFF_RESIDENT=0 / 1 forces it off / on (where supported).
 bool DeviceSession::resident_path() const
 {
-    if (resident_mode_ == 0 || replicas_ != 1 || slab_ || S_ > kernels::kLanes || !ws_[0].active) return false;
-    if (4 * resident_smem_per_warp() > 227 * 1024) return false;
+    if (resident_mode_ == 0 || replicas_ != 1 || slab_ || S_ > kernels::kLanes) return false;
+    for (int ax = 0; ax < 3; ++ax)
+        if (!ws_[ax].active || ws_[ax].n < 2) return false;
+    if (resident_smem_per_warp() + 8 * resident_coef_doubles() > 227 * 1024) return false;
     if (resident_mode_ == 1) return true;
     const double mb = static_cast<double>(value_count()) * 8.0 / 1e6;
     return mb <= std::atof(env_or("BIODIFF_RESIDENT_MB", "32"));
+}
+
+// Per-z-tile CSR of items [lo, hi) by voxel: count, scan, fill (item order
+// inside a tile is irrelevant: one item per voxel, distinct voxels commute).
+void DeviceSession::build_resident_list(const std::int64_t* vox, const std::int64_t* lo, const std::int64_t* hi,
+                                        std::int64_t cap, int* off, int* idx, int* tile)
+{
+    auto st = static_cast<cudaStream_t>(stream_);
+    const int tpr = resident_tpr();
+    const int tiles = tpr * mesh_.ny;
+    ck(cudaMemsetAsync(res_tile_cnt_, 0, sizeof(int) * tiles, st), "memset");
+    const int block = 256;
+    const unsigned grid = static_cast<unsigned>(std::max<std::int64_t>(1, (cap + block - 1) / block));
+    begin_kernel(kAux);
+    kernels::res_list_count<<<grid, block, 0, st>>>(vox, lo, hi, cap, mesh_.nx, mesh_.ny, S_, tpr, res_tile_cnt_);
+    end_kernel(kAux);
+    begin_kernel(kAux);
+    kernels::res_list_scan<<<1, 1024, 0, st>>>(res_tile_cnt_, off, tiles);
+    end_kernel(kAux);
+    begin_kernel(kAux);
+    kernels::res_list_fill<<<grid, block, 0, st>>>(vox, lo, hi, cap, mesh_.nx, mesh_.ny, S_, tpr, res_tile_cnt_, idx,
+                                                    tile);
+    end_kernel(kAux);
 }
 
 void DeviceSession::launch_resident(std::int64_t steps, double dt, bool with_sources)
@@ -1361,54 +1418,108 @@ void DeviceSession::launch_resident(std::int64_t steps, double dt, bool with_sou
     a.ny = mesh_.ny;
     a.nz = mesh_.nz;
     a.S = S_;
+    a.tpr = resident_tpr();
     for (int ax = 0; ax < 3; ++ax) {
         const DeviceWorkspace& w = ws_[ax];
-        a.ax[ax] = kernels::ResAxis{w.q, w.dinv, w.cb, w.dconst, w.cconst, w.settle, w.n, w.active ? 1 : 0};
+        a.ax[ax] = kernels::ResAxis{w.q, w.dinv, w.cb, w.dconst, w.cconst, w.settle, w.n};
     }
-    a.last = ws_[2].active ? 2 : ws_[1].active ? 1 : 0;
     a.clamp = kernels::Clamp{shell_values_, shell_mask_, z0_, nzg_};
-    a.dir_count = dir_res_count_;
-    a.dir_voxel = dir_res_voxel_;
-    a.dir_mask = dir_res_mask_;
-    a.dir_values = dir_res_values_;
+    const std::int64_t tiles = static_cast<std::int64_t>(a.tpr) * mesh_.ny;
+    a.dirichlet = dir_res_count_ > 0 ? 1 : 0;
+    if (a.dirichlet) {
+        if (!res_dir_valid_) {
+            dfree(res_dir_idx_);
+            ck(cudaMalloc(&res_dir_idx_, sizeof(int) * 2 * dir_res_count_), "cudaMalloc");
+            build_resident_list(dir_res_voxel_, nullptr, nullptr, dir_res_count_, res_dir_off_, res_dir_idx_, nullptr);
+            res_dir_valid_ = true;
+        }
+        a.zdir_off = res_dir_off_;
+        a.zdir_idx = res_dir_idx_;
+        a.dir_voxel = dir_res_voxel_;
+        a.dir_mask = dir_res_mask_;
+        a.dir_values = dir_res_values_;
+    }
     a.sources = with_sources && n_agents_ > 0 ? 1 : 0;
     if (a.sources) {
         ensure_source_factors(dt);
-        a.g_lo = rep_groups_;
-        a.g_hi = rep_groups_ + 1;
+        if (!res_grp_valid_) {
+            if (res_grp_cap_ < 2 * n_agents_) {
+                dfree(res_grp_idx_);
+                dfree(res_grp_tile_);
+                dfree(res_grp_desc_);
+                res_grp_cap_ = 2 * n_agents_;
+                ck(cudaMalloc(&res_grp_idx_, sizeof(int) * res_grp_cap_), "cudaMalloc");
+                ck(cudaMalloc(&res_grp_tile_, sizeof(int) * res_grp_cap_), "cudaMalloc");
+                ck(cudaMalloc(&res_grp_desc_, sizeof(kernels::ResSrc) * res_grp_cap_), "cudaMalloc");
+            }
+            build_resident_list(group_voxel_, rep_groups_, rep_groups_ + 1, n_agents_, res_grp_off_, res_grp_idx_,
+                                res_grp_tile_);
+            const int tiles_z = a.tpr * mesh_.ny;
+            begin_kernel(kAux);
+            kernels::res_src_desc<<<static_cast<unsigned>((res_grp_cap_ + 255) / 256), 256, 0, st>>>(
+                res_grp_idx_, res_grp_off_ + tiles_z, group_voxel_, group_offsets_, static_cast<kernels::ResSrc*>(res_grp_desc_));
+            end_kernel(kAux);
+            res_grp_valid_ = true;
+        }
+        a.zgrp_off = res_grp_off_;
+        a.zgrp_idx = res_grp_idx_;
+        a.zgrp_tile = res_grp_tile_;
+        a.zsrc = static_cast<const kernels::ResSrc*>(res_grp_desc_);
         a.group_voxel = group_voxel_;
         a.group_offsets = group_offsets_;
         a.add = agent_add_;
         a.den = agent_den_;
     }
     a.steps = steps;
-    a.bar = res_bar_;
-    const int rowlen = mesh_.nx * S_;
-    a.xrow = rowlen + ((S_ - rowlen) % 16 + 16) % 16;
+    a.cnt = res_cnt_;
     const int per_warp = resident_smem_per_warp();
-    a.warp_doubles = per_warp / 8;
-    constexpr int kWarps = 4;
+    a.buf_doubles = per_warp / 8;
+    a.coef_doubles = resident_coef_doubles();
+    a.coef_doubles = (a.coef_doubles + 15) / 16 * 16; // keeps the column blocks 128-byte aligned
+    const int kWarps = std::max(1, std::min(4, (227 * 1024 - 512 - a.coef_doubles * 8) / per_warp));
     const int block = kWarps * kernels::kLanes;
-    const int smem = kWarps * per_warp;
+    const int smem = 128 * kWarps + a.coef_doubles * 8 + kWarps * per_warp;
+    a.tma = res_tmap_ok_ ? 1 : 0;
     const void* fn = reinterpret_cast<const void*>(kernels::step_resident);
     ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
     int per_sm = 0;
     ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem), "occupancy");
     if (per_sm < 1) throw state_error("resident kernel does not fit an SM");
-    // Enough warps for the largest phase, at most what is co-resident.
+    // One warp tile per CTA first (warp rank = warp-in-block * grid + block),
+    // at most what is co-resident.
     const long long L = kernels::kLanes / S_;
-    const long long tpr = (rowlen + kernels::kLanes - 1) / kernels::kLanes;
-    long long tiles = (static_cast<long long>(mesh_.ny) * mesh_.nz + L - 1) / L;
-    if (ws_[1].active) tiles = std::max(tiles, tpr * mesh_.nz);
-    if (ws_[2].active) tiles = std::max(tiles, tpr * mesh_.ny);
-    const long long grid = std::max<long long>(1, std::min<long long>(static_cast<long long>(per_sm) * sm_count_,
-                                                                      (tiles + kWarps - 1) / kWarps));
-    ck(cudaMemsetAsync(res_bar_, 0, 2 * sizeof(unsigned), st), "barrier reset");
-    void* args[] = {&a};
+    long long max_tiles = (static_cast<long long>(mesh_.ny) * mesh_.nz + L - 1) / L;
+    max_tiles = std::max(max_tiles, static_cast<long long>(a.tpr) * std::max(mesh_.ny, mesh_.nz));
+    const long long grid = std::max<long long>(1, std::min<long long>(static_cast<long long>(per_sm) * sm_count_, max_tiles));
+    (void)tiles;
+    ck(cudaMemsetAsync(res_cnt_, 0,
+                       sizeof(unsigned) * kernels::kCntPad * (static_cast<std::size_t>(mesh_.nz) + a.tpr + 2 * mesh_.ny), st),
+       "counter reset");
+    const char* trace_path = std::getenv("BIODIFF_RES_TRACE"); // design probe: per-tile phase stamps
+    std::size_t trace_n = 0;
+    if (trace_path) {
+        a.trace_tiles = std::max<long long>(max_tiles, (n_agents_ * 2 + 31) / 32);
+        trace_n = static_cast<std::size_t>(8 * 4 * a.trace_tiles * 6);
+        ck(cudaMalloc(&a.trace, trace_n * 8), "cudaMalloc");
+        ck(cudaMemsetAsync(a.trace, 0, trace_n * 8, st), "memset");
+    }
+    void* args[] = {res_tmap_[0], res_tmap_[1], &a};
     begin_kernel(kResident);
     ck(cudaLaunchCooperativeKernel(fn, dim3(static_cast<unsigned>(grid)), dim3(block), args, smem, st),
        "resident launch");
     end_kernel(kResident);
+    if (trace_path) {
+        std::vector<unsigned long long> h(trace_n);
+        ck(cudaMemcpyAsync(h.data(), a.trace, trace_n * 8, cudaMemcpyDeviceToHost, st), "download");
+        ck(cudaStreamSynchronize(st), "sync");
+        cudaFree(a.trace);
+        if (FILE* f = std::fopen(trace_path, "wb")) {
+            const long long hdr[4] = {a.trace_tiles, grid, block, smem};
+            std::fwrite(hdr, sizeof(hdr), 1, f);
+            std::fwrite(h.data(), 8, trace_n, f);
+            std::fclose(f);
+        }
+    }
 }
 
 void DeviceSession::sweep(Axis axis)

@@ -166,8 +166,22 @@ public:
 private:
     // ---- resident multi-step kernel (resident.cuh) -------------------------
     int resident_mode_ = -1;       // BIODIFF_RESIDENT: 0 off, 1 forced where supported, -1 auto
-    unsigned* res_bar_ = nullptr;  // grid barrier words
+    unsigned* res_cnt_ = nullptr;  // dataflow counters: [nz] planes | [tpr] ranges | [ny] rows
+    int* res_tile_cnt_ = nullptr;  // per-z-tile list scratch (counts / fill cursor)
+    int* res_dir_off_ = nullptr;   // [tiles+1] residual Dirichlet entries per z tile
+    int* res_dir_idx_ = nullptr;
+    int* res_grp_off_ = nullptr;   // [tiles+1] agent groups per z tile
+    int* res_grp_idx_ = nullptr;
+    int* res_grp_tile_ = nullptr;  // z tile of each group entry (the sources phase's row waits)
+    void* res_grp_desc_ = nullptr; // kernels::ResSrc per group entry (voxel, agent range)
+    std::int64_t res_grp_cap_ = 0; // capacity of res_grp_idx_ (items)
+    bool res_dir_valid_ = false;   // lists match the current Dirichlet split / grouping
+    bool res_grp_valid_ = false;
+    int resident_tpr() const { return (mesh_.nx * S_ + 31) / 32; }
     int resident_smem_per_warp() const;
+    int resident_coef_doubles() const;
+    void build_resident_list(const std::int64_t* vox, const std::int64_t* lo, const std::int64_t* hi,
+                             std::int64_t cap, int* off, int* idx, int* tile);
     void launch_resident(std::int64_t steps, double dt, bool with_sources);
 
     bool slab_ = false;
@@ -347,6 +361,8 @@ private:
     };
     std::map<GraphKey, std::pair<void*, int>> graphs_; // cudaGraphExec_t, kernels per replay
     void* slots_[16] = {};                              // cudaEvent_t for event_record()
+    alignas(64) unsigned char res_tmap_[2][128] = {}; // resident kernel's y / z tensor maps
+    bool res_tmap_ok_ = false;
     alignas(64) unsigned char tmap_[3][128] = {};       // CUtensorMap per axis (x: swizzled 4-D view for ring2)
     bool tmap_ok_[3] = {false, false, false};
     void build_tensor_maps();

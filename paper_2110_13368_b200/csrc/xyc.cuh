@@ -340,6 +340,9 @@ __device__ __forceinline__ void xyc_body(const CUtensorMap* tmap_x, const CUtens
         P = Pn;
     }
     if (lane == 0) ptx::bulk_wait_all();
+    // No CTA may exit while another CTA of its cluster can still read its
+    // s_next through DSMEM (compute-sanitizer racecheck, r02).
+    cluster_sync();
 }
 
 template <int NS, int S>

@@ -210,13 +210,16 @@ def test_no_agents_no_dirichlet_and_empty_inputs():
 @pytest.mark.parametrize("resident", ["0", "1"])
 def test_advance_equals_stepwise_and_counts_launches(resident, monkeypatch):
     """advance(57) == 57 x [diffuse_decay_step; cell_sources_sinks_step]: graph
-    replay launches the same kernels; the resident kernel runs all 57 steps
-    in one cooperative launch (plus the once-per-dt source factors)."""
+    replay launches the same kernels; the resident kernel runs the steps of an
+    advance in one cooperative launch (the source factors and per-tile lists
+    are built once, by the first advance)."""
     monkeypatch.setenv("BIODIFF_RESIDENT", resident)
     w = W.make("t", (32, 24, 20), 2, 300, 1, seed=5)
     a = make_session(w)
     b = make_session(w)
-    a.advance(57, w.dt)
+    a.advance(50, w.dt)
+    a0 = a.launch_count()  # grouping, source factors, per-tile lists: once
+    a.advance(7, w.dt)
     for _ in range(57):
         b.diffuse_decay_step()
         b.cell_sources_sinks_step(w.dt)
@@ -224,7 +227,7 @@ def test_advance_equals_stepwise_and_counts_launches(resident, monkeypatch):
     if resident == "0":
         assert a.launch_count() == b.launch_count() > 0
     else:
-        assert a.launch_count() == 2 and b.launch_count() > 57
+        assert a.launch_count() - a0 == 1 and b.launch_count() > 57
     a.close()
     b.close()
 
@@ -244,7 +247,7 @@ def test_resident_kernel_full_steps_bitwise(shape, S, monkeypatch):
     t = s.kernel_times()
     want = Oracle.run(w, 7)
     assert bits_equal(got, want), first_diff(got, want)
-    if S <= 32:
+    if S <= 32 and min(shape) >= 2:  # 3-D fields only (resident_path)
         assert t["resident"][0] == 1 and t["sweep_x"][0] == 0
     s.close()
 
