@@ -57,6 +57,10 @@ const char* biodiff_last_error(void);
 /* ABI version: major*10000 + minor*100 + patch. */
 int32_t biodiff_version(void);
 
+/* Build flags: bit 0 = EXPERIMENTAL=1 build (measured-and-rejected kernel
+   variants compiled in for A/B runs). */
+int32_t biodiff_build_flags(void);
+
 /* CartesianMesh::from_bounds (mesh.hpp:28-31, mesh.cpp:12-44). */
 int biodiff_mesh_from_bounds(double x_min, double x_max, double y_min, double y_max, double z_min, double z_max,
                              double dx, double dy, double dz, biodiff_mesh* out);

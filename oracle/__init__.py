@@ -35,7 +35,7 @@ _vp = ctypes.c_void_p
 
 def build(quiet: bool = True):
     """Builds liboracle.so always, and the reference .so when its sources exist."""
-    targets = ["oracle"] + (["ref"] if os.path.isdir(REF_SOURCES) else [])
+    targets = ["oracle"] + (["ref", "binding"] if os.path.isdir(REF_SOURCES) else [])
     subprocess.run(["make", "-C", HERE, "-j8"] + targets, check=True,
                    stdout=subprocess.DEVNULL if quiet else None)
 

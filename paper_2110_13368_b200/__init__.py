@@ -97,6 +97,7 @@ PLANE_EXCHANGE = ctypes.CFUNCTYPE(ctypes.c_int, _vp, _P(_d), _i32, _P(_d), _i32,
 _SIGNATURES = {
     "biodiff_last_error": (ctypes.c_char_p, []),
     "biodiff_version": (_i32, []),
+    "biodiff_build_flags": (_i32, []),
     "biodiff_mesh_from_bounds": (ctypes.c_int, [_d] * 9 + [_P(Mesh)]),
     "biodiff_nearest_voxel": (ctypes.c_int, [_P(Mesh), _P(_d), _P(_i64)]),
     "biodiff_precompute_thomas": (ctypes.c_int, [_P(Mesh), _i32, _P(_d), _P(_d), _d, _i32, _i32, _P(_d), _P(_d), _P(_d)]),
@@ -275,6 +276,12 @@ def precompute_thomas_coefficients(mesh: Mesh, diffusion, decay, dt: float, axis
     _check(lib().biodiff_precompute_thomas(ctypes.byref(mesh), S, _dptr(D), _dptr(L), dt, axis, dims,
                                            _dptr(q), _dptr(dinv), _dptr(cb)))
     return q, dinv.reshape(n, S), cb.reshape(n, S)
+
+
+def experimental_build() -> bool:
+    """True when the library was built with EXPERIMENTAL=1 (the measured-and-
+    rejected kernel variants compiled in for A/B runs)."""
+    return bool(lib().biodiff_build_flags() & 1)
 
 
 def device_count() -> int:

@@ -199,6 +199,15 @@ const char* biodiff_last_error(void) { return g_last_error.c_str(); }
 
 int32_t biodiff_version(void) { return 10000; }
 
+int32_t biodiff_build_flags(void)
+{
+#ifdef BIODIFF_EXPERIMENTAL
+    return 1;
+#else
+    return 0;
+#endif
+}
+
 int biodiff_mesh_from_bounds(double x_min, double x_max, double y_min, double y_max, double z_min, double z_max,
                              double dx, double dy, double dz, biodiff_mesh* out)
 {

@@ -4,7 +4,9 @@
 #include "kernels.cuh"
 #include "ring.cuh"
 #include "ring2.cuh"
-#include "xy2.cuh"
+#ifdef BIODIFF_EXPERIMENTAL
+#include "xy2.cuh" // lagged-ticket x+y (measured slower; EXPERIMENTAL=1 builds only)
+#endif
 #include "xyc.cuh"
 #include "resident.cuh"
 
@@ -168,6 +170,10 @@ DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int devi
         const std::string m = env_or("BIODIFF_XY_FUSED", "auto");
         xy_mode_ = m == "auto" ? -1 : std::atoi(m.c_str());
         xy_fused_ = xy_mode_ != 0;
+#ifndef BIODIFF_EXPERIMENTAL
+        if (xy_mode_ == 1)
+            throw config_error("BIODIFF_XY_FUSED=1 (lagged-ticket x+y, xy2.cuh) needs a build with EXPERIMENTAL=1");
+#endif
     }
     l2_hints_ = std::atoi(env_or("BIODIFF_L2_HINTS", "2")); // stores evict_first: C3 0.635 -> 0.629 ms; load hints slower
     l2_keep_from8_ = std::atoi(env_or("BIODIFF_L2_KEEP_FROM8", "4"));
@@ -318,7 +324,11 @@ int DeviceSession::ring_slots(int axis) const
     // solve_short2) so the next tile loads while this one computes (C5
     // 64-point lines: y 1253 -> 1197 us, z 1294 -> 1246; x measured slower).
     if (!e && axis != 0 && nch <= 2 && std::getenv("BIODIFF_NO_SHORT") == nullptr) return 2 * nch;
+#ifdef BIODIFF_EXPERIMENTAL
     return std::min(nch, want);
+#else
+    return std::min(nch, std::min(want, 3)); // 4 slots: EXPERIMENTAL=1 builds (measured slower)
+#endif
 }
 
 int DeviceSession::ring_smem_bytes(int axis) const
@@ -996,6 +1006,7 @@ bool DeviceSession::xyz_cluster_pays() const
 
 namespace {
 
+#ifdef BIODIFF_EXPERIMENTAL
 template <int NS>
 const void* xy2_pick_s(int S)
 {
@@ -1013,6 +1024,7 @@ const void* xy2_pick(int ns, int S)
     default: return xy2_pick_s<4>(S);
     }
 }
+#endif
 
 } // namespace
 
@@ -1067,10 +1079,12 @@ const void* yz_ring2_pick(int ns, bool short_lines)
         return ns == 2 ? reinterpret_cast<const void*>(kernels::sweep_yz_ring2<2, CLAMP, true>)
                        : reinterpret_cast<const void*>(kernels::sweep_yz_ring2<4, CLAMP, true>);
     switch (ns) {
-    case 1: return yz_ring2_fn<1, CLAMP>();
+    case 1: return yz_ring2_fn<1, CLAMP>(); // one-chunk lines
+#ifdef BIODIFF_EXPERIMENTAL
+    case 4: return yz_ring2_fn<4, CLAMP>();
+#endif
     case 2: return yz_ring2_fn<2, CLAMP>();
-    case 3: return yz_ring2_fn<3, CLAMP>();
-    default: return yz_ring2_fn<4, CLAMP>();
+    default: return yz_ring2_fn<3, CLAMP>();
     }
 }
 
@@ -1081,10 +1095,12 @@ const void* x_ring2_pick_ns(int ns, bool short_lines)
         return ns == 2 ? reinterpret_cast<const void*>(kernels::sweep_x_ring2<2, S, CLAMP, true>)
                        : reinterpret_cast<const void*>(kernels::sweep_x_ring2<4, S, CLAMP, true>);
     switch (ns) {
-    case 1: return x_ring2_fn<1, S, CLAMP>();
+    case 1: return x_ring2_fn<1, S, CLAMP>(); // one-chunk lines
+#ifdef BIODIFF_EXPERIMENTAL
+    case 4: return x_ring2_fn<4, S, CLAMP>();
+#endif
     case 2: return x_ring2_fn<2, S, CLAMP>();
-    case 3: return x_ring2_fn<3, S, CLAMP>();
-    default: return x_ring2_fn<4, S, CLAMP>();
+    default: return x_ring2_fn<3, S, CLAMP>();
     }
 }
 
@@ -1206,6 +1222,7 @@ void DeviceSession::launch_ring2(int ax, bool do_clamp, const kernels::Clamp& cl
     launch_k(fn, grid, kernels::kLanes, args, smem, "launch yz ring2");
 }
 
+#ifdef BIODIFF_EXPERIMENTAL
 // Fused x+y on ring2 (xy2.cuh).
 void DeviceSession::launch_xy2()
 {
@@ -1258,6 +1275,9 @@ void DeviceSession::launch_xy2()
     ck(cudaLaunchKernel(fn, dim3(grid), dim3(kernels::kLanes), args, smem, st), "launch xy2");
     end_kernel(kSweepXY);
 }
+#else
+void DeviceSession::launch_xy2() { throw state_error("built without EXPERIMENTAL=1"); }
+#endif
 
 void DeviceSession::launch_residual_dirichlet(bool all_entries)
 {

@@ -24,6 +24,15 @@ def _need_gpu():
         pytest.fail("no sm_100 device visible: GPU tests must run on a B200 (no CPU fallback)")
 
 
+def _skip_experimental(path=None, env=None):
+    """Variants measured slower and compiled only by EXPERIMENTAL=1 builds:
+    ring2 with 4 slots, the lagged-ticket x+y kernel (BIODIFF_XY_FUSED=1)."""
+    if B.experimental_build():
+        return
+    if path == "r2s4" or (env or {}).get("BIODIFF_XY_FUSED") == "1":
+        pytest.skip("variant built only with EXPERIMENTAL=1")
+
+
 def _paths(monkeypatch, path):
     """Selects a sweep kernel family (read at session creation): auto = ring2
     (register-chunk ring, x 4 slots, y/z 3), r2sN = ring2 with N slots,
@@ -58,6 +67,7 @@ SWEEP_SHAPES = [
 @pytest.mark.parametrize("shape,S", SWEEP_SHAPES)
 def test_single_sweep_bitwise(shape, S, path, monkeypatch):
     """diffusion_sweep (solver.cpp:248-265) along every active axis, every kernel path."""
+    _skip_experimental(path=path)
     _paths(monkeypatch, path)
     w = W.make("t", shape, S, 0, 1, seed=2)
     rng = np.random.default_rng(hash((shape, S)) & 0xffff)
@@ -268,6 +278,7 @@ def test_resident_kernel_configs_bitwise(cfg, steps):
 
 @pytest.mark.parametrize("fused", ["1", "0"])
 def test_kernel_timing_reports_every_class(fused, monkeypatch):
+    _skip_experimental(env={"BIODIFF_XY_FUSED": fused})
     monkeypatch.setenv("BIODIFF_XY_FUSED", fused)
     w = W.make("t", (64, 64, 64), 2, 1000, 1, seed=6, interior_clamps=10)
     s = make_session(w)
@@ -374,6 +385,7 @@ FUSED_ENVS = [
 def test_fused_xy_step_bitwise(shape, S, env, monkeypatch):
     """The fused x+y kernel (ticketed items, per-plane release/acquire
     counters) gives the oracle's bits for full steps at every lag setting."""
+    _skip_experimental(env=env)
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     w = W.make("t", shape, S, 150, 1, seed=9, interior_clamps=4)
