@@ -9,6 +9,7 @@ import io
 import subprocess
 import sys
 
+# (metric, label, scale applied to the value in base units (ns / bytes), unit)
 KEYS = [
     ("gpu__time_duration.sum", "duration", 1e-3, "us"),
     ("dram__bytes_read.sum", "dram read", 1e-6, "MB"),
@@ -30,16 +31,21 @@ def main(path):
     if len(rows) < 3:
         print("no rows")
         return
-    h = rows[0]
+    h, units = rows[0], rows[1]
     ix = {k: i for i, k in enumerate(h)}
+    base = {"nsecond": 1.0, "usecond": 1e3, "msecond": 1e6, "second": 1e9, "ns": 1.0, "us": 1e3, "ms": 1e6,
+            "s": 1e9, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "B": 1.0, "KB": 1e3,
+            "MB": 1e6, "GB": 1e9}
     name_i = ix.get("Kernel Name")
     print(f"ncu report: {path}")
     for r in rows[2:]:
         print(f"\n== {r[name_i][:140]}")
+        if "gpu__time_duration.sum" in ix:
+            print(f"  (duration unit in report: {units[ix['gpu__time_duration.sum']]})")
         for k, label, scale, unit in KEYS:
             if k in ix and r[ix[k]] not in ("", "n/a"):
                 try:
-                    v = float(r[ix[k]].replace(",", "")) * scale
+                    v = float(r[ix[k]].replace(",", "")) * base.get(units[ix[k]], 1.0) * scale
                     print(f"  {label:22s} {v:12.2f} {unit}")
                 except ValueError:
                     pass
