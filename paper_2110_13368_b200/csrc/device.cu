@@ -9,6 +9,7 @@
 #endif
 #include "xyc.cuh"
 #include "resident.cuh"
+#include "small.cuh"
 
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -212,6 +213,7 @@ DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int devi
     // launches may be captured into graphs).
     ck(cudaMalloc(&xy_ctr_, sizeof(unsigned) * (1 + static_cast<std::size_t>(mesh.nz) * replicas_)), "cudaMalloc");
     ck(cudaMalloc(&xyc_ctr_, sizeof(unsigned)), "cudaMalloc");
+    small_mode_ = std::atoi(env_or("BIODIFF_SMALL", "-1")); // -1 auto, 0 off, 1 forced where it fits
     {
         // auto: off when another kernel family is forced for an A/B run
         const std::string m = env_or("BIODIFF_RESIDENT", "auto");
@@ -1542,6 +1544,143 @@ void DeviceSession::launch_resident(std::int64_t steps, double dt, bool with_sou
     }
 }
 
+// ---- one-cluster kernel for fields that fit a cluster's shared memory (small.cuh)
+
+// Cluster size, planes per CTA, row pitch and dynamic smem of the one-cluster
+// kernel, or false when the field does not fit (or the mode is off).
+bool DeviceSession::small_config(int& cl, int& planes, int& pitch, int& smem_bytes) const
+{
+    if (small_mode_ == 0 || resident_mode_ == 0 || replicas_ != 1 || slab_ || S_ > kernels::kLanes) return false;
+    for (int ax = 0; ax < 3; ++ax)
+        if (!ws_[ax].active || ws_[ax].n < 2) return false;
+    constexpr int kThreads = 256;
+    const int rowlen = mesh_.nx * S_;
+    const int coef = (resident_coef_doubles() + 15) / 16 * 16;
+    for (int c : {16, 8}) {
+        planes = (mesh_.nz + c - 1) / c;
+        // TMA slab moves need 16-byte rows and a box of <= 256 x 256; the
+        // rows are then dense (pitch = rowlen), else padded to S mod 16.
+        const bool tma = rowlen % 2 == 0 && rowlen <= 256 && planes * mesh_.ny <= 256;
+        if (!tma) continue; // slab moves by TMA only (the one-cluster kernel's supported shapes)
+        pitch = rowlen;
+        const long long slab = std::max<long long>(static_cast<long long>(planes) * mesh_.ny * pitch,
+                                                   static_cast<long long>(mesh_.nz) * kThreads);
+        const long long bytes = (16 + coef + slab) * 8;
+        if (bytes <= 227 * 1024) {
+            cl = c;
+            smem_bytes = static_cast<int>(bytes);
+            return true;
+        }
+    }
+    return false;
+}
+
+bool DeviceSession::small_path() const
+{
+    int cl, planes, pitch, smem;
+    if (!small_config(cl, planes, pitch, smem)) return false;
+    if (small_mode_ == 1) return true;
+    // auto: where the one-cluster kernel measured faster than the L2 dataflow
+    // kernel (BIODIFF_SMALL_MB, default 2 MB: C1's 1 MB field).
+    return static_cast<double>(value_count()) * 8.0 / 1e6 <= std::atof(env_or("BIODIFF_SMALL_MB", "2"));
+}
+
+void DeviceSession::launch_small(std::int64_t steps, double dt, bool with_sources)
+{
+    auto st = static_cast<cudaStream_t>(stream_);
+    int cl = 0, planes = 0, pitch = 0, smem = 0;
+    if (!small_config(cl, planes, pitch, smem)) throw state_error("field does not fit the one-cluster kernel");
+    kernels::Small a{};
+    a.rho = rho_;
+    a.nx = mesh_.nx;
+    a.ny = mesh_.ny;
+    a.nz = mesh_.nz;
+    a.S = S_;
+    a.pitch = pitch;
+    a.planes = planes;
+    for (int ax = 0; ax < 3; ++ax) {
+        const DeviceWorkspace& w = ws_[ax];
+        a.ax[ax] = kernels::ResAxis{w.q, w.dinv, w.cb, w.dconst, w.cconst, w.settle, w.n};
+    }
+    a.clamp = kernels::Clamp{shell_values_, shell_mask_, z0_, nzg_};
+    a.dir_count = dir_res_count_;
+    a.dir_voxel = dir_res_voxel_;
+    a.dir_mask = dir_res_mask_;
+    a.dir_values = dir_res_values_;
+    a.sources = with_sources && n_agents_ > 0 ? 1 : 0;
+    if (a.sources) {
+        ensure_source_factors(dt);
+        a.g_lo = rep_groups_;
+        a.g_hi = rep_groups_ + 1;
+        a.group_voxel = group_voxel_;
+        a.group_offsets = group_offsets_;
+        a.add = agent_add_;
+        a.den = agent_den_;
+    }
+    a.steps = steps;
+    a.coef_doubles = (resident_coef_doubles() + 15) / 16 * 16;
+    a.slab_doubles = smem / 8 - 16 - a.coef_doubles;
+    const long long rowlen = static_cast<long long>(mesh_.nx) * S_;
+    a.tma = pitch == rowlen && rowlen % 2 == 0 ? std::atoi(env_or("BIODIFF_SMALL_TMA_MASK", "3")) : 0;
+    alignas(64) unsigned char tmap[128] = {};
+    if (a.tma) { // 4-D view (row, (plane, j) row index, 1, 1), box (rowlen, planes * ny)
+        void* efn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        ck(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &efn, cudaEnableDefault, &q), "driver entry point");
+        using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+        const cuuint64_t dims[4] = {static_cast<cuuint64_t>(rowlen),
+                                    static_cast<cuuint64_t>(mesh_.ny) * static_cast<cuuint64_t>(mesh_.nz), 1, 1};
+        const cuuint64_t total = static_cast<cuuint64_t>(rowlen) * mesh_.ny * mesh_.nz * 8;
+        const cuuint64_t strides[3] = {static_cast<cuuint64_t>(rowlen) * 8, total, total};
+        const cuuint32_t box[4] = {static_cast<cuuint32_t>(rowlen), static_cast<cuuint32_t>(planes * mesh_.ny), 1, 1};
+        const cuuint32_t estr[4] = {1, 1, 1, 1};
+        if (reinterpret_cast<Encode>(efn)(reinterpret_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
+                                          rho_, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            throw state_error("slab tensor map");
+    }
+    const void* fn = reinterpret_cast<const void*>(kernels::step_small);
+    ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
+    if (cl > 8) ck(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1), "cluster 16");
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(cl);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = static_cast<std::size_t>(smem);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const char* trace_path = std::getenv("BIODIFF_RES_TRACE"); // design probe: per-CTA phase stamps
+    const std::size_t trace_n = static_cast<std::size_t>(8) * cl * 12;
+    if (trace_path) {
+        ck(cudaMalloc(&a.trace, trace_n * 8), "cudaMalloc");
+        ck(cudaMemsetAsync(a.trace, 0, trace_n * 8, st), "memset");
+    }
+    void* args[] = {tmap, &a};
+    begin_kernel(kResident);
+    ck(cudaLaunchKernelExC(&cfg, fn, args), "launch one-cluster kernel");
+    end_kernel(kResident);
+    if (trace_path) {
+        std::vector<unsigned long long> h(trace_n);
+        ck(cudaMemcpyAsync(h.data(), a.trace, trace_n * 8, cudaMemcpyDeviceToHost, st), "download");
+        ck(cudaStreamSynchronize(st), "sync");
+        cudaFree(a.trace);
+        if (FILE* f = std::fopen(trace_path, "wb")) {
+            const long long hdr[4] = {-1, cl, 256, smem}; // -1: one-cluster trace layout
+            std::fwrite(hdr, sizeof(hdr), 1, f);
+            std::fwrite(h.data(), 8, trace_n, f);
+            std::fclose(f);
+        }
+    }
+}
+
 void DeviceSession::sweep(Axis axis)
 {
     ck(cudaSetDevice(device_), "cudaSetDevice");
@@ -1652,7 +1791,7 @@ void DeviceSession::prepare_advance(std::int64_t steps, double dt, bool with_sou
     ck(cudaSetDevice(device_), "cudaSetDevice");
     check_advance(steps, dt);
     if (with_sources) ensure_source_factors(dt);
-    if (!uses_graphs() || resident_path()) return;
+    if (!uses_graphs() || resident_path() || small_path()) return;
     if (steps / kGraphSteps) graph_for(kGraphSteps, dt, with_sources);
     if (steps % kGraphSteps) graph_for(steps % kGraphSteps, dt, with_sources);
 }
@@ -1665,6 +1804,10 @@ void DeviceSession::advance(std::int64_t steps, double dt, bool with_sources)
     check_advance(steps, dt);
     auto st = static_cast<cudaStream_t>(stream_);
     if (with_sources) ensure_source_factors(dt); // not inside the graph capture
+    if (small_path()) { // every step in one launch of one cluster (field in shared memory)
+        launch_small(steps, dt, with_sources);
+        return;
+    }
     if (resident_path()) { // every step in one cooperative launch
         launch_resident(steps, dt, with_sources);
         return;

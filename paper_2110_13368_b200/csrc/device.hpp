@@ -113,6 +113,7 @@ public:
     void download_range(double* values, std::int64_t offset, std::int64_t count); // values[offset, +count)
     // advance() runs as one cooperative launch of the resident kernel (L2-resident grids).
     bool resident_path() const;
+    bool small_path() const; // advance() runs as one launch of one thread-block cluster (field in its smem)
 
     void sweep(Axis axis);                 // diffusion_sweep, no clamp
     void apply_dirichlet();                // apply_dirichlet_conditions
@@ -183,6 +184,10 @@ private:
     void build_resident_list(const std::int64_t* vox, const std::int64_t* lo, const std::int64_t* hi,
                              std::int64_t cap, int* off, int* idx, int* tile);
     void launch_resident(std::int64_t steps, double dt, bool with_sources);
+    // ---- one-cluster kernel (small.cuh): fields that fit a cluster's smem
+    int small_mode_ = -1; // BIODIFF_SMALL: 0 off, 1 forced where it fits, -1 auto
+    bool small_config(int& cl, int& planes, int& pitch, int& smem_bytes) const;
+    void launch_small(std::int64_t steps, double dt, bool with_sources);
 
     bool slab_ = false;
     int nzg_ = 0;

@@ -155,13 +155,14 @@ __device__ __forceinline__ uint32_t res_issue_tma(double* buf, const void* tmap,
     return wait;
 }
 
-__device__ __forceinline__ void res_issue(double* c, const double* g, long long gst, int n, int P, bool active)
+__device__ __forceinline__ void res_issue(double* c, const double* g, long long gst, int n, int P, bool active,
+                                          int W = kLanes)
 {
 #pragma unroll
     for (int G = 0; G < 4; ++G) {
         if (active) {
             const int m1 = min(n, (G + 1) * P);
-            for (int m = G * P; m < m1; ++m) ptx::cp_async8(c + m * kLanes, g + m * gst);
+            for (int m = G * P; m < m1; ++m) ptx::cp_async8(c + m * W, g + m * gst);
         }
         ptx::cp_async_commit();
     }

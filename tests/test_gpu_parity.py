@@ -242,13 +242,16 @@ def test_advance_equals_stepwise_and_counts_launches(resident, monkeypatch):
     b.close()
 
 
+@pytest.mark.parametrize("kernel", ["dataflow", "cluster"])
 @pytest.mark.parametrize("shape,S", SWEEP_SHAPES)
-def test_resident_kernel_full_steps_bitwise(shape, S, monkeypatch):
-    """The resident multi-step kernel (resident.cuh, one cooperative launch per
-    advance) over every sweep shape: 1-D / 2-D / n=1 axes, odd rows, S up to
-    40 (falls back where a tile does not fit), agents with collisions and
-    interior clamps: bit-identical to the oracle."""
+def test_resident_kernel_full_steps_bitwise(shape, S, kernel, monkeypatch):
+    """The single-launch multi-step kernels — the L2 dataflow kernel
+    (resident.cuh) and the one-cluster kernel (small.cuh, field in the
+    cluster's shared memory) — over every sweep shape: 1-D / 2-D / n=1 axes,
+    odd rows, S up to 40 (falls back where a tile does not fit), agents with
+    collisions and interior clamps: bit-identical to the oracle."""
     monkeypatch.setenv("BIODIFF_RESIDENT", "1")
+    monkeypatch.setenv("BIODIFF_SMALL", "1" if kernel == "cluster" else "0")
     w = W.make("t", shape, S, 120, 7, seed=sum(shape) + S, interior_clamps=3, immune_fraction=0.3)
     s = make_session(w)
     s.set_kernel_timing(True)
@@ -262,9 +265,13 @@ def test_resident_kernel_full_steps_bitwise(shape, S, monkeypatch):
     s.close()
 
 
-@pytest.mark.parametrize("cfg,steps", [("c1", 2000), ("c2", 300)])
-def test_resident_kernel_configs_bitwise(cfg, steps):
-    """C1 / C2 at full size take the resident kernel by default."""
+@pytest.mark.parametrize("cfg,steps,small", [("c1", 2000, "auto"), ("c1", 500, "0"), ("c2", 300, "auto")])
+def test_resident_kernel_configs_bitwise(cfg, steps, small, monkeypatch):
+    """C1 / C2 at full size take a single-launch kernel by default (C1: the
+    one-cluster kernel; C2: the L2 dataflow kernel); C1 also through the
+    dataflow kernel."""
+    if small != "auto":
+        monkeypatch.setenv("BIODIFF_SMALL", small)
     w = W.CONFIGS[cfg](steps)
     s = make_session(w)
     s.set_kernel_timing(True)

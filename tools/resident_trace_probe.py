@@ -32,6 +32,20 @@ def main():
     s.close()
     raw = np.fromfile(path, dtype=np.int64)
     max_tiles, grid, block, smem = raw[:4]
+    if max_tiles == -1:  # one-cluster kernel: [step][cta][8 phase stamps]
+        tr = raw[4:].view(np.uint64).reshape(8, grid, 12).astype(np.float64)
+        t0 = tr[tr > 0].min()
+        names = ["x", "y", "store+sync", "z", "sync", "load", "events"]
+        print(f"one-cluster kernel: {grid} CTAs x {block} threads, {smem} B smem")
+        for st in range(min(8, args.steps)):
+            v = tr[st]
+            spans = [(v[:, i + 1] - v[:, i]) / 1e3 for i in range(7)]
+            print(f"step {st}: start {(v[:, 0].min() - t0) / 1e3:8.2f} us, " + ", ".join(
+                f"{n} {sp.mean():5.2f}/{sp.max():5.2f}" for n, sp in zip(names, spans)) + "  (mean/max over CTAs, us)")
+            sub = [("store", 2, 8), ("sync1", 8, 3)]
+            print("        " + ", ".join(f"{n} {((v[:, b] - v[:, a]) / 1e3).mean():5.2f}/{((v[:, b] - v[:, a]) / 1e3).max():5.2f}"
+                                    for n, a, b in sub))
+        return
     tr = raw[4:].view(np.uint64).reshape(8, 4, max_tiles, 6).astype(np.float64)
     print(f"grid {grid} x {block} threads, {smem} B smem, {max_tiles} tiles max")
     t0 = tr[tr > 0].min()
