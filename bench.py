@@ -245,11 +245,21 @@ def main():
         return
 
     dist = None
+    # BIODIFF_BENCH_GLOO=1 (validation of the N>1 code path on a 1-GPU box):
+    # a gloo process group, every rank on GPU local % device_count, and the
+    # z-slab planes crossing through host buffers instead of NCCL (which
+    # refuses two ranks on one device). Driver runs use NCCL, one GPU per rank.
+    gloo = world > 1 and os.environ.get("BIODIFF_BENCH_GLOO") == "1"
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if gloo:
+            local = local % max(1, torch.cuda.device_count())
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_2110_13368_b200 as B
 
@@ -261,7 +271,7 @@ def main():
         if dist is None:
             return vals
         import torch
-        t = torch.tensor(vals, device=f"cuda:{device}", dtype=torch.float64)
+        t = torch.tensor(vals, device="cpu" if gloo else f"cuda:{device}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return [float(x) for x in t.tolist()]
 
@@ -278,10 +288,13 @@ def main():
         # k substrate shards x P z-slabs (shards.py); slabs of a shard exchange planes over NCCL.
         from paper_2110_13368_b200.shards import ShardRank, layout_for
         k, P = layout_for(world, w.S, w.n[2])
-        uids = [B.Session.nccl_unique_id() if (rank == 0 and P > 1) else None for _ in range(k)]
-        if dist is not None:
-            dist.broadcast_object_list(uids, src=0)
-        sr = ShardRank(w, rank, world, device, uids)
+        if gloo:
+            sr = ShardRank(w, rank, world, device, transport="host")
+        else:
+            uids = [B.Session.nccl_unique_id() if (rank == 0 and P > 1) else None for _ in range(k)]
+            if dist is not None:
+                dist.broadcast_object_list(uids, src=0)
+            sr = ShardRank(w, rank, world, device, uids)
         s = sr.session
         local_values = sr.values
         layout = (k, P)
@@ -485,6 +498,9 @@ def main():
         }
         if single is not None:
             line["single_gpu"] = single
+        if gloo:
+            line["validation_mode"] = ("BIODIFF_BENCH_GLOO=1: gloo process group, ranks sharing GPU(s), z-slab planes "
+                                       "through host buffers (not a scaling measurement)")
         print(json.dumps(line), flush=True)
     s.close()
     if dist is not None:
