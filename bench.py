@@ -448,7 +448,8 @@ def main():
         if layout:
             k, P = layout
             cfg["parallelism"] = (f"{k} substrate shard(s) x {P} z-slab(s) = {world} GPU(s): shards need no "
-                                  f"communication, slabs exchange interface planes over NCCL")
+                                  f"communication, slabs exchange interface planes over "
+                                  f"{'host buffers (gloo validation mode)' if gloo else 'NCCL'}")
         if ensemble:
             cfg["parallelism"] = f"{W.C5_REPLICAS} replicas sharded over {world} GPU(s), no communication, " \
                                  f"one stacked session per GPU"

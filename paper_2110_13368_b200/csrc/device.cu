@@ -856,7 +856,10 @@ bool DeviceSession::xy_cluster_pays() const
     const int yi = (mesh_.nx * S_ + kernels::kLanes - 1) / kernels::kLanes;
     const double plane_mb = static_cast<double>(mesh_.nx) * mesh_.ny * S_ * 8.0 / 1e6;
     const double clusters = std::min(static_cast<double>(mesh_.nz), sm_count_ / 4.0);
-    return xi >= 16 && yi >= 16 && plane_mb * clusters <= 80.0;
+    // Measured only to pay at S = 4 (C3: 0.587 vs 0.622 ms per step); at S = 2
+    // the same 256^2 planes run slower fused (0.46 vs 0.33 ms, r02
+    // tools/shard_probe.py), at S = 1 the x items are too few.
+    return S_ == 4 && xi >= 16 && yi >= 16 && plane_mb * clusters <= 80.0;
 }
 
 namespace {
