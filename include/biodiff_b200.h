@@ -363,6 +363,32 @@ int biodiff_zslab_link_local(biodiff_session** sessions, int32_t count);
 int biodiff_zslab_group_advance(biodiff_session** sessions, int32_t count, int64_t steps, double dt,
                                 int32_t with_sources);
 
+/* ---- XML configuration (the reference's config.hpp:75-116 schema) ---------
+ * `xml` is an in-memory document, or `path` (when non-null) a file:
+ * <simulation> with <domain>, <overall>, <parallel>, <microenvironment>
+ * (<substrate>*), <agents> (file | inline count/placement/seed/volume/rates),
+ * <save>; unknown elements, attributes, repeats and invalid values are
+ * status 1 (config_error) naming the element. */
+
+/* serialize_config(parse_config(...)) (config.cpp:325-398 canonical form);
+ * `needed` = bytes including the terminator; `out` filled when large enough. */
+int biodiff_config_canonical(const char* xml, const char* path, char* out, int64_t capacity, int64_t* needed);
+/* save_config (config.cpp:400-406). */
+int biodiff_config_save(const char* xml, const char* path, const char* out_path);
+/* build_microenvironment + build_agents (config.cpp:494-566): sizes (field ==
+ * NULL), then field[voxels*substrates], Dirichlet entries (voxel, mask[S],
+ * values[S]) and agents (ids, positions[3n], volume, secretion/uptake/
+ * saturation[n*S]). */
+int biodiff_config_build(const char* xml, const char* path, int64_t* voxels, int32_t* substrates,
+                         int64_t* dirichlet_count, int64_t* agent_count, double* field, int64_t* dir_voxel,
+                         uint8_t* dir_mask, double* dir_values, int64_t* ids, double* positions, double* volume,
+                         double* secretion, double* uptake, double* saturation);
+/* A ready session for a config: mesh, SolverWorkspaces::build at dt_diff,
+ * the boundary Dirichlet shell, the agents, the initial field; `clock`
+ * (optional) = biodiff_clock_make(dt_diff, dt_mech, dt_cell, max_time). */
+int biodiff_session_from_config(const char* xml, const char* path, int32_t device, biodiff_session** out,
+                                biodiff_clock* clock);
+
 #ifdef __cplusplus
 }
 #endif

@@ -432,3 +432,72 @@ def nproc():
 
 def now():
     return time.perf_counter()
+
+
+# ---- the reference's own XML config layer (config.cpp via oracle/boost_shim) ----
+
+def _ref_cfg():
+    L = ref_lib()
+    if not getattr(L, "_cfg_bound", False):
+        L.ref_config_last_error.restype = ctypes.c_char_p
+        L.ref_config_canonical.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, _i64, _P(_i64)]
+        L.ref_config_build.argtypes = [ctypes.c_char_p, ctypes.c_char_p, _P(_i64), _P(ctypes.c_int), _P(_i64),
+                                       _P(_i64), _P(_d), _P(_i64), _P(_u8), _P(_d), _P(_i64), _P(_d), _P(_d),
+                                       _P(_d), _P(_d), _P(_d)]
+        L.ref_config_run.argtypes = [ctypes.c_char_p, ctypes.c_char_p, _i64, ctypes.c_int, _P(_d), _i64]
+        L._cfg_bound = True
+    return L
+
+
+def _cfg_args(xml, path):
+    return (xml.encode() if xml is not None else None), (str(path).encode() if path is not None else None)
+
+
+def ref_config_canonical(xml=None, path=None):
+    """(status, text): serialize_config(parse_config...) of the reference
+    (config.cpp:295-398), or its error status (1 config_error, 4 io_error)
+    and message."""
+    L = _ref_cfg()
+    x, p = _cfg_args(xml, path)
+    need = _i64()
+    rc = L.ref_config_canonical(x, p, None, 0, ctypes.byref(need))
+    if rc:
+        return rc, L.ref_config_last_error().decode()
+    buf = ctypes.create_string_buffer(need.value)
+    L.ref_config_canonical(x, p, buf, need.value, ctypes.byref(need))
+    return 0, buf.value.decode()
+
+
+def ref_config_build(xml=None, path=None):
+    """build_microenvironment + build_agents of the reference (config.cpp:494-566)."""
+    L = _ref_cfg()
+    x, p = _cfg_args(xml, path)
+    nv, S, nd, na = _i64(), ctypes.c_int(), _i64(), _i64()
+    rc = L.ref_config_build(x, p, ctypes.byref(nv), ctypes.byref(S), ctypes.byref(nd), ctypes.byref(na),
+                            *([None] * 10))
+    if rc:
+        raise RuntimeError(L.ref_config_last_error().decode())
+    S_, nd_, na_ = S.value, nd.value, na.value
+    out = {"S": S_, "field": np.empty(nv.value * S_), "dir_voxel": np.empty(nd_, np.int64),
+           "dir_mask": np.empty(nd_ * S_, np.uint8), "dir_values": np.empty(nd_ * S_),
+           "ids": np.empty(na_, np.int64), "positions": np.empty(3 * na_), "volume": np.empty(na_),
+           "secretion": np.empty(na_ * S_), "uptake": np.empty(na_ * S_), "saturation": np.empty(na_ * S_)}
+    types = {"dir_voxel": _i64, "dir_mask": _u8, "ids": _i64}
+    ptrs = [out[k].ctypes.data_as(_P(types.get(k, _d))) for k in
+            ("field", "dir_voxel", "dir_mask", "dir_values", "ids", "positions", "volume", "secretion", "uptake",
+             "saturation")]
+    L.ref_config_build(x, p, ctypes.byref(nv), ctypes.byref(S), ctypes.byref(nd), ctypes.byref(na), *ptrs)
+    return out
+
+
+def ref_config_run(steps, xml=None, path=None, workers=0, count=None):
+    """The reference's step loop from a config: the final field."""
+    L = _ref_cfg()
+    x, p = _cfg_args(xml, path)
+    if count is None:
+        count = ref_config_build(xml, path)["field"].size
+    field = np.empty(count)
+    rc = L.ref_config_run(x, p, steps, workers, field.ctypes.data_as(_P(_d)), count)
+    if rc:
+        raise RuntimeError(L.ref_config_last_error().decode())
+    return field

@@ -98,6 +98,12 @@ _SIGNATURES = {
     "biodiff_last_error": (ctypes.c_char_p, []),
     "biodiff_version": (_i32, []),
     "biodiff_build_flags": (_i32, []),
+    "biodiff_config_canonical": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, _i64, _P(_i64)]),
+    "biodiff_config_save": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p]),
+    "biodiff_config_build": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, _P(_i64), _P(_i32), _P(_i64), _P(_i64),
+                                            _P(_d), _P(_i64), _P(ctypes.c_uint8), _P(_d), _P(_i64), _P(_d), _P(_d),
+                                            _P(_d), _P(_d), _P(_d)]),
+    "biodiff_session_from_config": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, _i32, _P(_vp), _vp]),
     "biodiff_mesh_from_bounds": (ctypes.c_int, [_d] * 9 + [_P(Mesh)]),
     "biodiff_nearest_voxel": (ctypes.c_int, [_P(Mesh), _P(_d), _P(_i64)]),
     "biodiff_precompute_thomas": (ctypes.c_int, [_P(Mesh), _i32, _P(_d), _P(_d), _d, _i32, _i32, _P(_d), _P(_d), _P(_d)]),
@@ -276,6 +282,74 @@ def precompute_thomas_coefficients(mesh: Mesh, diffusion, decay, dt: float, axis
     _check(lib().biodiff_precompute_thomas(ctypes.byref(mesh), S, _dptr(D), _dptr(L), dt, axis, dims,
                                            _dptr(q), _dptr(dinv), _dptr(cb)))
     return q, dinv.reshape(n, S), cb.reshape(n, S)
+
+
+def _cfg_args(xml, path):
+    if (xml is None) == (path is None):
+        raise ValueError("give exactly one of xml (a document) or path (a file)")
+    return (xml.encode() if xml is not None else None), (str(path).encode() if path is not None else None)
+
+
+def config_canonical(xml: Optional[str] = None, path=None) -> str:
+    """serialize_config(parse_config...) of an XML configuration (the
+    reference's schema, config.hpp:75-91): the canonical document."""
+    x, p = _cfg_args(xml, path)
+    need = _i64()
+    _check(lib().biodiff_config_canonical(x, p, None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    _check(lib().biodiff_config_canonical(x, p, buf, need.value, ctypes.byref(need)))
+    return buf.value.decode()
+
+
+def config_save(out_path, xml: Optional[str] = None, path=None) -> None:
+    """save_config: writes the canonical document of a configuration."""
+    x, p = _cfg_args(xml, path)
+    _check(lib().biodiff_config_save(x, p, str(out_path).encode()))
+
+
+def config_build(xml: Optional[str] = None, path=None) -> dict:
+    """build_microenvironment + build_agents of a configuration (config.cpp:494-566):
+    the initial field, the Dirichlet entries and the agents, as arrays."""
+    x, p = _cfg_args(xml, path)
+    nv, S, nd, na = _i64(), _i32(), _i64(), _i64()
+    nul = [None] * 10
+    _check(lib().biodiff_config_build(x, p, ctypes.byref(nv), ctypes.byref(S), ctypes.byref(nd), ctypes.byref(na),
+                                      *nul))
+    S_, nd_, na_ = int(S.value), int(nd.value), int(na.value)
+    out = {"S": S_, "field": np.empty(int(nv.value) * S_), "dir_voxel": np.empty(nd_, np.int64),
+           "dir_mask": np.empty(nd_ * S_, np.uint8), "dir_values": np.empty(nd_ * S_), "ids": np.empty(na_, np.int64),
+           "positions": np.empty(3 * na_), "volume": np.empty(na_), "secretion": np.empty(na_ * S_),
+           "uptake": np.empty(na_ * S_), "saturation": np.empty(na_ * S_)}
+    ptrs = [out[k].ctypes.data_as(_P(t)) for k, t in (("field", _d), ("dir_voxel", _i64), ("dir_mask", ctypes.c_uint8),
+                                                      ("dir_values", _d), ("ids", _i64), ("positions", _d),
+                                                      ("volume", _d), ("secretion", _d), ("uptake", _d),
+                                                      ("saturation", _d))]
+    _check(lib().biodiff_config_build(x, p, ctypes.byref(nv), ctypes.byref(S), ctypes.byref(nd), ctypes.byref(na),
+                                      *ptrs))
+    return out
+
+
+def session_from_config(xml: Optional[str] = None, path=None, device: int = 0):
+    """A ready Session for a configuration (mesh, coefficients at dt_diff,
+    boundary Dirichlet shell, agents, initial field) and its clock
+    (dt_diff, dt_mech, dt_cell, max_time, total_steps)."""
+    import re
+    from paper_2110_13368_b200.engine import CClock
+    x, p = _cfg_args(xml, path)
+    h = _vp()
+    clk = CClock()
+    _check(lib().biodiff_session_from_config(x, p, device, ctypes.byref(h), ctypes.addressof(clk)))
+    canon = config_canonical(xml=xml, path=path)
+    num = {k: float(v) for k, v in re.findall(r"<(x_min|x_max|y_min|y_max|z_min|z_max|dx|dy|dz)>([^<]+)<", canon)}
+    mesh = mesh_from_bounds(num["x_min"], num["x_max"], num["y_min"], num["y_max"], num["z_min"], num["z_max"],
+                            num["dx"], num["dy"], num["dz"])
+    s = Session.__new__(Session)
+    s.mesh, s.S_total, s.S = mesh, canon.count("<substrate>"), canon.count("<substrate>")
+    s.zslab, s.shard, s.replicas = None, None, 1
+    s._h = h
+    clock = {k: getattr(clk, k) for k in ("dt_diff", "dt_mech", "dt_cell", "t_max", "per_mech", "per_cell",
+                                          "total_steps")}
+    return s, clock
 
 
 def experimental_build() -> bool:

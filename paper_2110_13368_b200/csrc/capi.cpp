@@ -4,6 +4,7 @@
 // SPEC.md:499): config_error -> 1, io_error -> 4, everything else -> 2.
 #include "../../include/biodiff_b200.h"
 
+#include "config.hpp"
 #include "device.hpp"
 #include "engine.hpp"
 #include "host.hpp"
@@ -1129,3 +1130,97 @@ int biodiff_zslab_group_advance(biodiff_session** sessions, int32_t count, int64
 }
 
 } // extern "C"
+
+// ---- XML configuration (config.hpp; the reference's config.hpp:75-116) ----
+
+namespace {
+
+SimConfig config_from(const char* xml, const char* path)
+{
+    if (path) return parse_config(path);
+    need(xml, "xml");
+    return parse_config_text(xml);
+}
+
+} // namespace
+
+int biodiff_config_canonical(const char* xml, const char* path, char* out, int64_t capacity, int64_t* needed)
+{
+    return guarded([&] {
+        need(needed, "needed");
+        const std::string text = serialize_config(config_from(xml, path));
+        *needed = static_cast<int64_t>(text.size()) + 1;
+        if (out && capacity >= *needed) std::memcpy(out, text.c_str(), text.size() + 1);
+    });
+}
+
+int biodiff_config_save(const char* xml, const char* path, const char* out_path)
+{
+    return guarded([&] {
+        need(out_path, "out_path");
+        save_config(config_from(xml, path), out_path);
+    });
+}
+
+int biodiff_config_build(const char* xml, const char* path, int64_t* voxels, int32_t* substrates,
+                         int64_t* dirichlet_count, int64_t* agent_count, double* field, int64_t* dir_voxel,
+                         uint8_t* dir_mask, double* dir_values, int64_t* ids, double* positions, double* volume,
+                         double* secretion, double* uptake, double* saturation)
+{
+    return guarded([&] {
+        need(voxels, "voxels");
+        need(substrates, "substrates");
+        need(dirichlet_count, "dirichlet_count");
+        need(agent_count, "agent_count");
+        const SimConfig cfg = config_from(xml, path);
+        const Microenvironment env = build_microenvironment(cfg);
+        const AgentPopulation agents = build_agents(cfg, env.mesh);
+        const int S = env.substrate_count();
+        *voxels = env.mesh.voxel_count();
+        *substrates = S;
+        *dirichlet_count = static_cast<int64_t>(env.dirichlet.size());
+        *agent_count = static_cast<int64_t>(agents.size());
+        if (!field) return; // sizes only
+        std::memcpy(field, env.field.values.data(), sizeof(double) * env.field.values.size());
+        int64_t e = 0;
+        for (const auto& d : env.dirichlet.entries()) {
+            dir_voxel[e] = d.voxel;
+            std::copy(d.mask.begin(), d.mask.end(), dir_mask + e * S);
+            std::copy(d.values.begin(), d.values.end(), dir_values + e * S);
+            ++e;
+        }
+        int64_t a = 0;
+        for (const auto& c : agents.agents()) {
+            ids[a] = c.id;
+            std::copy(c.position.begin(), c.position.end(), positions + 3 * a);
+            volume[a] = c.volume;
+            std::copy(c.secretion_rates.begin(), c.secretion_rates.end(), secretion + a * S);
+            std::copy(c.uptake_rates.begin(), c.uptake_rates.end(), uptake + a * S);
+            std::copy(c.saturation_densities.begin(), c.saturation_densities.end(), saturation + a * S);
+            ++a;
+        }
+    });
+}
+
+int biodiff_session_from_config(const char* xml, const char* path, int32_t device, biodiff_session** out,
+                                biodiff_clock* clock)
+{
+    return guarded([&] {
+        need(out, "out");
+        *out = nullptr;
+        const SimConfig cfg = config_from(xml, path);
+        const Microenvironment env = build_microenvironment(cfg);
+        const AgentPopulation agents = build_agents(cfg, env.mesh);
+        auto s = std::make_unique<biodiff_session>();
+        s->mesh = env.mesh;
+        s->S = env.substrate_count();
+        s->s1 = s->S;
+        s->dev = std::make_unique<DeviceSession>(s->mesh, s->S, device);
+        upload_workspaces(s.get(), SolverWorkspaces::build(env.mesh, env.substrates, cfg.dt_diff));
+        s->dev->set_dirichlet(env.dirichlet);
+        if (!agents.empty()) install_agents(s.get(), agents);
+        s->dev->upload(env.field.values.data(), static_cast<std::int64_t>(env.field.values.size()));
+        if (clock) to_c_clock(SimulationClock::make(cfg.dt_diff, cfg.dt_mech, cfg.dt_cell, cfg.max_time), clock);
+        *out = s.release();
+    });
+}
