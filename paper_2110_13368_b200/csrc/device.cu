@@ -1551,8 +1551,9 @@ void DeviceSession::launch_resident(std::int64_t steps, double dt, bool with_sou
 
 // Cluster size, planes per CTA, row pitch and dynamic smem of the one-cluster
 // kernel, or false when the field does not fit (or the mode is off).
-bool DeviceSession::small_config(int& cl, int& planes, int& pitch, int& smem_bytes) const
+bool DeviceSession::small_config(int& cl, int& planes, int& pitch, int& smem_bytes, bool& grid) const
 {
+    grid = false;
     if (small_mode_ == 0 || resident_mode_ == 0 || replicas_ != 1 || slab_ || S_ > kernels::kLanes) return false;
     for (int ax = 0; ax < 3; ++ax)
         if (!ws_[ax].active || ws_[ax].n < 2) return false;
@@ -1575,24 +1576,41 @@ bool DeviceSession::small_config(int& cl, int& planes, int& pitch, int& smem_byt
             return true;
         }
     }
+    // Grid mode: one CTA per slab of planes, all co-resident (one per SM),
+    // grid barriers instead of cluster barriers.
+    for (planes = std::max(1, (mesh_.nz + sm_count_ - 1) / sm_count_); planes * mesh_.ny <= 256; ++planes) {
+        if (rowlen % 2 != 0 || rowlen > 256) break;
+        pitch = rowlen;
+        const long long slab = std::max<long long>(static_cast<long long>(planes) * mesh_.ny * pitch,
+                                                   static_cast<long long>(mesh_.nz) * kThreads);
+        const long long bytes = (16 + coef + slab) * 8;
+        if (bytes > 227 * 1024) continue;
+        cl = (mesh_.nz + planes - 1) / planes;
+        smem_bytes = static_cast<int>(bytes);
+        grid = true;
+        return true;
+    }
     return false;
 }
 
 bool DeviceSession::small_path() const
 {
     int cl, planes, pitch, smem;
-    if (!small_config(cl, planes, pitch, smem)) return false;
+    bool grid;
+    if (!small_config(cl, planes, pitch, smem, grid)) return false;
     if (small_mode_ == 1) return true;
-    // auto: where the one-cluster kernel measured faster than the L2 dataflow
-    // kernel (BIODIFF_SMALL_MB, default 2 MB: C1's 1 MB field).
-    return static_cast<double>(value_count()) * 8.0 / 1e6 <= std::atof(env_or("BIODIFF_SMALL_MB", "2"));
+    // auto: where it measured faster than the L2 dataflow kernel — the
+    // one-cluster mode (C1: 19.0 vs 27.3 us per step) and the slab-grid mode
+    // (C2: 41.4 vs 43.4 us) — for fields up to BIODIFF_SMALL_MB (32 MB).
+    return static_cast<double>(value_count()) * 8.0 / 1e6 <= std::atof(env_or("BIODIFF_SMALL_MB", "32"));
 }
 
 void DeviceSession::launch_small(std::int64_t steps, double dt, bool with_sources)
 {
     auto st = static_cast<cudaStream_t>(stream_);
     int cl = 0, planes = 0, pitch = 0, smem = 0;
-    if (!small_config(cl, planes, pitch, smem)) throw state_error("field does not fit the one-cluster kernel");
+    bool grid = false;
+    if (!small_config(cl, planes, pitch, smem, grid)) throw state_error("field does not fit the one-cluster kernel");
     kernels::Small a{};
     a.rho = rho_;
     a.nx = mesh_.nx;
@@ -1645,9 +1663,11 @@ void DeviceSession::launch_small(std::int64_t steps, double dt, bool with_source
                                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             throw state_error("slab tensor map");
     }
+    a.grid = grid ? 1 : 0;
+    a.bar = res_cnt_; // grid mode: two words of the resident kernel's counter block
     const void* fn = reinterpret_cast<const void*>(kernels::step_small);
     ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
-    if (cl > 8) ck(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1), "cluster 16");
+    if (!grid && cl > 8) ck(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1), "cluster 16");
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(cl);
     cfg.blockDim = dim3(256);
@@ -1668,7 +1688,14 @@ void DeviceSession::launch_small(std::int64_t steps, double dt, bool with_source
     }
     void* args[] = {tmap, &a};
     begin_kernel(kResident);
-    ck(cudaLaunchKernelExC(&cfg, fn, args), "launch one-cluster kernel");
+    if (grid) {
+        ck(cudaMemsetAsync(res_cnt_, 0, 2 * sizeof(unsigned), st), "barrier reset");
+        ck(cudaLaunchCooperativeKernel(fn, dim3(static_cast<unsigned>(cl)), dim3(256), args, static_cast<std::size_t>(smem),
+                                       st),
+           "launch slab-grid kernel");
+    } else {
+        ck(cudaLaunchKernelExC(&cfg, fn, args), "launch one-cluster kernel");
+    }
     end_kernel(kResident);
     if (trace_path) {
         std::vector<unsigned long long> h(trace_n);

@@ -186,7 +186,7 @@ private:
     void launch_resident(std::int64_t steps, double dt, bool with_sources);
     // ---- one-cluster kernel (small.cuh): fields that fit a cluster's smem
     int small_mode_ = -1; // BIODIFF_SMALL: 0 off, 1 forced where it fits, -1 auto
-    bool small_config(int& cl, int& planes, int& pitch, int& smem_bytes) const;
+    bool small_config(int& cl, int& planes, int& pitch, int& smem_bytes, bool& grid) const;
     void launch_small(std::int64_t steps, double dt, bool with_sources);
 
     bool slab_ = false;

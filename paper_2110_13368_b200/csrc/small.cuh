@@ -57,6 +57,8 @@ struct Small {
     int slab_doubles;   // max(planes*ny*pitch, nz*blockDim) doubles
     int coef_doubles;
     int tma;            // slab moves by one 2-D TMA box (pitch == rowlen)
+    int grid;           // 1: cooperative grid of slab CTAs with grid barriers (else one cluster)
+    unsigned* bar;      // grid mode: [arrivals, generation], zeroed before the launch
     unsigned long long* trace; // design probe: [step<8][cta][8] globaltimer stamps (thread 0 of each CTA)
 };
 #define SMALL_STAMP(I)                                                                                            \
@@ -67,7 +69,29 @@ __global__ void __launch_bounds__(256, 1) step_small(const __grid_constant__ CUt
     extern __shared__ __align__(128) double smem_small[];
     const int tid = threadIdx.x, nt = blockDim.x;
     const int lane = tid % kLanes, warp = tid / kLanes, nw = nt / kLanes;
-    const int C = static_cast<int>(cluster_nctarank()), cr = static_cast<int>(cluster_ctarank());
+    // Cluster mode: one cluster, cluster barriers. Grid mode (a.grid): a
+    // cooperative launch of one CTA per slab of planes (fields too large for
+    // one cluster's shared memory, e.g. C2), grid barriers.
+    const int C = a.grid ? static_cast<int>(gridDim.x) : static_cast<int>(cluster_nctarank());
+    const int cr = a.grid ? static_cast<int>(blockIdx.x) : static_cast<int>(cluster_ctarank());
+    unsigned gen = 0;
+    auto sync_all = [&]() {
+        if (!a.grid) {
+            cluster_sync();
+            return;
+        }
+        __syncthreads();
+        if (tid == 0) { // arrival counter + generation word; acquire also invalidates this SM's L1
+            if (ptx::atom_acq_rel_add(a.bar, 1u) == static_cast<unsigned>(C) - 1) {
+                atomicExch(a.bar, 0u);
+                ptx::st_release(a.bar + 1, gen + 1);
+            } else {
+                while (ptx::ld_acquire(a.bar + 1) == gen) __nanosleep(32);
+            }
+            ++gen;
+        }
+        __syncthreads();
+    };
     const int S = a.S;
     const long long rowlen = static_cast<long long>(a.nx) * S;
     const long long plane = static_cast<long long>(a.ny) * rowlen;
@@ -161,7 +185,7 @@ __global__ void __launch_bounds__(256, 1) step_small(const __grid_constant__ CUt
         SMALL_STAMP(2)
         store_slab();
         SMALL_STAMP(8)
-        cluster_sync();
+        sync_all();
         SMALL_STAMP(3)
         // ---- z: the cluster's columns (j, e), C-way split; column block of
         // the CTA's threads in the free slab memory ([m][thread]).
@@ -187,7 +211,7 @@ __global__ void __launch_bounds__(256, 1) step_small(const __grid_constant__ CUt
             ptx::fence_proxy_async_smem(); // generic writes of the column block before the slab's TMA refill
         }
         SMALL_STAMP(4)
-        cluster_sync();
+        sync_all();
         SMALL_STAMP(5)
         // ---- residual Dirichlet entries (solver.cpp:298), then the sources
         // (agents.cpp:97-109), on the L2 copy, spread over every thread of
@@ -198,7 +222,7 @@ __global__ void __launch_bounds__(256, 1) step_small(const __grid_constant__ CUt
                 const int s = static_cast<int>(it % S);
                 if (a.dir_mask[q * S + s]) a.rho[a.dir_voxel[q] * S + s] = a.dir_values[q * S + s];
             }
-            if (a.sources) cluster_sync();
+            if (a.sources) sync_all();
         }
         if (a.sources) {
             const long long glo = *a.g_lo, ghi = *a.g_hi;
@@ -223,7 +247,7 @@ __global__ void __launch_bounds__(256, 1) step_small(const __grid_constant__ CUt
                 *p = x;
             }
         }
-        if (a.dir_count || a.sources) cluster_sync();
+        if (a.dir_count || a.sources) sync_all();
         SMALL_STAMP(6)
         load_slab();
         SMALL_STAMP(7)

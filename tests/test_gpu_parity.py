@@ -265,10 +265,11 @@ def test_resident_kernel_full_steps_bitwise(shape, S, kernel, monkeypatch):
     s.close()
 
 
-@pytest.mark.parametrize("cfg,steps,small", [("c1", 2000, "auto"), ("c1", 500, "0"), ("c2", 300, "auto")])
+@pytest.mark.parametrize("cfg,steps,small", [("c1", 2000, "auto"), ("c1", 500, "0"), ("c2", 300, "auto"),
+                                             ("c2", 300, "0")])
 def test_resident_kernel_configs_bitwise(cfg, steps, small, monkeypatch):
     """C1 / C2 at full size take a single-launch kernel by default (C1: the
-    one-cluster kernel; C2: the L2 dataflow kernel); C1 also through the
+    one-cluster kernel; C2: its slab-grid mode); both also through the L2
     dataflow kernel."""
     if small != "auto":
         monkeypatch.setenv("BIODIFF_SMALL", small)

@@ -64,6 +64,7 @@ def main(argv):
         "xy_cluster_4x8": ({"BIODIFF_XY_FUSED": "2", "BIODIFF_XYC_WARPS": "8", "BIODIFF_XYC_CLUSTER": "4"}, wb, False),
         "resident": ({"BIODIFF_RESIDENT": "1"}, wc, False),
         "resident_dirichlet": ({"BIODIFF_RESIDENT": "1"}, wa, False),
+        "dataflow": ({"BIODIFF_RESIDENT": "1", "BIODIFF_SMALL": "0"}, wa, False),
         "regroup": ({"BIODIFF_RESIDENT": "0"}, wc, True),
     }
     chosen = argv or list(cases) + ["xyz_cluster"]
