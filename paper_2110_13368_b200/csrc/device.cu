@@ -1549,6 +1549,17 @@ void DeviceSession::launch_resident(std::int64_t steps, double dt, bool with_sou
 
 // ---- one-cluster kernel for fields that fit a cluster's shared memory (small.cuh)
 
+// Shared row pitch of the one-cluster / slab-grid kernel: the TMA box is
+// `pitch` doubles wide (columns past the row zero-filled on load, clipped on
+// store), chosen so the (line, substrate) lanes of the x chains spread over
+// the bank pairs: pitch = S (mod 16) for even S (conflict-free), 2 (mod 16)
+// for odd S (the box width must stay a multiple of 16 bytes).
+static int small_pitch(int rowlen, int S)
+{
+    const int want = S % 2 == 0 ? S % 16 : 2;
+    return rowlen + ((want - rowlen) % 16 + 16) % 16;
+}
+
 // Cluster size, planes per CTA, row pitch and dynamic smem of the one-cluster
 // kernel, or false when the field does not fit (or the mode is off).
 bool DeviceSession::small_config(int& cl, int& planes, int& pitch, int& smem_bytes, bool& grid) const
@@ -1564,9 +1575,9 @@ bool DeviceSession::small_config(int& cl, int& planes, int& pitch, int& smem_byt
         planes = (mesh_.nz + c - 1) / c;
         // TMA slab moves need 16-byte rows and a box of <= 256 x 256; the
         // rows are then dense (pitch = rowlen), else padded to S mod 16.
-        const bool tma = rowlen % 2 == 0 && rowlen <= 256 && planes * mesh_.ny <= 256;
+        pitch = small_pitch(rowlen, S_);
+        const bool tma = rowlen % 2 == 0 && pitch <= 256 && planes * mesh_.ny <= 256;
         if (!tma) continue; // slab moves by TMA only (the one-cluster kernel's supported shapes)
-        pitch = rowlen;
         const long long slab = std::max<long long>(static_cast<long long>(planes) * mesh_.ny * pitch,
                                                    static_cast<long long>(mesh_.nz) * kThreads);
         const long long bytes = (16 + coef + slab) * 8;
@@ -1579,8 +1590,8 @@ bool DeviceSession::small_config(int& cl, int& planes, int& pitch, int& smem_byt
     // Grid mode: one CTA per slab of planes, all co-resident (one per SM),
     // grid barriers instead of cluster barriers.
     for (planes = std::max(1, (mesh_.nz + sm_count_ - 1) / sm_count_); planes * mesh_.ny <= 256; ++planes) {
-        if (rowlen % 2 != 0 || rowlen > 256) break;
-        pitch = rowlen;
+        pitch = small_pitch(rowlen, S_);
+        if (rowlen % 2 != 0 || pitch > 256) break;
         const long long slab = std::max<long long>(static_cast<long long>(planes) * mesh_.ny * pitch,
                                                    static_cast<long long>(mesh_.nz) * kThreads);
         const long long bytes = (16 + coef + slab) * 8;
@@ -1642,7 +1653,7 @@ void DeviceSession::launch_small(std::int64_t steps, double dt, bool with_source
     a.coef_doubles = (resident_coef_doubles() + 15) / 16 * 16;
     a.slab_doubles = smem / 8 - 16 - a.coef_doubles;
     const long long rowlen = static_cast<long long>(mesh_.nx) * S_;
-    a.tma = pitch == rowlen && rowlen % 2 == 0 ? std::atoi(env_or("BIODIFF_SMALL_TMA_MASK", "3")) : 0;
+    a.tma = rowlen % 2 == 0 ? std::atoi(env_or("BIODIFF_SMALL_TMA_MASK", "3")) : 0;
     alignas(64) unsigned char tmap[128] = {};
     if (a.tma) { // 4-D view (row, (plane, j) row index, 1, 1), box (rowlen, planes * ny)
         void* efn = nullptr;
@@ -1655,7 +1666,7 @@ void DeviceSession::launch_small(std::int64_t steps, double dt, bool with_source
                                     static_cast<cuuint64_t>(mesh_.ny) * static_cast<cuuint64_t>(mesh_.nz), 1, 1};
         const cuuint64_t total = static_cast<cuuint64_t>(rowlen) * mesh_.ny * mesh_.nz * 8;
         const cuuint64_t strides[3] = {static_cast<cuuint64_t>(rowlen) * 8, total, total};
-        const cuuint32_t box[4] = {static_cast<cuuint32_t>(rowlen), static_cast<cuuint32_t>(planes * mesh_.ny), 1, 1};
+        const cuuint32_t box[4] = {static_cast<cuuint32_t>(pitch), static_cast<cuuint32_t>(planes * mesh_.ny), 1, 1};
         const cuuint32_t estr[4] = {1, 1, 1, 1};
         if (reinterpret_cast<Encode>(efn)(reinterpret_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
                                           rho_, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,

@@ -56,7 +56,8 @@ struct Small {
     long long steps;
     int slab_doubles;   // max(planes*ny*pitch, nz*blockDim) doubles
     int coef_doubles;
-    int tma;            // slab moves by one 2-D TMA box (pitch == rowlen)
+    int tma;            // slab moves by one 2-D TMA box of pitch x rows (columns past rowlen: zero-filled on
+                        // load, clipped on store)
     int grid;           // 1: cooperative grid of slab CTAs with grid barriers (else one cluster)
     unsigned* bar;      // grid mode: [arrivals, generation], zeroed before the launch
     unsigned long long* trace; // design probe: [step<8][cta][8] globaltimer stamps (thread 0 of each CTA)
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(256, 1) step_small(const __grid_constant__ CUt
         if (a.tma & 1) {
             if (tid == 0) {
                 ptx::fence_proxy_async_global(); // other CTAs' generic writes (z, sources) before the async read
-                ptx::mbar_arrive_expect_tx(bar, static_cast<uint32_t>(a.planes * a.ny * rowlen * 8));
+                ptx::mbar_arrive_expect_tx(bar, static_cast<uint32_t>(a.planes * a.ny * a.pitch * 8));
                 ptx::tma_load_4d(slab, &tmap_slab, 0, k0 * a.ny, 0, 0, bar);
             }
             ptx::mbar_wait(bar, phase);
