@@ -309,8 +309,8 @@ void DeviceSession::rebuild_voxel_grouping()
     m.key_span = m.vox_hi - m.vox_lo;
     m.sentinel = m.key_span * replicas_;
     const int end_bit = bits_for(m.sentinel);
-    const unsigned long long none = ~0ull;
-    ck(cudaMemcpyAsync(agent_bad_, &none, sizeof(none), cudaMemcpyHostToDevice, st), "reset");
+    if (!host_pin_) ck(cudaMallocHost(&host_pin_, 64), "cudaMallocHost"); // pinned: the two read-backs below
+    ck(cudaMemsetAsync(agent_bad_, 0xff, sizeof(unsigned long long), st), "reset"); // ~0: no agent outside
     const int block = 256;
     begin_kernel(kAux);
     agent_keys<<<blocks(N, block), block, 0, st>>>(in_pos_, in_rep_, N, m, id_order_, keys_a_, agent_bad_);
@@ -318,9 +318,10 @@ void DeviceSession::rebuild_voxel_grouping()
     // The domain check comes before any group array is touched: a failed
     // rebuild keeps the previous grouping, as the reference does (its
     // nearest_voxel throws before groups_ is reassigned, agents.cpp:56-73).
-    unsigned long long bad = 0;
-    ck(cudaMemcpyAsync(&bad, agent_bad_, sizeof(bad), cudaMemcpyDeviceToHost, st), "download");
+    auto* pin = static_cast<unsigned long long*>(host_pin_);
+    ck(cudaMemcpyAsync(pin, agent_bad_, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "download");
     ck(cudaStreamSynchronize(st), "sync");
+    const unsigned long long bad = pin[0];
     if (bad != ~0ull) {
         // mesh.cpp:74-76 (nearest_voxel's std::domain_error, same message).
         double p[3];
@@ -351,8 +352,8 @@ void DeviceSession::rebuild_voxel_grouping()
     rep_group_bounds<<<blocks(replicas_ + 1, block), block, 0, st>>>(group_voxel_, agent_counts_, m.key_span,
                                                                       replicas_, rep_groups_);
     end_kernel(kAux);
-    long long counts[2] = {0, 0};
-    ck(cudaMemcpyAsync(counts, agent_counts_, sizeof(counts), cudaMemcpyDeviceToHost, st), "download");
+    auto* counts = reinterpret_cast<long long*>(host_pin_) + 1;
+    ck(cudaMemcpyAsync(counts, agent_counts_, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st), "download");
     ck(cudaStreamSynchronize(st), "sync");
     factors_valid_ = false;
     res_grp_valid_ = false;

@@ -258,6 +258,7 @@ DeviceSession::~DeviceSession()
     dfree(shell_values_);
     dfree(xy_ctr_);
     dfree(xyc_ctr_);
+    if (host_pin_) cudaFreeHost(host_pin_);
     dfree(res_cnt_);
     dfree(res_tile_cnt_);
     dfree(res_dir_off_);
