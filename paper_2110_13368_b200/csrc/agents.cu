@@ -170,6 +170,114 @@ __global__ void agent_sample(const int64_t* keys_sorted, const int64_t* order, c
     out[order[i] * S + s] = rho[keys_sorted[i] * S + s];
 }
 
+// Small populations (one replica, no slab filter, N <= kSmallRegroup): the
+// whole pipeline above in ONE CTA — keys (same domain check and voxel rule),
+// a bitonic sort of (key << 32 | id rank) in shared memory (= the stable
+// radix sort's (key, id) order), group flags, a block scan, the CSR, the
+// gather — so a regroup costs one launch and one read-back instead of ~12
+// launches and two. An agent outside the domain leaves every live array
+// untouched (the reference's failed rebuild keeps the old grouping).
+constexpr long long kSmallRegroup = 2048; // measured: C1 (1000 agents) 65.6 -> 44.7 us per regroup; at 10k agents the one-CTA sort loses to CUB (304 us)
+
+__global__ void __launch_bounds__(1024) regroup_small(const double* pos, long long N, AgentMesh m,
+                                                      const int64_t* id_order, int S, const double* vol,
+                                                      const double* sec, const double* upt, const double* sat,
+                                                      int64_t* keys_sorted, int64_t* order, int64_t* group_voxel,
+                                                      int64_t* group_offsets, int64_t* counts, int64_t* rep_groups,
+                                                      double* vol_g, double* sec_g, double* upt_g, double* sat_g,
+                                                      unsigned long long* bad)
+{
+    extern __shared__ unsigned long long sk[]; // [P] packed keys, then [1024] scan partials
+    __shared__ unsigned long long s_bad;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    long long P = 1;
+    while (P < N) P <<= 1;
+    unsigned long long* part = sk + P;
+    if (tid == 0) s_bad = ~0ull;
+    __syncthreads();
+    for (long long r = tid; r < P; r += nt) {
+        if (r >= N) {
+            sk[r] = ~0ull;
+            continue;
+        }
+        const long long a = id_order[r];
+        const double p0 = pos[3 * a], p1 = pos[3 * a + 1], p2 = pos[3 * a + 2];
+        const bool inside = p0 >= m.lo[0] && p0 <= m.hi[0] && p1 >= m.lo[1] && p1 <= m.hi[1] && p2 >= m.lo[2] &&
+                            p2 <= m.hi[2];
+        if (!inside) {
+            atomicMin(&s_bad, static_cast<unsigned long long>(a));
+            sk[r] = ~0ull;
+            continue;
+        }
+        const int i = cell_of(p0, m.lo[0], m.h[0], m.n[0]);
+        const int j = cell_of(p1, m.lo[1], m.h[1], m.n[1]);
+        const int k = cell_of(p2, m.lo[2], m.h[2], m.n[2]);
+        const unsigned long long v = static_cast<unsigned long long>(i) +
+                                     static_cast<unsigned long long>(m.n[0]) * (j + static_cast<unsigned long long>(m.n[1]) * k);
+        sk[r] = (v << 32) | static_cast<unsigned long long>(r);
+    }
+    __syncthreads();
+    if (s_bad != ~0ull) {
+        if (tid == 0) *bad = s_bad;
+        return;
+    }
+    for (long long size = 2; size <= P; size <<= 1) // bitonic sort, ascending
+        for (long long stride = size >> 1; stride > 0; stride >>= 1) {
+            for (long long t = tid; t < P / 2; t += nt) {
+                const long long lo = 2 * t - (t & (stride - 1));
+                const long long hi = lo + stride;
+                const bool up = (lo & size) == 0;
+                const unsigned long long x = sk[lo], y = sk[hi];
+                if ((x > y) == up) {
+                    sk[lo] = y;
+                    sk[hi] = x;
+                }
+            }
+            __syncthreads();
+        }
+    // group flags + exclusive scan (each thread a contiguous run of `per` entries)
+    const long long per = (N + nt - 1) / nt, b = tid * per, e = min(N, b + per);
+    unsigned long long run = 0;
+    for (long long i = b; i < e; ++i) run += (i == 0 || (sk[i] >> 32) != (sk[i - 1] >> 32)) ? 1 : 0;
+    part[tid] = run;
+    __syncthreads();
+    for (int d = 1; d < nt; d <<= 1) {
+        const unsigned long long add = tid >= d ? part[tid - d] : 0;
+        __syncthreads();
+        part[tid] += add;
+        __syncthreads();
+    }
+    long long g = static_cast<long long>(part[tid] - run);
+    for (long long i = b; i < e; ++i) {
+        const long long key = static_cast<long long>(sk[i] >> 32);
+        const long long a = id_order[sk[i] & 0xffffffffull];
+        keys_sorted[i] = key;
+        order[i] = a;
+        if (i == 0 || key != static_cast<long long>(sk[i - 1] >> 32)) {
+            group_voxel[g] = key;
+            group_offsets[g] = i;
+            ++g;
+        }
+        if (S > 0) {
+            vol_g[i] = vol[a];
+            for (int s = 0; s < S; ++s) {
+                sec_g[i * S + s] = sec[a * S + s];
+                upt_g[i * S + s] = upt[a * S + s];
+                sat_g[i * S + s] = sat[a * S + s];
+            }
+        }
+    }
+    if (tid == nt - 1) {
+        const long long G = static_cast<long long>(part[nt - 1]);
+        group_offsets[G] = N;
+        counts[0] = G;
+        counts[1] = N;
+        rep_groups[0] = 0;
+        rep_groups[1] = G;
+        *bad = ~0ull;
+    }
+}
+
 int bits_for(long long v)
 {
     int b = 1;
@@ -310,6 +418,35 @@ void DeviceSession::rebuild_voxel_grouping()
     m.sentinel = m.key_span * replicas_;
     const int end_bit = bits_for(m.sentinel);
     if (!host_pin_) ck(cudaMallocHost(&host_pin_, 64), "cudaMallocHost"); // pinned: the two read-backs below
+    if (replicas_ == 1 && !agent_filter_ && N <= kSmallRegroup && m.nvox < (1LL << 31) &&
+        std::getenv("BIODIFF_REGROUP_CUB") == nullptr) { // one launch, one read-back
+        long long P = 1;
+        while (P < N) P <<= 1;
+        const int smem = static_cast<int>((P + 1024) * sizeof(unsigned long long));
+        ck(cudaFuncSetAttribute(regroup_small, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), "smem attr");
+        begin_kernel(kAux);
+        regroup_small<<<1, 1024, smem, st>>>(in_pos_, N, m, id_order_, S_, in_vol_, in_sec_, in_upt_, in_sat_,
+                                             keys_b_, vals_b_, group_voxel_, group_offsets_, agent_counts_,
+                                             rep_groups_, agent_volume_, agent_secretion_, agent_uptake_,
+                                             agent_saturation_, agent_bad_);
+        end_kernel(kAux);
+        auto* pin = static_cast<long long*>(host_pin_);
+        ck(cudaMemcpyAsync(pin, agent_bad_, sizeof(long long), cudaMemcpyDeviceToHost, st), "download");
+        ck(cudaMemcpyAsync(pin + 1, agent_counts_, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st), "download");
+        ck(cudaStreamSynchronize(st), "sync");
+        const unsigned long long bad = static_cast<unsigned long long>(pin[0]);
+        if (bad != ~0ull) {
+            double p[3];
+            ck(cudaMemcpy(p, in_pos_ + 3 * bad, sizeof(p), cudaMemcpyDeviceToHost), "download");
+            throw std::domain_error("position (" + format_double(p[0]) + "," + format_double(p[1]) + "," +
+                                    format_double(p[2]) + ") outside the simulation domain");
+        }
+        factors_valid_ = false;
+        res_grp_valid_ = false;
+        groups_ = pin[1];
+        grouped_agents_ = pin[2];
+        return;
+    }
     ck(cudaMemsetAsync(agent_bad_, 0xff, sizeof(unsigned long long), st), "reset"); // ~0: no agent outside
     const int block = 256;
     begin_kernel(kAux);
