@@ -115,7 +115,13 @@ private:
                 out += it->second;
             } else if (e.size() > 1 && e[0] == '#') {
                 const bool hex = e[1] == 'x' || e[1] == 'X';
-                out += static_cast<char>(std::stoul(e.substr(hex ? 2 : 1), nullptr, hex ? 16 : 10));
+                const std::string digits = e.substr(hex ? 2 : 1);
+                const bool ok = !digits.empty() && std::all_of(digits.begin(), digits.end(), [&](char ch) {
+                    return hex ? std::isxdigit(static_cast<unsigned char>(ch)) != 0
+                               : std::isdigit(static_cast<unsigned char>(ch)) != 0;
+                });
+                if (!ok || digits.size() > 6) bad_config("malformed XML: invalid character reference &" + e + ";");
+                out += static_cast<char>(std::stoul(digits, nullptr, hex ? 16 : 10));
             } else {
                 out += raw.substr(i, semi - i + 1);
             }
