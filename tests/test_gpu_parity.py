@@ -389,7 +389,7 @@ FUSED_ENVS = [
 
 @pytest.mark.parametrize("env", FUSED_ENVS, ids=["unfused", "fused", "lag1", "lagmax", "1cta", "slots2", "cluster",
                                                  "cluster2x3", "cluster4x8", "cluster16x1", "cluster_static"])
-@pytest.mark.parametrize("shape,S", SWEEP_SHAPES)
+@pytest.mark.parametrize("shape,S", SWEEP_SHAPES + [((36, 200, 5), 4), ((130, 160, 3), 2)])
 def test_fused_xy_step_bitwise(shape, S, env, monkeypatch):
     """The fused x+y kernel (ticketed items, per-plane release/acquire
     counters) gives the oracle's bits for full steps at every lag setting."""
