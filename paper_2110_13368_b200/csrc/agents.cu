@@ -159,6 +159,19 @@ __global__ void rep_group_bounds(const int64_t* group_voxel, const int64_t* coun
 // The densities each grouped agent senses (its cached voxel's values, the
 // reference's field.values[agent.voxel * S + s]) in input order; agents
 // outside this session's voxels (other z-slabs) keep the NaN fill.
+// Grid-stride copy of `count` doubles from a device-mapped host buffer
+// (16-byte aligned), 16 bytes per load.
+__global__ void copy_from_mapped(const double* __restrict__ src, double* __restrict__ dst, long long count)
+{
+    const long long pairs = count / 2;
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+    double2* d2 = reinterpret_cast<double2*>(dst);
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < pairs;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        d2[i] = s2[i];
+    if (count % 2 && blockIdx.x == 0 && threadIdx.x == 0) dst[count - 1] = src[count - 1];
+}
+
 __global__ void agent_sample(const int64_t* keys_sorted, const int64_t* order, const int64_t* counts, long long N,
                              int S, const double* rho, double* out)
 {
@@ -521,7 +534,23 @@ void DeviceSession::set_agent_positions(const double* xyz, std::int64_t n)
     if (n == 0) return;
     ck(cudaSetDevice(device_), "cudaSetDevice");
     auto st = static_cast<cudaStream_t>(stream_);
-    ck(cudaMemcpyAsync(in_pos_, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st), "upload positions");
+    // Page-locked, device-mapped caller buffers (cudaHostAlloc / pin_memory)
+    // are read by a copy kernel (zero-copy loads over PCIe) instead of a DMA
+    // copy: BIODIFF_ZC_POSITIONS=0 forces the DMA path.
+    cudaPointerAttributes attr{};
+    const bool mapped = zc_positions_ && cudaPointerGetAttributes(&attr, xyz) == cudaSuccess &&
+                        attr.type == cudaMemoryTypeHost && attr.devicePointer != nullptr &&
+                        reinterpret_cast<std::uintptr_t>(attr.devicePointer) % 16 == 0;
+    cudaGetLastError();
+    if (mapped) {
+        const long long pairs = (3 * n + 1) / 2;
+        begin_kernel(kAux);
+        copy_from_mapped<<<static_cast<unsigned>(std::min<long long>((pairs + 255) / 256, 4LL * sm_count_)), 256, 0,
+                           st>>>(static_cast<const double*>(attr.devicePointer), in_pos_, 3 * n);
+        end_kernel(kAux);
+    } else {
+        ck(cudaMemcpyAsync(in_pos_, xyz, sizeof(double) * 3 * n, cudaMemcpyHostToDevice, st), "upload positions");
+    }
     ck(cudaStreamSynchronize(st), "sync");
 }
 

@@ -182,6 +182,7 @@ DeviceSession::DeviceSession(const CartesianMesh& mesh, int substrates, int devi
     // graph replay: C1 28.2 -> 30.3 us, C2 49.3 -> 53.2 us per step, C3 no
     // change (the kernels' griddepcontrol.wait is a no-op without it).
     pdl_ = std::atoi(env_or("BIODIFF_PDL", "0")) != 0;
+    zc_positions_ = std::atoi(env_or("BIODIFF_ZC_POSITIONS", "1")) != 0;
     if (replicas_ > 1) { // L2 replica batches (step_body_batches)
         const double replica_mb = static_cast<double>(mesh.voxel_count()) * substrates * 8.0 / 1e6;
         const double budget = std::atof(env_or("BIODIFF_L2_BATCH_MB", "0")); // opt-in: measured slower (C5 latency-bound)

@@ -325,6 +325,7 @@ private:
     std::int64_t* agent_counts_ = nullptr; // [0] groups, [1] grouped agents (device)
     std::int64_t* rep_groups_ = nullptr;   // [R+1] first group of each replica (device)
     void* host_pin_ = nullptr;             // 64 pinned host bytes: the regrouping's read-backs
+    bool zc_positions_ = true;             // set_agent_positions reads mapped caller buffers by a kernel
     std::vector<std::int64_t> rep_agents_; // agents per replica (host)
     unsigned long long* agent_bad_ = nullptr;
     void* cub_tmp_ = nullptr;

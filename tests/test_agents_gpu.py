@@ -196,3 +196,29 @@ def test_sample_agent_densities_reads_each_agents_voxel():
     with pytest.raises(B.StateError):
         B._check(B.lib().biodiff_sample_agent_densities(s._h, B._dptr(np.zeros(3)), 3))
     s.close()
+
+
+@pytest.mark.parametrize("zero_copy", ["1", "0"])
+@pytest.mark.parametrize("n", [301, 2000])
+def test_positions_from_page_locked_buffers(zero_copy, n, monkeypatch):
+    """set_agent_positions from a page-locked, device-mapped caller buffer
+    (torch pin_memory = cudaHostAlloc) goes through the zero-copy kernel
+    (BIODIFF_ZC_POSITIONS=1, default) or the DMA copy; both give the
+    oracle's grouping, also from an 8-byte-offset view (DMA fallback) and for
+    odd value counts."""
+    import torch
+    monkeypatch.setenv("BIODIFF_ZC_POSITIONS", zero_copy)
+    w = W.make("t", (24, 20, 18), 2, n, 1, seed=n, immune_fraction=0.2)
+    s = make_session(w)
+    rng = np.random.default_rng(n)
+    for offset in (0, 1):
+        w.agent_pos = _move(rng, w)
+        buf = torch.empty(3 * n + 1, dtype=torch.float64).pin_memory()
+        view = buf.numpy()[offset:offset + 3 * n]
+        view[:] = w.agent_pos.reshape(-1)
+        s.set_agent_positions(view.reshape(n, 3))
+        s.rebuild_voxel_grouping()
+        gv, go, order = s.agent_grouping()
+        wv, wo, word = _oracle_grouping(w)
+        assert np.array_equal(gv, wv) and np.array_equal(go, wo) and np.array_equal(order, word)
+    s.close()
