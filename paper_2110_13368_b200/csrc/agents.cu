@@ -101,12 +101,24 @@ __global__ void group_flags(const int64_t* keys, long long N, long long sentinel
     flags[i] = keys[i] != sentinel && (i == 0 || keys[i] != keys[i - 1]) ? 1 : 0;
 }
 
+// The live grouping arrays are written only when no agent lies outside the
+// domain (bad == ~0): a failed rebuild leaves them as they were, without a
+// host round trip between the key pass and the writes.
+__global__ void group_reset(const unsigned long long* bad, int64_t* counts, int64_t* group_offsets)
+{
+    if (*bad != ~0ull) return;
+    counts[0] = 0;
+    counts[1] = 0;
+    group_offsets[0] = 0;
+}
+
 // counts[0] = groups, counts[1] = grouped agents (keys before the first sentinel).
 __global__ void group_write(const int64_t* keys, const int* flags, const int64_t* gidx, long long N,
-                            long long sentinel, int64_t* group_voxel, int64_t* group_offsets, int64_t* counts)
+                            long long sentinel, int64_t* group_voxel, int64_t* group_offsets, int64_t* counts,
+                            const unsigned long long* bad)
 {
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= N) return;
+    if (i >= N || *bad != ~0ull) return;
     if (flags[i]) {
         group_voxel[gidx[i]] = keys[i];
         group_offsets[gidx[i]] = i;
@@ -123,10 +135,10 @@ __global__ void group_write(const int64_t* keys, const int* flags, const int64_t
 
 __global__ void agent_gather(const int64_t* order, long long N, int S, const double* vol, const double* sec,
                              const double* upt, const double* sat, double* vol_g, double* sec_g, double* upt_g,
-                             double* sat_g)
+                             double* sat_g, const unsigned long long* bad)
 {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (t >= N * S) return;
+    if (t >= N * S || *bad != ~0ull) return;
     const long long i = t / S;
     const int s = static_cast<int>(t % S);
     const long long a = order[i];
@@ -139,10 +151,10 @@ __global__ void agent_gather(const int64_t* order, long long N, int S, const dou
 // rep_groups[r] = first group of replica r (groups are sorted by key, keys of
 // replica r start at r * key_span); rep_groups[R] = G.
 __global__ void rep_group_bounds(const int64_t* group_voxel, const int64_t* counts, long long key_span, int R,
-                                 int64_t* rep_groups)
+                                 int64_t* rep_groups, const unsigned long long* bad)
 {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
-    if (r > R) return;
+    if (r > R || *bad != ~0ull) return;
     const long long G = counts[0];
     const long long key = static_cast<long long>(r) * key_span;
     long long lo = 0, hi = G;
@@ -156,9 +168,6 @@ __global__ void rep_group_bounds(const int64_t* group_voxel, const int64_t* coun
     rep_groups[r] = r == R ? G : lo;
 }
 
-// The densities each grouped agent senses (its cached voxel's values, the
-// reference's field.values[agent.voxel * S + s]) in input order; agents
-// outside this session's voxels (other z-slabs) keep the NaN fill.
 // Grid-stride copy of `count` doubles from a device-mapped host buffer
 // (16-byte aligned), 16 bytes per load.
 __global__ void copy_from_mapped(const double* __restrict__ src, double* __restrict__ dst, long long count)
@@ -172,15 +181,18 @@ __global__ void copy_from_mapped(const double* __restrict__ src, double* __restr
     if (count % 2 && blockIdx.x == 0 && threadIdx.x == 0) dst[count - 1] = src[count - 1];
 }
 
+// The densities each grouped agent senses (its cached voxel's values, the
+// reference's field.values[agent.voxel * S + s]) in input order; agents
+// outside this session's voxels (other z-slabs) keep the NaN fill.
 __global__ void agent_sample(const int64_t* keys_sorted, const int64_t* order, const int64_t* counts, long long N,
                              int S, const double* rho, double* out)
 {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= N * S) return;
     const long long i = t / S;
-    if (i >= counts[1]) return;
     const int s = static_cast<int>(t % S);
-    out[order[i] * S + s] = rho[keys_sorted[i] * S + s];
+    // agents not grouped here (outside this z-slab) read NaN
+    out[order[i] * S + s] = i < counts[1] ? rho[keys_sorted[i] * S + s] : __longlong_as_double(-1LL);
 }
 
 // Small populations (one replica, no slab filter, N <= kSmallRegroup): the
@@ -304,7 +316,7 @@ unsigned blocks(long long n, int block) { return static_cast<unsigned>(std::max(
 
 void DeviceSession::release_agents()
 {
-    for (auto** p : {&in_ids_, &id_order_, &keys_a_, &keys_b_, &vals_b_, &scan_, &group_voxel_, &group_offsets_,
+    for (auto** p : {&in_ids_, &id_order_, &keys_a_, &keys_b_, &vals_b_, &keys_c_, &vals_c_, &scan_, &group_voxel_, &group_offsets_,
                      &agent_counts_, &rep_groups_})
         dfree(*p);
     for (auto** p : {&in_pos_, &in_vol_, &in_sec_, &in_upt_, &in_sat_, &agent_volume_, &agent_secretion_,
@@ -320,6 +332,7 @@ void DeviceSession::release_agents()
     groups_ = 0;
     grouped_agents_ = 0;
     res_grp_valid_ = false;
+    destroy_regroup_graphs();
     id_index_.clear();
     rep_agents_.clear();
 }
@@ -381,6 +394,8 @@ void DeviceSession::set_agents_multi(const std::vector<const AgentPopulation*>& 
     dalloc(keys_a_, N);
     dalloc(keys_b_, N);
     dalloc(vals_b_, N);
+    dalloc(keys_c_, N);
+    dalloc(vals_c_, N);
     dalloc(flags_, N);
     dalloc(scan_, N);
     dalloc(group_voxel_, N);
@@ -402,6 +417,14 @@ void DeviceSession::set_agents_multi(const std::vector<const AgentPopulation*>& 
     cub_bytes_ = std::max(sort_bytes, scan_bytes);
     ck(cudaMalloc(&cub_tmp_, cub_bytes_), "cudaMalloc cub");
     rebuild_voxel_grouping();
+}
+
+void DeviceSession::destroy_regroup_graphs()
+{
+    for (auto& g : regroup_graphs_) {
+        if (g.exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(g.exec));
+        g = RegroupGraph{};
+    }
 }
 
 void DeviceSession::rebuild_voxel_grouping()
@@ -460,18 +483,73 @@ void DeviceSession::rebuild_voxel_grouping()
         grouped_agents_ = pin[2];
         return;
     }
-    ck(cudaMemsetAsync(agent_bad_, 0xff, sizeof(unsigned long long), st), "reset"); // ~0: no agent outside
-    const int block = 256;
-    begin_kernel(kAux);
-    agent_keys<<<blocks(N, block), block, 0, st>>>(in_pos_, in_rep_, N, m, id_order_, keys_a_, agent_bad_);
-    end_kernel(kAux);
-    // The domain check comes before any group array is touched: a failed
-    // rebuild keeps the previous grouping, as the reference does (its
-    // nearest_voxel throws before groups_ is reassigned, agents.cpp:56-73).
-    auto* pin = static_cast<unsigned long long*>(host_pin_);
-    ck(cudaMemcpyAsync(pin, agent_bad_, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st), "download");
+    auto* pin = static_cast<long long*>(host_pin_);
+    auto issue = [&] {
+        ck(cudaMemsetAsync(agent_bad_, 0xff, sizeof(unsigned long long), st), "reset"); // ~0: no agent outside
+        const int block = 256;
+        begin_kernel(kAux);
+        agent_keys<<<blocks(N, block), block, 0, st>>>(in_pos_, in_rep_, N, m, id_order_, keys_a_, agent_bad_);
+        end_kernel(kAux);
+        // The sort goes to the spare (keys, order) pair and every write of a live
+        // array is conditional on the domain check (group_reset / group_write /
+        // agent_gather / rep_group_bounds skip when an agent is outside), so the
+        // pipeline runs with ONE read-back at its end; a failed rebuild keeps the
+        // previous grouping, as the reference does (its nearest_voxel throws
+        // before groups_ is reassigned, agents.cpp:56-73).
+        std::size_t bytes = cub_bytes_;
+        ck(cub::DeviceRadixSort::SortPairs(cub_tmp_, bytes, keys_a_, keys_c_, id_order_, vals_c_, N, 0, end_bit, st),
+           "cub sort");
+        begin_kernel(kAux);
+        group_flags<<<blocks(N, block), block, 0, st>>>(keys_c_, N, m.sentinel, flags_);
+        end_kernel(kAux);
+        bytes = cub_bytes_;
+        ck(cub::DeviceScan::ExclusiveSum(cub_tmp_, bytes, flags_, scan_, N, st), "cub scan");
+        begin_kernel(kAux);
+        group_reset<<<1, 1, 0, st>>>(agent_bad_, agent_counts_, group_offsets_);
+        end_kernel(kAux);
+        begin_kernel(kAux);
+        group_write<<<blocks(N, block), block, 0, st>>>(keys_c_, flags_, scan_, N, m.sentinel, group_voxel_,
+                                                        group_offsets_, agent_counts_, agent_bad_);
+        end_kernel(kAux);
+        begin_kernel(kAux);
+        agent_gather<<<blocks(N * S_, block), block, 0, st>>>(vals_c_, N, S_, in_vol_, in_sec_, in_upt_, in_sat_,
+                                                              agent_volume_, agent_secretion_, agent_uptake_,
+                                                              agent_saturation_, agent_bad_);
+        end_kernel(kAux);
+        begin_kernel(kAux);
+        rep_group_bounds<<<blocks(replicas_ + 1, block), block, 0, st>>>(group_voxel_, agent_counts_, m.key_span,
+                                                                          replicas_, rep_groups_, agent_bad_);
+        end_kernel(kAux);
+        ck(cudaMemcpyAsync(pin, agent_bad_, sizeof(long long), cudaMemcpyDeviceToHost, st), "download");
+        ck(cudaMemcpyAsync(pin + 1, agent_counts_, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st), "download");
+    };
+    // The pipeline is static for a population (sizes, buffers, mesh): it is
+    // captured once per sort-output buffer and replayed (one launch instead
+    // of ~12); kernel timing runs it eagerly.
+    const char* rg = std::getenv("BIODIFF_REGROUP_GRAPH");
+    if (!timing_ && (rg == nullptr || std::atoi(rg) != 0)) {
+        RegroupGraph& g = regroup_graphs_[keys_c_ < keys_b_ ? 0 : 1];
+        if (!g.exec || g.n != N || g.end_bit != end_bit || g.keys != keys_c_) {
+            if (g.exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(g.exec));
+            g.exec = nullptr;
+            const std::int64_t before = launches_;
+            cudaGraph_t graph;
+            ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "begin capture");
+            issue();
+            ck(cudaStreamEndCapture(st, &graph), "end capture");
+            cudaGraphExec_t exec;
+            ck(cudaGraphInstantiate(&exec, graph, 0), "graph instantiate");
+            cudaGraphDestroy(graph);
+            g = RegroupGraph{exec, N, end_bit, keys_c_, static_cast<int>(launches_ - before)};
+            launches_ = before;
+        }
+        ck(cudaGraphLaunch(static_cast<cudaGraphExec_t>(g.exec), st), "graph launch");
+        launches_ += g.kernels;
+    } else {
+        issue();
+    }
     ck(cudaStreamSynchronize(st), "sync");
-    const unsigned long long bad = pin[0];
+    const unsigned long long bad = static_cast<unsigned long long>(pin[0]);
     if (bad != ~0ull) {
         // mesh.cpp:74-76 (nearest_voxel's std::domain_error, same message).
         double p[3];
@@ -479,36 +557,12 @@ void DeviceSession::rebuild_voxel_grouping()
         throw std::domain_error("position (" + format_double(p[0]) + "," + format_double(p[1]) + "," +
                                 format_double(p[2]) + ") outside the simulation domain");
     }
-    ck(cudaMemsetAsync(agent_counts_, 0, 2 * sizeof(long long), st), "reset");
-    ck(cudaMemsetAsync(group_offsets_, 0, sizeof(long long), st), "reset");
-    std::size_t bytes = cub_bytes_;
-    ck(cub::DeviceRadixSort::SortPairs(cub_tmp_, bytes, keys_a_, keys_b_, id_order_, vals_b_, N, 0, end_bit, st),
-       "cub sort");
-    begin_kernel(kAux);
-    group_flags<<<blocks(N, block), block, 0, st>>>(keys_b_, N, m.sentinel, flags_);
-    end_kernel(kAux);
-    bytes = cub_bytes_;
-    ck(cub::DeviceScan::ExclusiveSum(cub_tmp_, bytes, flags_, scan_, N, st), "cub scan");
-    begin_kernel(kAux);
-    group_write<<<blocks(N, block), block, 0, st>>>(keys_b_, flags_, scan_, N, m.sentinel, group_voxel_,
-                                                    group_offsets_, agent_counts_);
-    end_kernel(kAux);
-    begin_kernel(kAux);
-    agent_gather<<<blocks(N * S_, block), block, 0, st>>>(vals_b_, N, S_, in_vol_, in_sec_, in_upt_, in_sat_,
-                                                          agent_volume_, agent_secretion_, agent_uptake_,
-                                                          agent_saturation_);
-    end_kernel(kAux);
-    begin_kernel(kAux);
-    rep_group_bounds<<<blocks(replicas_ + 1, block), block, 0, st>>>(group_voxel_, agent_counts_, m.key_span,
-                                                                      replicas_, rep_groups_);
-    end_kernel(kAux);
-    auto* counts = reinterpret_cast<long long*>(host_pin_) + 1;
-    ck(cudaMemcpyAsync(counts, agent_counts_, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st), "download");
-    ck(cudaStreamSynchronize(st), "sync");
+    std::swap(keys_b_, keys_c_);
+    std::swap(vals_b_, vals_c_);
     factors_valid_ = false;
     res_grp_valid_ = false;
-    groups_ = counts[0];
-    grouped_agents_ = counts[1];
+    groups_ = pin[1];
+    grouped_agents_ = pin[2];
 }
 
 void DeviceSession::sample_agent_densities(double* out, std::int64_t count)
@@ -518,7 +572,6 @@ void DeviceSession::sample_agent_densities(double* out, std::int64_t count)
     ck(cudaSetDevice(device_), "cudaSetDevice");
     auto st = static_cast<cudaStream_t>(stream_);
     if (!agent_sample_) dalloc(agent_sample_, count);
-    ck(cudaMemsetAsync(agent_sample_, 0xff, sizeof(double) * count, st), "memset"); // NaN
     const int block = 256;
     begin_kernel(kAux);
     agent_sample<<<blocks(count, block), block, 0, st>>>(keys_b_, vals_b_, agent_counts_, n_agents_, S_, rho_,

@@ -320,6 +320,18 @@ private:
     std::int64_t* keys_a_ = nullptr;
     std::int64_t* keys_b_ = nullptr;
     std::int64_t* vals_b_ = nullptr;   // agent indices in (voxel, id) order
+    std::int64_t* keys_c_ = nullptr;   // the next rebuild's sort output (swapped in when it succeeds)
+    std::int64_t* vals_c_ = nullptr;
+    // The CUB regrouping pipeline captured once per sort-output buffer.
+    struct RegroupGraph {
+        void* exec = nullptr;
+        std::int64_t n = -1;
+        int end_bit = -1;
+        std::int64_t* keys = nullptr;
+        int kernels = 0;
+    };
+    RegroupGraph regroup_graphs_[2];
+    void destroy_regroup_graphs();
     int* flags_ = nullptr;
     std::int64_t* scan_ = nullptr;
     std::int64_t* agent_counts_ = nullptr; // [0] groups, [1] grouped agents (device)
