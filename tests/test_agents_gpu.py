@@ -79,7 +79,15 @@ def test_moving_agents_full_run_bitwise():
     s.close()
 
 
-def test_set_position_by_id_and_errors():
+@pytest.mark.parametrize("path", ["one_cta", "cub_graph", "cub_eager"])
+def test_set_position_by_id_and_errors(path, monkeypatch):
+    """Every regrouping path (one-CTA sort; the CUB pipeline replayed as a
+    graph, or eagerly): a failed rebuild keeps the previous grouping, and a
+    later good one (same captured graph) replaces it."""
+    if path != "one_cta":
+        monkeypatch.setenv("BIODIFF_REGROUP_CUB", "1")
+    if path == "cub_eager":
+        monkeypatch.setenv("BIODIFF_REGROUP_GRAPH", "0")
     w = W.make("t", (20, 20, 20), 1, 100, 1, seed=3)
     s = make_session(w)
     aid = int(w.agent_ids[17])
@@ -105,6 +113,17 @@ def test_set_position_by_id_and_errors():
     s.set_agent_position(aid, p)
     s.rebuild_voxel_grouping()
     assert all(np.array_equal(a, b) for a, b in zip(s.agent_grouping(), _oracle_grouping(w)))
+    for k in range(3):  # alternate sort buffers, failures in between
+        w.agent_pos = _move(np.random.default_rng(k), w)
+        w.agent_pos[17] = p
+        s.set_agent_positions(w.agent_pos)
+        s.rebuild_voxel_grouping()
+        assert all(np.array_equal(a, b) for a, b in zip(s.agent_grouping(), _oracle_grouping(w)))
+        s.set_agent_position(aid, bad)
+        with pytest.raises(B.StateError, match=r"outside the simulation domain"):
+            s.rebuild_voxel_grouping()
+        assert all(np.array_equal(a, b) for a, b in zip(s.agent_grouping(), _oracle_grouping(w)))
+        s.set_agent_position(aid, p)
     s.close()
 
 
