@@ -66,6 +66,7 @@ def main(argv):
         "resident_dirichlet": ({"BIODIFF_RESIDENT": "1"}, wa, False),
         "dataflow": ({"BIODIFF_RESIDENT": "1", "BIODIFF_SMALL": "0"}, wa, False),
         "regroup": ({"BIODIFF_RESIDENT": "0"}, wc, True),
+        "regroup_cub": ({"BIODIFF_RESIDENT": "0", "BIODIFF_REGROUP_CUB": "1"}, wc, True),  # captured CUB pipeline
     }
     chosen = argv or list(cases) + ["xyz_cluster"]
     bad = 0
