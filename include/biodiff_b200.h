@@ -125,7 +125,11 @@ int biodiff_agent_grouping(biodiff_session* session, int64_t* groups, int64_t* g
  * grouping is stale until biodiff_rebuild_voxel_grouping (the reference's
  * contract: "the caller is expected to rebuild the voxel grouping before
  * the next reaction step").
- *   set_agent_positions : all n positions, xyz[3n] host, agent-index order
+ *   set_agent_positions : all n positions, xyz[3n] host, agent-index order;
+ *                         synchronous (the buffer may be reused on return).
+ *                         A page-locked, device-mapped buffer (cudaHostAlloc,
+ *                         torch pin_memory), 16-byte aligned, is read by a
+ *                         zero-copy kernel, any other buffer by a DMA copy
  *   set_agent_position  : AgentPopulation::set_position(id, p) (agents.cpp:45-54);
  *                         status 2 "no agent with id" if absent
  *   agent_positions_device: the device xyz[3n] buffer (stream-ordered with
