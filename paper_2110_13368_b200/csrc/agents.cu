@@ -425,6 +425,7 @@ void DeviceSession::destroy_regroup_graphs()
         if (g.exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(g.exec));
         g = RegroupGraph{};
     }
+    sort_parity_ = 0;
 }
 
 void DeviceSession::rebuild_voxel_grouping()
@@ -528,7 +529,7 @@ void DeviceSession::rebuild_voxel_grouping()
     // of ~12); kernel timing runs it eagerly.
     const char* rg = std::getenv("BIODIFF_REGROUP_GRAPH");
     if (!timing_ && (rg == nullptr || std::atoi(rg) != 0)) {
-        RegroupGraph& g = regroup_graphs_[keys_c_ < keys_b_ ? 0 : 1];
+        RegroupGraph& g = regroup_graphs_[sort_parity_];
         if (!g.exec || g.n != N || g.end_bit != end_bit || g.keys != keys_c_) {
             if (g.exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(g.exec));
             g.exec = nullptr;
@@ -558,6 +559,7 @@ void DeviceSession::rebuild_voxel_grouping()
                                 format_double(p[2]) + ") outside the simulation domain");
     }
     std::swap(keys_b_, keys_c_);
+    sort_parity_ ^= 1;
     std::swap(vals_b_, vals_c_);
     factors_valid_ = false;
     res_grp_valid_ = false;

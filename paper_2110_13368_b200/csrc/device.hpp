@@ -331,6 +331,7 @@ private:
         int kernels = 0;
     };
     RegroupGraph regroup_graphs_[2];
+    int sort_parity_ = 0; // which of the two sort-output pairs keys_c_ / vals_c_ is (its graph slot)
     void destroy_regroup_graphs();
     int* flags_ = nullptr;
     std::int64_t* scan_ = nullptr;
