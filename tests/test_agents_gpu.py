@@ -241,3 +241,25 @@ def test_positions_from_page_locked_buffers(zero_copy, n, monkeypatch):
         wv, wo, word = _oracle_grouping(w)
         assert np.array_equal(gv, wv) and np.array_equal(go, wo) and np.array_equal(order, word)
     s.close()
+
+
+def test_regroup_graph_across_populations_and_timing(monkeypatch):
+    """The captured CUB regrouping pipeline is per population: a new
+    set_agents (another size) re-captures it, and kernel timing (eager
+    pipeline) in between gives the same grouping."""
+    monkeypatch.setenv("BIODIFF_REGROUP_CUB", "1")
+    w = W.make("t", (24, 20, 18), 2, 900, 1, seed=21, immune_fraction=0.2)
+    s = make_session(w)
+    rng = np.random.default_rng(21)
+    for n, timing in ((900, False), (1500, True), (700, False)):
+        w2 = W.make("t", (24, 20, 18), 2, n, 1, seed=n, immune_fraction=0.3)
+        s.set_agents(w2.agent_ids, w2.agent_pos, w2.agent_vol, w2.agent_sec, w2.agent_upt, w2.agent_sat)
+        s.set_kernel_timing(timing)
+        for _ in range(3):
+            w2.agent_pos = _move(rng, w2)
+            s.set_agent_positions(w2.agent_pos)
+            s.rebuild_voxel_grouping()
+            gv, go, order = s.agent_grouping()
+            wv, wo, word = _oracle_grouping(w2)
+            assert np.array_equal(gv, wv) and np.array_equal(go, wo) and np.array_equal(order, word)
+    s.close()
