@@ -151,9 +151,14 @@ __global__ void agent_gather(const int64_t* order, long long N, int S, const dou
 // rep_groups[r] = first group of replica r (groups are sorted by key, keys of
 // replica r start at r * key_span); rep_groups[R] = G.
 __global__ void rep_group_bounds(const int64_t* group_voxel, const int64_t* counts, long long key_span, int R,
-                                 int64_t* rep_groups, const unsigned long long* bad)
+                                 int64_t* rep_groups, const unsigned long long* bad, long long* host_out)
 {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r == 0 && host_out) { // [bad, groups, grouped agents] straight to the page-locked host buffer
+        host_out[0] = static_cast<long long>(*bad);
+        host_out[1] = counts[0];
+        host_out[2] = counts[1];
+    }
     if (r > R || *bad != ~0ull) return;
     const long long G = counts[0];
     const long long key = static_cast<long long>(r) * key_span;
@@ -210,8 +215,10 @@ __global__ void __launch_bounds__(1024) regroup_small(const double* pos, long lo
                                                       int64_t* keys_sorted, int64_t* order, int64_t* group_voxel,
                                                       int64_t* group_offsets, int64_t* counts, int64_t* rep_groups,
                                                       double* vol_g, double* sec_g, double* upt_g, double* sat_g,
-                                                      unsigned long long* bad)
+                                                      unsigned long long* bad, long long* host_out)
 {
+    // host_out (page-locked, device-mapped, or nullptr): [bad, groups,
+    // grouped agents] written straight to the host — no read-back copies.
     extern __shared__ unsigned long long sk[]; // [P] packed keys, then [1024] scan partials
     __shared__ unsigned long long s_bad;
     const int tid = threadIdx.x, nt = blockDim.x;
@@ -243,7 +250,10 @@ __global__ void __launch_bounds__(1024) regroup_small(const double* pos, long lo
     }
     __syncthreads();
     if (s_bad != ~0ull) {
-        if (tid == 0) *bad = s_bad;
+        if (tid == 0) {
+            *bad = s_bad;
+            if (host_out) host_out[0] = static_cast<long long>(s_bad);
+        }
         return;
     }
     for (long long size = 2; size <= P; size <<= 1) // bitonic sort, ascending
@@ -300,6 +310,11 @@ __global__ void __launch_bounds__(1024) regroup_small(const double* pos, long lo
         rep_groups[0] = 0;
         rep_groups[1] = G;
         *bad = ~0ull;
+        if (host_out) {
+            host_out[0] = -1; // ~0: no agent outside
+            host_out[1] = G;
+            host_out[2] = N;
+        }
     }
 }
 
@@ -455,6 +470,13 @@ void DeviceSession::rebuild_voxel_grouping()
     m.sentinel = m.key_span * replicas_;
     const int end_bit = bits_for(m.sentinel);
     if (!host_pin_) ck(cudaMallocHost(&host_pin_, 64), "cudaMallocHost"); // pinned: the two read-backs below
+    // The read-back buffer is device-mapped (UVA): the last kernel of the
+    // pipeline writes it directly, no copies.
+    long long* pin_dev = nullptr;
+    if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&pin_dev), host_pin_, 0) != cudaSuccess) {
+        cudaGetLastError();
+        pin_dev = nullptr;
+    }
     if (replicas_ == 1 && !agent_filter_ && N <= kSmallRegroup && m.nvox < (1LL << 31) &&
         std::getenv("BIODIFF_REGROUP_CUB") == nullptr) { // one launch, one read-back
         long long P = 1;
@@ -465,11 +487,13 @@ void DeviceSession::rebuild_voxel_grouping()
         regroup_small<<<1, 1024, smem, st>>>(in_pos_, N, m, id_order_, S_, in_vol_, in_sec_, in_upt_, in_sat_,
                                              keys_b_, vals_b_, group_voxel_, group_offsets_, agent_counts_,
                                              rep_groups_, agent_volume_, agent_secretion_, agent_uptake_,
-                                             agent_saturation_, agent_bad_);
+                                             agent_saturation_, agent_bad_, pin_dev);
         end_kernel(kAux);
         auto* pin = static_cast<long long*>(host_pin_);
-        ck(cudaMemcpyAsync(pin, agent_bad_, sizeof(long long), cudaMemcpyDeviceToHost, st), "download");
-        ck(cudaMemcpyAsync(pin + 1, agent_counts_, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st), "download");
+        if (!pin_dev) {
+            ck(cudaMemcpyAsync(pin, agent_bad_, sizeof(long long), cudaMemcpyDeviceToHost, st), "download");
+            ck(cudaMemcpyAsync(pin + 1, agent_counts_, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st), "download");
+        }
         ck(cudaStreamSynchronize(st), "sync");
         const unsigned long long bad = static_cast<unsigned long long>(pin[0]);
         if (bad != ~0ull) {
@@ -519,10 +543,12 @@ void DeviceSession::rebuild_voxel_grouping()
         end_kernel(kAux);
         begin_kernel(kAux);
         rep_group_bounds<<<blocks(replicas_ + 1, block), block, 0, st>>>(group_voxel_, agent_counts_, m.key_span,
-                                                                          replicas_, rep_groups_, agent_bad_);
+                                                                          replicas_, rep_groups_, agent_bad_, pin_dev);
         end_kernel(kAux);
-        ck(cudaMemcpyAsync(pin, agent_bad_, sizeof(long long), cudaMemcpyDeviceToHost, st), "download");
-        ck(cudaMemcpyAsync(pin + 1, agent_counts_, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st), "download");
+        if (!pin_dev) {
+            ck(cudaMemcpyAsync(pin, agent_bad_, sizeof(long long), cudaMemcpyDeviceToHost, st), "download");
+            ck(cudaMemcpyAsync(pin + 1, agent_counts_, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st), "download");
+        }
     };
     // The pipeline is static for a population (sizes, buffers, mesh): it is
     // captured once per sort-output buffer and replayed (one launch instead
