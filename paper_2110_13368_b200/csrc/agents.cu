@@ -135,14 +135,17 @@ __global__ void group_write(const int64_t* keys, const int* flags, const int64_t
 
 __global__ void agent_gather(const int64_t* order, long long N, int S, const double* vol, const double* sec,
                              const double* upt, const double* sat, double* vol_g, double* sec_g, double* upt_g,
-                             double* sat_g, const unsigned long long* bad)
+                             double* sat_g, const unsigned long long* bad, int64_t* rank)
 {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= N * S || *bad != ~0ull) return;
     const long long i = t / S;
     const int s = static_cast<int>(t % S);
     const long long a = order[i];
-    if (s == 0) vol_g[i] = vol[a];
+    if (s == 0) {
+        vol_g[i] = vol[a];
+        rank[a] = i; // inverse of the (voxel, id) order: agent -> sorted position
+    }
     sec_g[t] = sec[a * S + s];
     upt_g[t] = upt[a * S + s];
     sat_g[t] = sat[a * S + s];
@@ -186,18 +189,19 @@ __global__ void copy_from_mapped(const double* __restrict__ src, double* __restr
     if (count % 2 && blockIdx.x == 0 && threadIdx.x == 0) dst[count - 1] = src[count - 1];
 }
 
-// The densities each grouped agent senses (its cached voxel's values, the
-// reference's field.values[agent.voxel * S + s]) in input order; agents
-// outside this session's voxels (other z-slabs) keep the NaN fill.
-__global__ void agent_sample(const int64_t* keys_sorted, const int64_t* order, const int64_t* counts, long long N,
+// The densities each agent senses (its cached voxel's values, the
+// reference's field.values[agent.voxel * S + s]), in agent-index order:
+// thread (a, s) looks up a's sorted position, so the output is written
+// contiguously (into a device buffer, or straight into a mapped host
+// buffer). Agents outside this session's voxels (other z-slabs) read NaN.
+__global__ void agent_sample(const int64_t* keys_sorted, const int64_t* rank, const int64_t* counts, long long N,
                              int S, const double* rho, double* out)
 {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= N * S) return;
-    const long long i = t / S;
+    const long long i = rank[t / S];
     const int s = static_cast<int>(t % S);
-    // agents not grouped here (outside this z-slab) read NaN
-    out[order[i] * S + s] = i < counts[1] ? rho[keys_sorted[i] * S + s] : __longlong_as_double(-1LL);
+    out[t] = i < counts[1] ? rho[keys_sorted[i] * S + s] : __longlong_as_double(-1LL);
 }
 
 // Small populations (one replica, no slab filter, N <= kSmallRegroup): the
@@ -215,7 +219,7 @@ __global__ void __launch_bounds__(1024) regroup_small(const double* pos, long lo
                                                       int64_t* keys_sorted, int64_t* order, int64_t* group_voxel,
                                                       int64_t* group_offsets, int64_t* counts, int64_t* rep_groups,
                                                       double* vol_g, double* sec_g, double* upt_g, double* sat_g,
-                                                      unsigned long long* bad, long long* host_out)
+                                                      unsigned long long* bad, long long* host_out, int64_t* rank)
 {
     // host_out (page-locked, device-mapped, or nullptr): [bad, groups,
     // grouped agents] written straight to the host — no read-back copies.
@@ -288,6 +292,7 @@ __global__ void __launch_bounds__(1024) regroup_small(const double* pos, long lo
         const long long a = id_order[sk[i] & 0xffffffffull];
         keys_sorted[i] = key;
         order[i] = a;
+        rank[a] = i;
         if (i == 0 || key != static_cast<long long>(sk[i - 1] >> 32)) {
             group_voxel[g] = key;
             group_offsets[g] = i;
@@ -331,7 +336,7 @@ unsigned blocks(long long n, int block) { return static_cast<unsigned>(std::max(
 
 void DeviceSession::release_agents()
 {
-    for (auto** p : {&in_ids_, &id_order_, &keys_a_, &keys_b_, &vals_b_, &keys_c_, &vals_c_, &scan_, &group_voxel_, &group_offsets_,
+    for (auto** p : {&in_ids_, &id_order_, &keys_a_, &keys_b_, &vals_b_, &keys_c_, &vals_c_, &agent_rank_, &scan_, &group_voxel_, &group_offsets_,
                      &agent_counts_, &rep_groups_})
         dfree(*p);
     for (auto** p : {&in_pos_, &in_vol_, &in_sec_, &in_upt_, &in_sat_, &agent_volume_, &agent_secretion_,
@@ -411,6 +416,7 @@ void DeviceSession::set_agents_multi(const std::vector<const AgentPopulation*>& 
     dalloc(vals_b_, N);
     dalloc(keys_c_, N);
     dalloc(vals_c_, N);
+    dalloc(agent_rank_, N);
     dalloc(flags_, N);
     dalloc(scan_, N);
     dalloc(group_voxel_, N);
@@ -487,7 +493,7 @@ void DeviceSession::rebuild_voxel_grouping()
         regroup_small<<<1, 1024, smem, st>>>(in_pos_, N, m, id_order_, S_, in_vol_, in_sec_, in_upt_, in_sat_,
                                              keys_b_, vals_b_, group_voxel_, group_offsets_, agent_counts_,
                                              rep_groups_, agent_volume_, agent_secretion_, agent_uptake_,
-                                             agent_saturation_, agent_bad_, pin_dev);
+                                             agent_saturation_, agent_bad_, pin_dev, agent_rank_);
         end_kernel(kAux);
         auto* pin = static_cast<long long*>(host_pin_);
         if (!pin_dev) {
@@ -539,7 +545,7 @@ void DeviceSession::rebuild_voxel_grouping()
         begin_kernel(kAux);
         agent_gather<<<blocks(N * S_, block), block, 0, st>>>(vals_c_, N, S_, in_vol_, in_sec_, in_upt_, in_sat_,
                                                               agent_volume_, agent_secretion_, agent_uptake_,
-                                                              agent_saturation_, agent_bad_);
+                                                              agent_saturation_, agent_bad_, agent_rank_);
         end_kernel(kAux);
         begin_kernel(kAux);
         rep_group_bounds<<<blocks(replicas_ + 1, block), block, 0, st>>>(group_voxel_, agent_counts_, m.key_span,
@@ -599,13 +605,22 @@ void DeviceSession::sample_agent_densities(double* out, std::int64_t count)
     if (count == 0) return;
     ck(cudaSetDevice(device_), "cudaSetDevice");
     auto st = static_cast<cudaStream_t>(stream_);
-    if (!agent_sample_) dalloc(agent_sample_, count);
+    // A page-locked, device-mapped caller buffer is written by the kernel
+    // directly (contiguous 8-byte stores over PCIe); any other buffer gets a
+    // device buffer and one copy.
+    cudaPointerAttributes attr{};
+    const bool mapped = zc_positions_ && cudaPointerGetAttributes(&attr, out) == cudaSuccess &&
+                        attr.type == cudaMemoryTypeHost && attr.devicePointer != nullptr;
+    cudaGetLastError();
+    if (!mapped && !agent_sample_) dalloc(agent_sample_, count);
+    double* dst = mapped ? static_cast<double*>(attr.devicePointer) : agent_sample_;
     const int block = 256;
     begin_kernel(kAux);
-    agent_sample<<<blocks(count, block), block, 0, st>>>(keys_b_, vals_b_, agent_counts_, n_agents_, S_, rho_,
-                                                         agent_sample_);
+    agent_sample<<<blocks(count, block), block, 0, st>>>(keys_b_, agent_rank_, agent_counts_, n_agents_, S_, rho_,
+                                                         dst);
     end_kernel(kAux);
-    ck(cudaMemcpyAsync(out, agent_sample_, sizeof(double) * count, cudaMemcpyDeviceToHost, st), "download");
+    if (!mapped)
+        ck(cudaMemcpyAsync(out, agent_sample_, sizeof(double) * count, cudaMemcpyDeviceToHost, st), "download");
     ck(cudaStreamSynchronize(st), "sync");
 }
 

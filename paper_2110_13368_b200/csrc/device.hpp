@@ -322,6 +322,7 @@ private:
     std::int64_t* vals_b_ = nullptr;   // agent indices in (voxel, id) order
     std::int64_t* keys_c_ = nullptr;   // the next rebuild's sort output (swapped in when it succeeds)
     std::int64_t* vals_c_ = nullptr;
+    std::int64_t* agent_rank_ = nullptr; // agent -> position in (voxel, id) order (the density gather)
     // The CUB regrouping pipeline captured once per sort-output buffer.
     struct RegroupGraph {
         void* exec = nullptr;
@@ -338,7 +339,7 @@ private:
     std::int64_t* agent_counts_ = nullptr; // [0] groups, [1] grouped agents (device)
     std::int64_t* rep_groups_ = nullptr;   // [R+1] first group of each replica (device)
     void* host_pin_ = nullptr;             // 64 pinned host bytes: the regrouping's read-backs
-    bool zc_positions_ = true;             // set_agent_positions reads mapped caller buffers by a kernel
+    bool zc_positions_ = true;             // mapped caller buffers: positions read / densities written by kernels
     std::vector<std::int64_t> rep_agents_; // agents per replica (host)
     unsigned long long* agent_bad_ = nullptr;
     void* cub_tmp_ = nullptr;

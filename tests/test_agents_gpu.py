@@ -190,15 +190,34 @@ def test_zslab_agents_cross_slabs():
         w.agent_pos = pos
     total = sum(s.agent_grouping()[1][-1] for s in g.sessions)
     assert total == w.n_agents  # each agent grouped by exactly one slab
+    # what each slab's agents sense: their voxel's values; the others NaN —
+    # together exactly the single domain's samples
+    want = single.sample_agent_densities()
+    merged = np.full_like(want, np.nan)
+    for sl in g.sessions:
+        got = sl.sample_agent_densities()
+        own = ~np.isnan(got)
+        assert not np.any(own & ~np.isnan(merged))  # no agent sampled by two slabs
+        merged[own] = got[own]
+    d = np.abs(merged - want) / np.maximum(np.abs(want), 1e-290)
+    assert d.max() <= 1e-13
     g.close()
     single.close()
 
 
-def test_sample_agent_densities_reads_each_agents_voxel():
+@pytest.mark.parametrize("n,buf,zc", [(400, "pageable", "1"), (400, "pinned", "1"), (3000, "pinned", "1"),
+                                       (3000, "pinned", "0"), (3000, "pageable", "1")])
+def test_sample_agent_densities_reads_each_agents_voxel(n, buf, zc, monkeypatch):
     """What each agent senses: field.values[agent.voxel * S + s] (agents.hpp:22,
-    mesh.hpp:62-90), in agent-index order, after steps and after a move."""
-    w = W.make("t", (20, 18, 16), 2, 400, 1, seed=4, immune_fraction=0.3)
+    mesh.hpp:62-90), in agent-index order, after steps and after a move; the
+    one-CTA and CUB regroupings (n), into pageable or page-locked mapped
+    buffers (written by the gather kernel directly unless
+    BIODIFF_ZC_POSITIONS=0)."""
+    import torch
+    monkeypatch.setenv("BIODIFF_ZC_POSITIONS", zc)
+    w = W.make("t", (20, 18, 16), 2, n, 1, seed=4, immune_fraction=0.3)
     s = make_session(w)
+    out = torch.empty((n, w.S), dtype=torch.float64).pin_memory().numpy() if buf == "pinned" else None
     rng = np.random.default_rng(2)
     for _ in range(2):
         s.advance(5, w.dt)
@@ -207,7 +226,7 @@ def test_sample_agent_densities_reads_each_agents_voxel():
         vox = np.empty(w.n_agents, np.int64)
         for g in range(gv.size):
             vox[order[go[g]:go[g + 1]]] = gv[g]
-        got = s.sample_agent_densities()
+        got = s.sample_agent_densities(out)
         assert bits_equal(got, f[vox])
         w.agent_pos = _move(rng, w)
         s.set_agent_positions(w.agent_pos)
