@@ -142,7 +142,9 @@ int biodiff_agent_grouping(biodiff_session* session, int64_t* groups, int64_t* g
  *                         its cached voxel (field.values[agent.voxel*S + s],
  *                         mesh.hpp:62-90, agents.hpp:22) — into host
  *                         out[n*S] in agent-index order; agents outside this
- *                         session's voxels (other z-slabs) read NaN. */
+ *                         session's voxels (other z-slabs) read NaN. A
+ *                         page-locked, device-mapped `out` is written by the
+ *                         gather kernel directly; synchronous either way. */
 int biodiff_agent_count(biodiff_session* session, int64_t* n);
 int biodiff_set_agent_positions(biodiff_session* session, const double* xyz, int64_t n);
 int biodiff_set_agent_position(biodiff_session* session, int64_t id, const double* xyz);
