@@ -133,22 +133,42 @@ __global__ void group_write(const int64_t* keys, const int* flags, const int64_t
     }
 }
 
+// Per-agent source factors of one (agent, substrate) for step dt — the
+// expressions of sources_factors (kernels.cuh), computed in the gather so a
+// regrouping leaves them ready (fac.add == nullptr: not computed here).
+struct FactorOut {
+    double* add;
+    double* den;
+    double dt;
+    double inv_voxel_volume;
+};
+__device__ __forceinline__ void gather_factors(const FactorOut& fo, long long t, double volume, double sec, double upt,
+                                               double sat)
+{
+    const double f = __dmul_rn(__dmul_rn(fo.dt, volume), fo.inv_voxel_volume);
+    fo.add[t] = __dmul_rn(__dmul_rn(f, sec), sat);
+    fo.den[t] = __dadd_rn(1.0, __dmul_rn(f, __dadd_rn(sec, upt)));
+}
+
 __global__ void agent_gather(const int64_t* order, long long N, int S, const double* vol, const double* sec,
                              const double* upt, const double* sat, double* vol_g, double* sec_g, double* upt_g,
-                             double* sat_g, const unsigned long long* bad, int64_t* rank)
+                             double* sat_g, const unsigned long long* bad, int64_t* rank, FactorOut fo)
 {
     const long long t = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
     if (t >= N * S || *bad != ~0ull) return;
     const long long i = t / S;
     const int s = static_cast<int>(t % S);
     const long long a = order[i];
+    const double v = vol[a];
     if (s == 0) {
-        vol_g[i] = vol[a];
+        vol_g[i] = v;
         rank[a] = i; // inverse of the (voxel, id) order: agent -> sorted position
     }
-    sec_g[t] = sec[a * S + s];
-    upt_g[t] = upt[a * S + s];
-    sat_g[t] = sat[a * S + s];
+    const double se = sec[a * S + s], up = upt[a * S + s], sa = sat[a * S + s];
+    sec_g[t] = se;
+    upt_g[t] = up;
+    sat_g[t] = sa;
+    if (fo.add) gather_factors(fo, t, v, se, up, sa);
 }
 
 // rep_groups[r] = first group of replica r (groups are sorted by key, keys of
@@ -219,7 +239,8 @@ __global__ void __launch_bounds__(1024) regroup_small(const double* pos, long lo
                                                       int64_t* keys_sorted, int64_t* order, int64_t* group_voxel,
                                                       int64_t* group_offsets, int64_t* counts, int64_t* rep_groups,
                                                       double* vol_g, double* sec_g, double* upt_g, double* sat_g,
-                                                      unsigned long long* bad, long long* host_out, int64_t* rank)
+                                                      unsigned long long* bad, long long* host_out, int64_t* rank,
+                                                      FactorOut fo)
 {
     // host_out (page-locked, device-mapped, or nullptr): [bad, groups,
     // grouped agents] written straight to the host — no read-back copies.
@@ -299,11 +320,14 @@ __global__ void __launch_bounds__(1024) regroup_small(const double* pos, long lo
             ++g;
         }
         if (S > 0) {
-            vol_g[i] = vol[a];
+            const double v = vol[a];
+            vol_g[i] = v;
             for (int s = 0; s < S; ++s) {
-                sec_g[i * S + s] = sec[a * S + s];
-                upt_g[i * S + s] = upt[a * S + s];
-                sat_g[i * S + s] = sat[a * S + s];
+                const double se = sec[a * S + s], up = upt[a * S + s], sa = sat[a * S + s];
+                sec_g[i * S + s] = se;
+                upt_g[i * S + s] = up;
+                sat_g[i * S + s] = sa;
+                if (fo.add) gather_factors(fo, i * S + s, v, se, up, sa);
             }
         }
     }
@@ -353,6 +377,7 @@ void DeviceSession::release_agents()
     grouped_agents_ = 0;
     res_grp_valid_ = false;
     destroy_regroup_graphs();
+    sort_parity_ = 0; // the sort buffers are freed with the population
     id_index_.clear();
     rep_agents_.clear();
 }
@@ -440,13 +465,20 @@ void DeviceSession::set_agents_multi(const std::vector<const AgentPopulation*>& 
     rebuild_voxel_grouping();
 }
 
+// After a successful rebuild: the factors the gather wrote (for dt_) are
+// current; else they must be recomputed before the next sources step.
+void DeviceSession::mark_factors(bool computed)
+{
+    factors_valid_ = computed;
+    if (computed) std::memcpy(&factors_dt_bits_, &dt_, sizeof(factors_dt_bits_));
+}
+
 void DeviceSession::destroy_regroup_graphs()
 {
     for (auto& g : regroup_graphs_) {
         if (g.exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(g.exec));
         g = RegroupGraph{};
     }
-    sort_parity_ = 0;
 }
 
 void DeviceSession::rebuild_voxel_grouping()
@@ -483,6 +515,10 @@ void DeviceSession::rebuild_voxel_grouping()
         cudaGetLastError();
         pin_dev = nullptr;
     }
+    // The source factors for the session's dt come out of the gather (the
+    // step would otherwise recompute them after every regrouping).
+    const bool with_factors = dt_ > 0.0;
+    const FactorOut fo{with_factors ? agent_add_ : nullptr, agent_den_, dt_, 1.0 / mesh_.voxel_volume()};
     if (replicas_ == 1 && !agent_filter_ && N <= kSmallRegroup && m.nvox < (1LL << 31) &&
         std::getenv("BIODIFF_REGROUP_CUB") == nullptr) { // one launch, one read-back
         long long P = 1;
@@ -493,7 +529,7 @@ void DeviceSession::rebuild_voxel_grouping()
         regroup_small<<<1, 1024, smem, st>>>(in_pos_, N, m, id_order_, S_, in_vol_, in_sec_, in_upt_, in_sat_,
                                              keys_b_, vals_b_, group_voxel_, group_offsets_, agent_counts_,
                                              rep_groups_, agent_volume_, agent_secretion_, agent_uptake_,
-                                             agent_saturation_, agent_bad_, pin_dev, agent_rank_);
+                                             agent_saturation_, agent_bad_, pin_dev, agent_rank_, fo);
         end_kernel(kAux);
         auto* pin = static_cast<long long*>(host_pin_);
         if (!pin_dev) {
@@ -508,7 +544,7 @@ void DeviceSession::rebuild_voxel_grouping()
             throw std::domain_error("position (" + format_double(p[0]) + "," + format_double(p[1]) + "," +
                                     format_double(p[2]) + ") outside the simulation domain");
         }
-        factors_valid_ = false;
+        mark_factors(with_factors);
         res_grp_valid_ = false;
         groups_ = pin[1];
         grouped_agents_ = pin[2];
@@ -545,7 +581,7 @@ void DeviceSession::rebuild_voxel_grouping()
         begin_kernel(kAux);
         agent_gather<<<blocks(N * S_, block), block, 0, st>>>(vals_c_, N, S_, in_vol_, in_sec_, in_upt_, in_sat_,
                                                               agent_volume_, agent_secretion_, agent_uptake_,
-                                                              agent_saturation_, agent_bad_, agent_rank_);
+                                                              agent_saturation_, agent_bad_, agent_rank_, fo);
         end_kernel(kAux);
         begin_kernel(kAux);
         rep_group_bounds<<<blocks(replicas_ + 1, block), block, 0, st>>>(group_voxel_, agent_counts_, m.key_span,
@@ -593,7 +629,7 @@ void DeviceSession::rebuild_voxel_grouping()
     std::swap(keys_b_, keys_c_);
     sort_parity_ ^= 1;
     std::swap(vals_b_, vals_c_);
-    factors_valid_ = false;
+    mark_factors(with_factors);
     res_grp_valid_ = false;
     groups_ = pin[1];
     grouped_agents_ = pin[2];

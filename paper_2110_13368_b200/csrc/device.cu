@@ -386,6 +386,7 @@ void DeviceSession::invalidate_graphs()
 {
     for (auto& g : graphs_) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(g.second.first));
     graphs_.clear();
+    destroy_regroup_graphs(); // they carry dt and the mesh (source factors in the gather)
 }
 
 void DeviceSession::set_workspace(Axis axis, int n, int dims, double dt, const double* q, const double* dinv,

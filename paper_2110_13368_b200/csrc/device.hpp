@@ -334,6 +334,7 @@ private:
     RegroupGraph regroup_graphs_[2];
     int sort_parity_ = 0; // which of the two sort-output pairs keys_c_ / vals_c_ is (its graph slot)
     void destroy_regroup_graphs();
+    void mark_factors(bool computed);
     int* flags_ = nullptr;
     std::int64_t* scan_ = nullptr;
     std::int64_t* agent_counts_ = nullptr; // [0] groups, [1] grouped agents (device)
